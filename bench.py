@@ -1,0 +1,383 @@
+"""Benchmark of the WADG RHS + LSRK45 path (BASELINE.json metric: DOF-updates
+per second per RK stage, GDOF/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4]
+                    [--impl wadg|reference]
+
+A "step" is one full LSRK45 time step (5 RK stages, each = volume + surface
++ fused WADG-update/axpy kernel) over the whole mesh.  value = (d+1) K Np x 5
+x steps / device time, summed over ranks (max-over-ranks time).
+
+Default workload (N=1): BASELINE config 4 — warped Kuhn cube 64^3 x 6 =
+1,572,864 tets, N = 4, fp32, c^2 = 1 + 0.5 sin(2 pi x) sin(2 pi y) sin(2 pi z)
+folded into the WADG update weights, Gaussian pulse, strong-weak form.
+Inputs (fields 0.9 GB, geometry 9.9 GB) are far larger than the 126 MB L2, so
+no explicit L2 flush is needed between timed steps.
+
+--impl reference times the reference algorithm on the host: the reference
+package is pure Python/numpy and cannot travel to the GPU box, so its
+restatement in oracle/wadg_oracle.py (pinned to the reference's golden
+vectors) is timed on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (description, n, N, dtype, heterogeneous c2, steps in BASELINE)
+    "c2": ("config 2: warped cube 8^3x6 tets, N=3, fp64", 8, 3, "float64", False, 10),
+    "c3": ("config 3: warped cube 32^3x6 tets, fp64/fp32 sweep", 32, 4, "float64", False, 50),
+    "c4": ("config 4: warped cube 64^3x6 tets, N=4, fp32, heterogeneous c^2", 64, 4, "float32", True, 100),
+    "c5": ("config 5: warped cube 48x48x(48G)x6 tets per GPU, N=5, fp32", 48, 5, "float32", False, 100),
+}
+
+
+def c2_het(x, y, z):
+    return 1.0 + 0.5 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y) * np.sin(2 * np.pi * z)
+
+
+def gaussian_ic(*xyz):
+    r2 = sum(a * a for a in xyz)
+    try:
+        import torch
+        if isinstance(r2, torch.Tensor):
+            p = torch.exp(-25.0 * r2)
+            return (p,) + tuple(torch.zeros_like(p) for _ in xyz)
+    except ImportError:
+        pass
+    p = np.exp(-25.0 * r2)
+    return (p,) + tuple(np.zeros_like(p) for _ in xyz)
+
+
+def algorithmic_model(d, K, Np, Nq, Nqu, F, w, n_omega):
+    """SURVEY.md §8(d) per-element bytes / flops per RK stage, times K."""
+    fld = d + 1
+    B = {
+        "volume": w * (2 * fld * Np + d * d * Nq),
+        "surface": w * (3 * fld * Np + fld * F + (d + 1) * F) + 4 * F,
+        "update": w * (5 * fld * Np + n_omega * Nqu),
+    }
+    FL = {
+        "volume": 8 * d * Np * Nq + (2 * d * (2 * d - 1) + d) * Nq,
+        "surface": 4 * fld * Np * F + 30 * F,
+        "update": fld * (4 * Np * Nqu + Nqu) + 4 * fld * Np,
+    }
+    return {k: v * K for k, v in B.items()}, {k: v * K for k, v in FL.items()}
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def build_problem(cfg_name, N_override=None, dtype_override=None, rank=0, world=1):
+    from paper_1608_03836_b200 import meshgen, parallel, solver
+    desc, n, N, dtype, het, _ = CONFIGS[cfg_name]
+    N = N_override or N
+    dtype = dtype_override or dtype
+    if cfg_name == "c5":
+        nz = 48 * world
+        mesh = meshgen.warped_cube_tet_mesh(n, N, nz=nz, z_range=(-1.0, -1.0 + 2.0 * nz / n))
+    else:
+        mesh = meshgen.warped_cube_tet_mesh(n, N)
+    cfg = solver.SolverConfig(N=N, formulation=solver.Formulation.StrongWeak, dtype=dtype)
+    medium = solver.MediumField(c2_het if het else 1.0)
+    if world > 1:
+        disc = parallel.slab_discretization(mesh, cfg, medium, rank, world, n_layers=mesh.provenance["nz"])
+    else:
+        disc = solver.Discretization(mesh, cfg, medium)
+    return mesh, cfg, medium, disc, desc
+
+
+def cpu_oracle_rate(cfg_name, n_sample, steps, N_override=None):
+    """Time the reference algorithm (numpy oracle, fp64, all host threads) on
+    a bounded sample mesh: GDOF-updates per RK stage per second."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import wadg_oracle as O
+    from paper_1608_03836_b200 import meshgen
+    _, _, N, _, het, _ = CONFIGS[cfg_name]
+    N = N_override or N
+    mesh = meshgen.warped_cube_tet_mesh(n_sample, N)
+    od = O.OracleDiscretization(mesh, N, True, c2=(c2_het if het else 1.0))
+    st = O.project_initial_condition(mesh, N, gaussian_ic)
+    dt = 0.5 * (2.0 / n_sample) / (N + 1) ** 2
+    fn = lambda y: O.rhs_full(y, od)
+    st = O.lsrk_step(st, dt, fn)                      # warm-up
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st = O.lsrk_step(st, dt, fn)
+    el = time.perf_counter() - t0
+    dof = 4 * mesh.K * od.ref.Np
+    return dof * 5 * steps / el / 1e9, mesh.K, el
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_sample = 16
+    t_all = []
+    K = None
+    for _ in range(args.warmup):
+        cpu_oracle_rate(args.config, n_sample, 1, args.order)
+    for _ in range(args.steps):
+        v, K, el = cpu_oracle_rate(args.config, n_sample, 1, args.order)
+        t_all.append(el)
+    _, _, N, _, het, _ = CONFIGS[args.config]
+    N = args.order or N
+    from paper_1608_03836_b200 import refelem
+    Np = refelem.basis_dimension(refelem.ElementShape.Tetrahedron, N)
+    dof = 4 * K * Np
+    t = float(np.median(t_all))
+    value = dof * 5 / t / 1e9
+    cores = os.cpu_count()
+    sample = f"warped cube {n_sample}^3x6 = {K} tets, N={N}, fp64 numpy oracle, 1 LSRK step per timed step"
+    line = {
+        "impl": "reference", "metric": "GDOF/s per RK stage", "value": value, "unit": "GDOF/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIGS[args.config][0], "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--order", type=int, default=None, help="override N (config 3 sweep)")
+    ap.add_argument("--dtype", default=None)
+    ap.add_argument("--impl", default="wadg", choices=["wadg", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_1608_03836_b200 import _native, solver
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    t_setup = time.perf_counter()
+    mesh, cfg, medium, disc, desc = build_problem(args.config, args.order, args.dtype, rank, world)
+    d = disc.dev
+    state = solver.project_initial_condition_device(disc, gaussian_ic)
+    setup_s = time.perf_counter() - t_setup
+    N = cfg.N
+    dt = 0.5 * mesh.h / (N + 1) ** 2
+    Q = state
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    res, rhs = d.empty_fields(), d.empty_fields()
+    vp = lambda t: ctypes.c_void_p(t.data_ptr())
+    fl = disc.flux
+    exch = getattr(disc, "exchange", None)
+
+    def stage(a, b, ev=None):
+        if exch is not None:
+            exch.start(Q)
+        if ev is not None:
+            ev[0].record(stream)
+        _native.call("wadg_volume", ctypes.byref(d.struct), vp(Q), vp(rhs), sp)
+        if ev is not None:
+            ev[1].record(stream)
+        if exch is not None:
+            exch.surface(Q, rhs, fl.tau_p, fl.tau_u, sp)
+        else:
+            _native.call("wadg_surface", ctypes.byref(d.struct), vp(Q), vp(rhs), fl.tau_p, fl.tau_u,
+                         1, 0, -1, sp)
+        if ev is not None:
+            ev[2].record(stream)
+        _native.call("wadg_update_lsrk", ctypes.byref(d.struct), vp(rhs), vp(res), vp(Q), a, b, dt, sp)
+        if ev is not None:
+            ev[3].record(stream)
+
+    def step(evs=None):
+        for s, (a, b) in enumerate(zip(solver.LSRK4A, solver.LSRK4B)):
+            stage(a, b, None if evs is None else evs[s])
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(5)]
+           for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0.record(stream)
+    for i in range(args.steps):
+        step(evs[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms_total = t0.elapsed_time(t1)
+    clk = clocks.stop()
+    kern = {"volume": [], "surface": [], "update": []}
+    for i in range(args.steps):
+        for s in range(5):
+            e = evs[i][s]
+            kern["volume"].append(e[0].elapsed_time(e[1]))
+            kern["surface"].append(e[1].elapsed_time(e[2]))
+            kern["update"].append(e[2].elapsed_time(e[3]))
+    if world > 1:
+        tt = torch.tensor([ms_total], device="cuda")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_step = ms_total / args.steps
+
+    ref = disc.ref
+    K_local = d.K
+    Np = ref.Np
+    dof_stage = (mesh.dim + 1) * K_local * Np
+    dof_all = dof_stage * world
+    value = dof_all * 5 * args.steps / (ms_total * 1e-3) / 1e9
+
+    # roofline of the dominant kernel
+    w = 4 if cfg.dtype == "float32" else 8
+    B, FL = algorithmic_model(mesh.dim, K_local, Np, ref.Nq, disc.ref_upd.Nq,
+                              ref.n_faces * ref.nfq, w, 2 if callable(medium.c2) else 1)
+    avg = {k: float(np.mean(v)) for k, v in kern.items()}
+    top = max(avg, key=avg.get)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm_peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(peaks_path):
+        with open(peaks_path) as f:
+            hbm_peak = float(json.load(f)["hbm_gbs"])
+        peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+    achieved = B[top] / (avg[top] * 1e-3) / 1e9
+    kernels = {k: {"ms": avg[k], "GB/s": B[k] / (avg[k] * 1e-3) / 1e9,
+                   "hbm_frac": B[k] / (avg[k] * 1e-3) / 1e9 / hbm_peak,
+                   "TFLOP/s": FL[k] / (avg[k] * 1e-3) / 1e12,
+                   "share": avg[k] / sum(avg.values())} for k in avg}
+
+    # end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        import torch as _t
+        host = [_t.empty((K_local, Np), dtype=d.dtype).pin_memory() for _ in range(mesh.dim + 1)]
+        for i in range(mesh.dim + 1):
+            host[i].copy_(Q[i, :, :K_local].T.cpu())
+        hstate = solver.FieldState.from_fields(host)
+        n_e2e = max(2, min(args.steps, 5))
+        hstate = solver.lsrk_step(hstate, dt, disc.rhs)
+        torch.cuda.synchronize()
+        e0, e1 = _t.cuda.Event(enable_timing=True), _t.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_e2e):
+            hstate = solver.lsrk_step(hstate, dt, disc.rhs)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / n_e2e
+        nb = sum(h.numel() * h.element_size() for h in host)
+        e2e = {"value": dof_stage * 5 / (e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "ms_per_step": e_ms,
+               "api": "solver.lsrk_step(FieldState(pinned host tensors), dt, disc.rhs)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, Ks, el = cpu_oracle_rate(args.config, 16, 3, args.order)
+        cpu = {"value": v, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"numpy oracle (fp64) on warped cube 16^3x6 = {Ks} tets, N={N}, "
+                         f"3 LSRK steps, {el:.1f} s"}
+
+    if rank == 0:
+        Np2, Nqu = Np * Np, disc.ref_upd.Nq
+        line = {
+            "metric": "GDOF/s per RK stage", "value": value, "unit": "GDOF/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak" if args.config == "c5" else "strong",
+            "vs_baseline": None,
+            "dtype": "f32" if cfg.dtype == "float32" else "f64", "data": "synthetic",
+            "config": {"workload": desc, "K": mesh.K, "N": N, "Np": Np, "formulation": "strong-weak",
+                       "dt": dt, "l2": "inputs > L2 (fields+geometry ~GBs); no flush needed",
+                       "parallelism": f"z-slabs x{world}", "setup_s": round(setup_s, 1)},
+            "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm_peak,
+                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": B[top],
+                         "fp_achieved_tflops": FL[top] / (avg[top] * 1e-3) / 1e12},
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": 15 * args.steps * (1 if exch is None else 1),
+            "clocks": clk,
+            "storage_words_per_element": {"wadg_weights": 2 * Nqu, "dense_inverse": 2 * Np2,
+                                          "ratio": Np2 / Nqu},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,127 @@
+/*
+ * wadg_b200.h — C ABI of the B200-native WADG right-hand-side / LSRK45 path.
+ *
+ * The reference (arXiv 1608.03836 restated as the Python package `wadg`) has
+ * no FFI: its boundary is the Python API of wadg.solver.  Each entry point
+ * below replaces one of those functions (or the array kernel inside it) for
+ * device-resident data; the Python drop-in (paper_1608_03836_b200.solver)
+ * binds them with ctypes (INTEGRATION.md shows the binding):
+ *
+ *   wadg_volume        <- solver._volume_terms            R/pkg/src/wadg/solver.py:241-265
+ *   wadg_surface       <- solver._surface_terms + face_traces  solver.py:195-238
+ *   wadg_mass_inverse  <- solver.apply_mass_inverse (WADG)     solver.py:290-301
+ *                         -> operators.apply_weight_adjusted_inverse operators.py:45-61
+ *   wadg_update_lsrk   <- apply_mass_inverse fused with the LSRK stage axpy
+ *                         of solver.lsrk_step                  solver.py:348-363
+ *   wadg_stage         <- one LSRK stage of lsrk_step(state, dt, rhs_full)
+ *                         = volume + surface + update_lsrk
+ *   wadg_lsrk_axpy     <- the stage axpy of lsrk_step for an arbitrary rhs_fn
+ *   wadg_energy        <- solver.energy                        solver.py:314-321
+ *   wadg_pack_halo     <- (new) face-trace halo for element slabs; no reference counterpart
+ *
+ * Conventions: plain pointers and sizes only.  All array pointers are device
+ * pointers in the dtype named by `dtype` (WADG_F64 / WADG_F32) unless typed
+ * int32_t.  Element index is the fastest (stride-1) dimension of every
+ * per-element array, padded to Kpad (a multiple of WADG_ELEMS_PER_BLOCK).
+ * Kernels never allocate and never synchronise; `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  Return 0 on success, nonzero on error
+ * with a message in wadg_last_error() (thread-local).
+ */
+#ifndef WADG_B200_H
+#define WADG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WADG_ABI_VERSION 1
+#define WADG_ELEMS_PER_BLOCK 32
+
+enum { WADG_F64 = 0, WADG_F32 = 1 };
+enum { WADG_STRONG = 0, WADG_STRONG_WEAK = 1 };
+
+typedef struct wadg_problem {
+    /* sizes */
+    int32_t dim;          /* 2 or 3; fields = dim + 1 (p, u_1..u_dim) */
+    int32_t dtype;        /* WADG_F64 | WADG_F32 */
+    int32_t K, Kpad;      /* elements, padded element stride */
+    int32_t Np, Nq, Nqu;  /* nodes, volume quad points, update quad points */
+    int32_t Nf, Nfp, Nfq; /* faces, nodes per face, quad points per face */
+    int32_t n_orient;     /* face orientation codes (2 in 2D, 6 in 3D) */
+    int32_t formulation;  /* WADG_STRONG | WADG_STRONG_WEAK */
+    /* reference operators, row-major */
+    const void *Vq;       /* [Nq][Np]      volume interpolation            */
+    const void *Dq;       /* [dim][Nq][Np] reference derivatives at quad   */
+    const void *Pq;       /* [Np][Nq]      Mhat^-1 Vq^T W                  */
+    const void *DTW;      /* [dim][Np][Nq] Mhat^-1 D_a^T W (strong-weak p) */
+    const void *Vu;       /* [Nqu][Np]     update-rule interpolation       */
+    const void *Pu;       /* [Np][Nqu]     update-rule projection          */
+    const void *Vfi;      /* [Nfq][Nfp]    face nodes -> face quad points  */
+    const void *Pf;       /* [Np][Nf*Nfq]  Mhat^-1 Vf^T Wf (lift)          */
+    const int32_t *fmask;    /* [Nf][Nfp] volume node of each face node            */
+    const int32_t *ext_node; /* [Nf*n_orient][Nfp] neighbour volume node, by code  */
+    const int32_t *fperm;    /* [n_orient][Nfp] face-node permutation, by orient.  */
+    /* per-element data, element index fastest */
+    const void *geo;      /* [dim*dim][Nq][Kpad]  (dr_a/dx_i) J, row a*dim+i      */
+    const void *fgeo;     /* [dim+1][Nf*Nfq][Kpad] n_1..n_dim, sJ/2               */
+    const void *wu;       /* [Nqu][Kpad] 1/J at update points                     */
+    const void *wp;       /* [Nqu][Kpad] c^2/J, or NULL: use c2 * wu             */
+    double c2;            /* constant c^2 when wp == NULL                         */
+    const int32_t *nbr;   /* [Nf][Kpad] neighbour element; -1 = Dirichlet mirror;
+                             <= -2 = halo slot (-nbr-2)                          */
+    const int32_t *ncode; /* [Nf][Kpad] nbr face * n_orient + orientation        */
+    /* halo face traces from other ranks: [n_halo][dim+1][Nfp] (sender order)  */
+    const void *halo;
+    int32_t n_halo;
+    /* energy quadrature (diagnostics) */
+    int32_t Ne;
+    const void *Ve;       /* [Ne][Np] */
+    const void *we;       /* [Ne]     */
+    const void *ewp;      /* [Ne][Kpad] */
+    const void *ewu;      /* [Ne][Kpad] */
+    int32_t e_recip;      /* 1: weights are we/ew*, 0: we*ew*                     */
+} wadg_problem;
+
+int wadg_abi_version(void);
+const char *wadg_last_error(void);
+
+/* rhs = volume term of the Mhat^-1-premultiplied RHS (overwrites rhs) */
+int wadg_volume(const wadg_problem *P, const void *Q, void *rhs, void *stream);
+
+/* rhs (+)= surface term over element blocks [block_begin, block_end) (units of
+ * WADG_ELEMS_PER_BLOCK); block_end < 0 means all blocks */
+int wadg_surface(const wadg_problem *P, const void *Q, void *rhs, double tau_p,
+                 double tau_u, int accumulate, int block_begin, int block_end,
+                 void *stream);
+
+/* out = WADG mass inverse of a premultiplied rhs */
+int wadg_mass_inverse(const wadg_problem *P, const void *rhs, void *out, void *stream);
+
+/* res = a*res + dt*Minv(rhs); Q += b*res  (a == 0 ignores the old res) */
+int wadg_update_lsrk(const wadg_problem *P, const void *rhs, void *res, void *Q,
+                     double a, double b, double dt, void *stream);
+
+/* one LSRK stage: volume -> surface -> update_lsrk (rhs is scratch) */
+int wadg_stage(const wadg_problem *P, void *Q, void *res, void *rhs, double tau_p,
+               double tau_u, double a, double b, double dt, void *stream);
+
+/* generic stage axpy over n entries: res = a*res + dt*d; Q += b*res */
+int wadg_lsrk_axpy(int dtype, int64_t n, const void *d, void *res, void *Q,
+                   double a, double b, double dt, void *stream);
+
+/* energy: partials must hold ceil(Kpad/32) doubles; writes the total to
+ * out_dev[0] (device double) */
+int wadg_energy(const wadg_problem *P, const void *Q, double *partials,
+                double *out_dev, void *stream);
+
+/* buf[(s*(dim+1) + fld)*Nfp + i] = Q[fld][fmask[send_f[s]][i]][send_k[s]] */
+int wadg_pack_halo(const wadg_problem *P, const void *Q, const int32_t *send_k,
+                   const int32_t *send_f, int32_t n_send, void *buf, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WADG_B200_H */

@@ -1,0 +1,725 @@
+// B200 (sm_100a) kernels for the WADG right-hand side and LSRK45 stage.
+//
+// Execution model (all kernels): one CTA owns KB = 32 consecutive elements;
+// lane e of every warp is element e of the block, warp g walks operator rows
+// g, g+NG, ...  Per-element arrays are stored element-fastest, so each warp
+// access to a per-element row is one coalesced 128 B (fp32) / 256 B (fp64)
+// transaction, and every operator entry a warp needs is warp-uniform (one
+// broadcast through L1).  Element fields are staged once in shared memory;
+// quadrature-point intermediates go through a chunked shared-memory scratch
+// so any N (1..7) fits.  Register accumulators hold each thread's output rows.
+//
+// Reference counterparts (R/pkg/src/wadg/):
+//   k_volume  <- solver._volume_terms      solver.py:241-265
+//   k_surface <- solver._surface_terms     solver.py:207-238 (+ face_traces :195-201)
+//   k_update  <- solver.apply_mass_inverse / operators.apply_weight_adjusted_inverse
+//                fused with the lsrk_step axpy (solver.py:290-301, 348-363)
+//   k_energy  <- solver.energy             solver.py:314-321
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "wadg_b200.h"
+
+namespace wadg {
+
+constexpr int KB = WADG_ELEMS_PER_BLOCK;
+constexpr int NT = 256;
+constexpr int NG = NT / KB;
+
+template <typename T>
+struct Prob {
+    int K, Kpad, Np, Nq, Nqu, Nf, Nfp, Nfq, nor;
+    const T *Vq, *Dq, *Pq, *DTW, *Vu, *Pu, *Vfi, *Pf;
+    const int32_t *fmask, *ext_node, *fperm;
+    const T *geo, *fgeo, *wu, *wp;
+    T c2;
+    const int32_t *nbr, *ncode;
+    const T *halo;
+    int n_halo;
+    int Ne;
+    const T *Ve, *we, *ewp, *ewu;
+    int e_recip;
+};
+
+template <typename T>
+Prob<T> make_prob(const wadg_problem &p) {
+    Prob<T> q;
+    q.K = p.K; q.Kpad = p.Kpad; q.Np = p.Np; q.Nq = p.Nq; q.Nqu = p.Nqu;
+    q.Nf = p.Nf; q.Nfp = p.Nfp; q.Nfq = p.Nfq; q.nor = p.n_orient;
+    q.Vq = (const T *)p.Vq; q.Dq = (const T *)p.Dq; q.Pq = (const T *)p.Pq;
+    q.DTW = (const T *)p.DTW; q.Vu = (const T *)p.Vu; q.Pu = (const T *)p.Pu;
+    q.Vfi = (const T *)p.Vfi; q.Pf = (const T *)p.Pf;
+    q.fmask = p.fmask; q.ext_node = p.ext_node; q.fperm = p.fperm;
+    q.geo = (const T *)p.geo; q.fgeo = (const T *)p.fgeo;
+    q.wu = (const T *)p.wu; q.wp = (const T *)p.wp; q.c2 = (T)p.c2;
+    q.nbr = p.nbr; q.ncode = p.ncode;
+    q.halo = (const T *)p.halo; q.n_halo = p.n_halo;
+    q.Ne = p.Ne; q.Ve = (const T *)p.Ve; q.we = (const T *)p.we;
+    q.ewp = (const T *)p.ewp; q.ewu = (const T *)p.ewu; q.e_recip = p.e_recip;
+    return q;
+}
+
+// ---------------------------------------------------------------------------
+// Volume term.  Strong-weak (SW): r_u_i = -Pq (sum_a G_ai D_a p),
+// r_p = sum_a DTW_a (sum_i G_ai Vq u_i).  Strong: r_p = -Pq (sum_ia G_ai D_a u_i).
+template <typename T, int DIM, int RJ, bool SW>
+__global__ void __launch_bounds__(NT)
+k_volume(const Prob<T> P, const T *__restrict__ Q, T *__restrict__ rhs, int QC) {
+    constexpr int FLD = DIM + 1;
+    constexpr int NW = SW ? 2 * DIM : DIM + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *sQ = reinterpret_cast<T *>(smem_raw);
+    T *sW = sQ + FLD * P.Np * KB;
+    const int e = threadIdx.x % KB, g = threadIdx.x / KB;
+    const size_t S = P.Kpad;
+    const size_t k = (size_t)blockIdx.x * KB + e;
+    const int Np = P.Np, Nq = P.Nq;
+
+    for (int r = g; r < FLD * Np; r += NG) sQ[r * KB + e] = Q[(size_t)r * S + k];
+    __syncthreads();
+
+    T acc[FLD][RJ];
+#pragma unroll
+    for (int f = 0; f < FLD; ++f)
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) acc[f][r] = T(0);
+
+    for (int q0 = 0; q0 < Nq; q0 += QC) {
+        const int qn = min(QC, Nq - q0);
+        for (int qq = g; qq < qn; qq += NG) {
+            const int q = q0 + qq;
+            T G[DIM][DIM];
+#pragma unroll
+            for (int a = 0; a < DIM; ++a)
+#pragma unroll
+                for (int i = 0; i < DIM; ++i)
+                    G[a][i] = P.geo[(size_t)((a * DIM + i) * Nq + q) * S + k];
+            if (SW) {
+                T d[DIM], U[DIM];
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) { d[a] = T(0); U[a] = T(0); }
+                const T *Vrow = P.Vq + (size_t)q * Np;
+                const T *Drow = P.Dq + (size_t)q * Np;
+#pragma unroll 4
+                for (int j = 0; j < Np; ++j) {
+                    const T pj = sQ[j * KB + e];
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a)
+                        d[a] = fma(__ldg(Drow + (size_t)a * Nq * Np + j), pj, d[a]);
+                    const T vj = __ldg(Vrow + j);
+#pragma unroll
+                    for (int i = 0; i < DIM; ++i)
+                        U[i] = fma(vj, sQ[((1 + i) * Np + j) * KB + e], U[i]);
+                }
+#pragma unroll
+                for (int i = 0; i < DIM; ++i) {
+                    T s = T(0);
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) s = fma(G[a][i], d[a], s);
+                    sW[(i * QC + qq) * KB + e] = s;
+                }
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    T s = T(0);
+#pragma unroll
+                    for (int i = 0; i < DIM; ++i) s = fma(G[a][i], U[i], s);
+                    sW[((DIM + a) * QC + qq) * KB + e] = s;
+                }
+            } else {
+                T d[FLD][DIM];
+#pragma unroll
+                for (int f = 0; f < FLD; ++f)
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) d[f][a] = T(0);
+                const T *Drow = P.Dq + (size_t)q * Np;
+#pragma unroll 2
+                for (int j = 0; j < Np; ++j) {
+                    T x[FLD];
+#pragma unroll
+                    for (int f = 0; f < FLD; ++f) x[f] = sQ[(f * Np + j) * KB + e];
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) {
+                        const T D = __ldg(Drow + (size_t)a * Nq * Np + j);
+#pragma unroll
+                        for (int f = 0; f < FLD; ++f) d[f][a] = fma(D, x[f], d[f][a]);
+                    }
+                }
+                T div = T(0);
+#pragma unroll
+                for (int i = 0; i < DIM; ++i) {
+                    T s = T(0);
+#pragma unroll
+                    for (int a = 0; a < DIM; ++a) {
+                        s = fma(G[a][i], d[0][a], s);
+                        div = fma(G[a][i], d[1 + i][a], div);
+                    }
+                    sW[(i * QC + qq) * KB + e] = s;
+                }
+                sW[(DIM * QC + qq) * KB + e] = div;
+            }
+        }
+        __syncthreads();
+        for (int qq = 0; qq < qn; ++qq) {
+            const int q = q0 + qq;
+            T w[NW];
+#pragma unroll
+            for (int m = 0; m < NW; ++m) w[m] = sW[(m * QC + qq) * KB + e];
+#pragma unroll
+            for (int r = 0; r < RJ; ++r) {
+                const int j = g + r * NG;
+                if (j < Np) {
+                    const T pv = __ldg(P.Pq + (size_t)j * Nq + q);
+#pragma unroll
+                    for (int i = 0; i < DIM; ++i) acc[1 + i][r] = fma(-pv, w[i], acc[1 + i][r]);
+                    if (SW) {
+                        T s = acc[0][r];
+#pragma unroll
+                        for (int a = 0; a < DIM; ++a)
+                            s = fma(__ldg(P.DTW + (size_t)(a * Np + j) * Nq + q), w[DIM + a], s);
+                        acc[0][r] = s;
+                    } else {
+                        acc[0][r] = fma(-pv, w[DIM], acc[0][r]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < RJ; ++r) {
+        const int j = g + r * NG;
+        if (j < Np) {
+#pragma unroll
+            for (int f = 0; f < FLD; ++f) rhs[(size_t)(f * Np + j) * S + k] = acc[f][r];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Surface term: nodal face traces (own + neighbour, permuted by orientation,
+// Dirichlet mirror p+ = -p-, u+ = u-), interpolation to face quadrature,
+// penalty flux, lift with Pf.  One face at a time through shared memory.
+template <typename T, int DIM, int RJ, bool SW>
+__global__ void __launch_bounds__(NT)
+k_surface(const Prob<T> P, const T *__restrict__ Q, T *__restrict__ rhs, T tau_p, T tau_u,
+          int accumulate, int block0, int QF) {
+    constexpr int FLD = DIM + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int Np = P.Np, Nfp = P.Nfp, Nfq = P.Nfq, Nf = P.Nf, NFQ = Nf * Nfq;
+    T *sM = reinterpret_cast<T *>(smem_raw);
+    T *sP = sM + FLD * Nfp * KB;
+    T *sG = sP + FLD * Nfp * KB;
+    const int e = threadIdx.x % KB, g = threadIdx.x / KB;
+    const size_t S = P.Kpad;
+    const size_t k = (size_t)(block0 + blockIdx.x) * KB + e;
+
+    T acc[FLD][RJ];
+#pragma unroll
+    for (int f = 0; f < FLD; ++f)
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) acc[f][r] = T(0);
+
+    for (int f = 0; f < Nf; ++f) {
+        const int nb = P.nbr[(size_t)f * S + k];
+        const int code = P.ncode[(size_t)f * S + k];
+        for (int r = g; r < FLD * Nfp; r += NG) {
+            const int fld = r / Nfp, i = r - fld * Nfp;
+            const T m = Q[(size_t)(fld * Np + P.fmask[f * Nfp + i]) * S + k];
+            T pv;
+            if (nb >= 0) {
+                pv = Q[(size_t)(fld * Np + P.ext_node[code * Nfp + i]) * S + nb];
+            } else if (nb == -1) {
+                pv = (fld == 0) ? -m : m;
+            } else {
+                const int h = -nb - 2, o = code % P.nor;
+                pv = P.halo[((size_t)h * FLD + fld) * Nfp + P.fperm[o * Nfp + i]];
+            }
+            sM[r * KB + e] = m;
+            sP[r * KB + e] = pv;
+        }
+        __syncthreads();
+        for (int c0 = 0; c0 < Nfq; c0 += QF) {
+            const int cn = min(QF, Nfq - c0);
+            for (int cc = g; cc < cn; cc += NG) {
+                const int fq = c0 + cc;
+                T mM[FLD], mP[FLD];
+#pragma unroll
+                for (int c = 0; c < FLD; ++c) { mM[c] = T(0); mP[c] = T(0); }
+                const T *Vrow = P.Vfi + (size_t)fq * Nfp;
+                for (int i = 0; i < Nfp; ++i) {
+                    const T v = __ldg(Vrow + i);
+#pragma unroll
+                    for (int c = 0; c < FLD; ++c) {
+                        mM[c] = fma(v, sM[(c * Nfp + i) * KB + e], mM[c]);
+                        mP[c] = fma(v, sP[(c * Nfp + i) * KB + e], mP[c]);
+                    }
+                }
+                const int idx = f * Nfq + fq;
+                T n[DIM];
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) n[d] = P.fgeo[(size_t)(d * NFQ + idx) * S + k];
+                const T sJh = P.fgeo[(size_t)(DIM * NFQ + idx) * S + k];
+                const T dp = mP[0] - mM[0];
+                T dUn = T(0), avg = T(0);
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) {
+                    dUn += (mP[1 + d] - mM[1 + d]) * n[d];
+                    avg += (mP[1 + d] + mM[1 + d]) * n[d];
+                }
+                const T fp = (SW ? avg : dUn) - tau_p * dp;
+                const T fu = dp - tau_u * dUn;
+                sG[cc * KB + e] = fp * sJh;
+#pragma unroll
+                for (int d = 0; d < DIM; ++d) sG[((1 + d) * QF + cc) * KB + e] = fu * (sJh * n[d]);
+            }
+            __syncthreads();
+            for (int cc = 0; cc < cn; ++cc) {
+                T w[FLD];
+#pragma unroll
+                for (int c = 0; c < FLD; ++c) w[c] = sG[(c * QF + cc) * KB + e];
+#pragma unroll
+                for (int r = 0; r < RJ; ++r) {
+                    const int j = g + r * NG;
+                    if (j < Np) {
+                        const T pf = __ldg(P.Pf + (size_t)j * NFQ + f * Nfq + c0 + cc);
+#pragma unroll
+                        for (int c = 0; c < FLD; ++c) acc[c][r] = fma(-pf, w[c], acc[c][r]);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < RJ; ++r) {
+        const int j = g + r * NG;
+        if (j < Np) {
+#pragma unroll
+            for (int c = 0; c < FLD; ++c) {
+                const size_t o = (size_t)(c * Np + j) * S + k;
+                rhs[o] = accumulate ? rhs[o] + acc[c][r] : acc[c][r];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// WADG mass inverse Pu diag(w) Vu per field (w = c^2/J for p, 1/J for u);
+// MODE 0: out = result;  MODE 1: res = a res + dt result, Q += b res.
+template <typename T, int DIM, int RJ, int MODE>
+__global__ void __launch_bounds__(NT)
+k_update(const Prob<T> P, const T *__restrict__ rhs, T *__restrict__ out, T *__restrict__ Qo,
+         T a, T b, T dt, int QC) {
+    constexpr int FLD = DIM + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int Np = P.Np, Nqu = P.Nqu;
+    T *sR = reinterpret_cast<T *>(smem_raw);
+    T *sZ = sR + FLD * Np * KB;
+    const int e = threadIdx.x % KB, g = threadIdx.x / KB;
+    const size_t S = P.Kpad;
+    const size_t k = (size_t)blockIdx.x * KB + e;
+
+    for (int r = g; r < FLD * Np; r += NG) sR[r * KB + e] = rhs[(size_t)r * S + k];
+    __syncthreads();
+
+    T acc[FLD][RJ];
+#pragma unroll
+    for (int f = 0; f < FLD; ++f)
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) acc[f][r] = T(0);
+
+    for (int q0 = 0; q0 < Nqu; q0 += QC) {
+        const int qn = min(QC, Nqu - q0);
+        for (int qq = g; qq < qn; qq += NG) {
+            const int q = q0 + qq;
+            const T wu = P.wu[(size_t)q * S + k];
+            const T wp = P.wp ? P.wp[(size_t)q * S + k] : P.c2 * wu;
+            T z[FLD];
+#pragma unroll
+            for (int c = 0; c < FLD; ++c) z[c] = T(0);
+            const T *Vrow = P.Vu + (size_t)q * Np;
+#pragma unroll 4
+            for (int j = 0; j < Np; ++j) {
+                const T v = __ldg(Vrow + j);
+#pragma unroll
+                for (int c = 0; c < FLD; ++c) z[c] = fma(v, sR[(c * Np + j) * KB + e], z[c]);
+            }
+            sZ[qq * KB + e] = wp * z[0];
+#pragma unroll
+            for (int c = 1; c < FLD; ++c) sZ[(c * QC + qq) * KB + e] = wu * z[c];
+        }
+        __syncthreads();
+        for (int qq = 0; qq < qn; ++qq) {
+            const int q = q0 + qq;
+            T w[FLD];
+#pragma unroll
+            for (int c = 0; c < FLD; ++c) w[c] = sZ[(c * QC + qq) * KB + e];
+#pragma unroll
+            for (int r = 0; r < RJ; ++r) {
+                const int j = g + r * NG;
+                if (j < Np) {
+                    const T pu = __ldg(P.Pu + (size_t)j * Nqu + q);
+#pragma unroll
+                    for (int c = 0; c < FLD; ++c) acc[c][r] = fma(pu, w[c], acc[c][r]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < RJ; ++r) {
+        const int j = g + r * NG;
+        if (j < Np) {
+#pragma unroll
+            for (int c = 0; c < FLD; ++c) {
+                const size_t o = (size_t)(c * Np + j) * S + k;
+                if (MODE == 0) {
+                    out[o] = acc[c][r];
+                } else {
+                    const T rr = (a == T(0)) ? dt * acc[c][r] : a * out[o] + dt * acc[c][r];
+                    out[o] = rr;
+                    Qo[o] = Qo[o] + b * rr;
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+template <typename T, int DIM>
+__global__ void __launch_bounds__(NT)
+k_energy(const Prob<T> P, const T *__restrict__ Q, double *__restrict__ partial) {
+    constexpr int FLD = DIM + 1;
+    __shared__ double red[NT];
+    const int e = threadIdx.x % KB, g = threadIdx.x / KB;
+    const size_t S = P.Kpad;
+    const size_t k = (size_t)blockIdx.x * KB + e;
+    const int Np = P.Np;
+    double sum = 0.0;
+    for (int q = g; q < P.Ne; q += NG) {
+        T v[FLD];
+#pragma unroll
+        for (int c = 0; c < FLD; ++c) v[c] = T(0);
+        for (int j = 0; j < Np; ++j) {
+            const T x = __ldg(P.Ve + (size_t)q * Np + j);
+#pragma unroll
+            for (int c = 0; c < FLD; ++c) v[c] = fma(x, Q[(size_t)(c * Np + j) * S + k], v[c]);
+        }
+        double uu = 0.0;
+#pragma unroll
+        for (int c = 1; c < FLD; ++c) uu += (double)v[c] * (double)v[c];
+        const double wq = (double)P.we[q];
+        const double ap = (double)P.ewp[(size_t)q * S + k], au = (double)P.ewu[(size_t)q * S + k];
+        const double pp = (double)v[0] * (double)v[0];
+        sum += P.e_recip ? wq * (pp / ap + uu / au) : wq * (pp * ap + uu * au);
+    }
+    red[threadIdx.x] = sum;
+    __syncthreads();
+    for (int s = NT / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = 0.5 * red[0];
+}
+
+__global__ void k_reduce(const double *__restrict__ partial, int n, double *__restrict__ out) {
+    __shared__ double red[1024];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += partial[i];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = red[0];
+}
+
+template <typename T, int DIM>
+__global__ void k_pack_halo(const Prob<T> P, const T *__restrict__ Q, const int32_t *__restrict__ send_k,
+                            const int32_t *__restrict__ send_f, int n_send, T *__restrict__ buf) {
+    constexpr int FLD = DIM + 1;
+    const int Nfp = P.Nfp;
+    const int64_t total = (int64_t)n_send * FLD * Nfp;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t % Nfp);
+        const int fld = (int)((t / Nfp) % FLD);
+        const int s = (int)(t / ((int64_t)Nfp * FLD));
+        const int node = P.fmask[send_f[s] * Nfp + i];
+        buf[t] = Q[(size_t)(fld * P.Np + node) * P.Kpad + send_k[s]];
+    }
+}
+
+template <typename T>
+__global__ void k_axpy(int64_t n, const T *__restrict__ d, T *__restrict__ res, T *__restrict__ Q,
+                       T a, T b, T dt) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const T rr = (a == T(0)) ? dt * d[i] : a * res[i] + dt * d[i];
+        res[i] = rr;
+        Q[i] = Q[i] + b * rr;
+    }
+}
+
+}  // namespace wadg
+
+// ===========================================================================
+// C ABI
+using namespace wadg;
+
+static thread_local char g_err[512] = "";
+
+static int fail(const char *msg) {
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return 1;
+}
+
+static int check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+        return 2;
+    }
+    return 0;
+}
+
+static int rows_per_thread(int Np) {
+    const int rj = (Np + NG - 1) / NG;
+    if (rj <= 2) return 2;
+    if (rj <= 4) return 4;
+    if (rj <= 8) return 8;
+    if (rj <= 16) return 16;
+    return -1;
+}
+
+static int validate(const wadg_problem *P) {
+    if (!P) return fail("null problem");
+    if (P->dim != 2 && P->dim != 3) return fail("dim must be 2 or 3");
+    if (P->dtype != WADG_F64 && P->dtype != WADG_F32) return fail("bad dtype");
+    if (P->Kpad % KB != 0 || P->Kpad < P->K) return fail("Kpad must be a multiple of 32 and >= K");
+    if (rows_per_thread(P->Np) < 0) return fail("Np too large (max 128)");
+    return 0;
+}
+
+template <typename KernelT>
+static int set_smem(KernelT kern, size_t bytes) {
+    if (bytes > 227 * 1024) return fail("shared-memory requirement exceeds 227 KB");
+    if (bytes > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return fail(cudaGetErrorString(e));
+    }
+    return 0;
+}
+
+// quadrature chunk: multiple of NG, bounded by the shared-memory budget
+static int pick_qc(int nq, size_t fixed_bytes, size_t per_q_bytes) {
+    int qc = ((nq + NG - 1) / NG) * NG;
+    if (qc > 64) qc = 64;
+    while (qc > NG && fixed_bytes + per_q_bytes * qc > 96 * 1024) qc -= NG;
+    return qc;
+}
+
+template <typename T, int DIM, int RJ>
+static int launch_volume(const wadg_problem *Pc, const void *Q, void *rhs, cudaStream_t st) {
+    Prob<T> P = make_prob<T>(*Pc);
+    constexpr int FLD = DIM + 1;
+    const bool sw = Pc->formulation == WADG_STRONG_WEAK;
+    const int NW = sw ? 2 * DIM : DIM + 1;
+    const size_t fixed = (size_t)FLD * P.Np * KB * sizeof(T);
+    const int qc = pick_qc(P.Nq, fixed, (size_t)NW * KB * sizeof(T));
+    const size_t smem = fixed + (size_t)NW * qc * KB * sizeof(T);
+    const dim3 grid(P.Kpad / KB);
+    if (sw) {
+        if (set_smem(k_volume<T, DIM, RJ, true>, smem)) return 1;
+        k_volume<T, DIM, RJ, true><<<grid, NT, smem, st>>>(P, (const T *)Q, (T *)rhs, qc);
+    } else {
+        if (set_smem(k_volume<T, DIM, RJ, false>, smem)) return 1;
+        k_volume<T, DIM, RJ, false><<<grid, NT, smem, st>>>(P, (const T *)Q, (T *)rhs, qc);
+    }
+    return check_launch("wadg_volume");
+}
+
+template <typename T, int DIM, int RJ>
+static int launch_surface(const wadg_problem *Pc, const void *Q, void *rhs, double tp, double tu,
+                          int accumulate, int b0, int b1, cudaStream_t st) {
+    Prob<T> P = make_prob<T>(*Pc);
+    constexpr int FLD = DIM + 1;
+    const int nblk = P.Kpad / KB;
+    if (b1 < 0 || b1 > nblk) b1 = nblk;
+    if (b0 < 0) b0 = 0;
+    if (b1 <= b0) return 0;
+    const size_t fixed = (size_t)FLD * 2 * P.Nfp * KB * sizeof(T);
+    const int qf = pick_qc(P.Nfq, fixed, (size_t)FLD * KB * sizeof(T));
+    const size_t smem = fixed + (size_t)FLD * qf * KB * sizeof(T);
+    const dim3 grid(b1 - b0);
+    if (Pc->formulation == WADG_STRONG_WEAK) {
+        if (set_smem(k_surface<T, DIM, RJ, true>, smem)) return 1;
+        k_surface<T, DIM, RJ, true><<<grid, NT, smem, st>>>(P, (const T *)Q, (T *)rhs, (T)tp, (T)tu,
+                                                            accumulate, b0, qf);
+    } else {
+        if (set_smem(k_surface<T, DIM, RJ, false>, smem)) return 1;
+        k_surface<T, DIM, RJ, false><<<grid, NT, smem, st>>>(P, (const T *)Q, (T *)rhs, (T)tp, (T)tu,
+                                                             accumulate, b0, qf);
+    }
+    return check_launch("wadg_surface");
+}
+
+template <typename T, int DIM, int RJ, int MODE>
+static int launch_update(const wadg_problem *Pc, const void *rhs, void *out, void *Q, double a,
+                         double b, double dt, cudaStream_t st) {
+    Prob<T> P = make_prob<T>(*Pc);
+    constexpr int FLD = DIM + 1;
+    const size_t fixed = (size_t)FLD * P.Np * KB * sizeof(T);
+    const int qc = pick_qc(P.Nqu, fixed, (size_t)FLD * KB * sizeof(T));
+    const size_t smem = fixed + (size_t)FLD * qc * KB * sizeof(T);
+    if (set_smem(k_update<T, DIM, RJ, MODE>, smem)) return 1;
+    k_update<T, DIM, RJ, MODE><<<P.Kpad / KB, NT, smem, st>>>(P, (const T *)rhs, (T *)out, (T *)Q,
+                                                              (T)a, (T)b, (T)dt, qc);
+    return check_launch("wadg_update");
+}
+
+// dispatch helpers -----------------------------------------------------------
+#define WADG_DISPATCH(P, FN, ...)                                                   \
+    do {                                                                            \
+        const int rj_ = rows_per_thread((P)->Np);                                   \
+        if ((P)->dtype == WADG_F64) {                                               \
+            if ((P)->dim == 2) {                                                    \
+                switch (rj_) {                                                      \
+                    case 2: return FN<double, 2, 2>(__VA_ARGS__);                   \
+                    case 4: return FN<double, 2, 4>(__VA_ARGS__);                   \
+                    case 8: return FN<double, 2, 8>(__VA_ARGS__);                   \
+                    default: return FN<double, 2, 16>(__VA_ARGS__);                 \
+                }                                                                   \
+            } else {                                                                \
+                switch (rj_) {                                                      \
+                    case 2: return FN<double, 3, 2>(__VA_ARGS__);                   \
+                    case 4: return FN<double, 3, 4>(__VA_ARGS__);                   \
+                    case 8: return FN<double, 3, 8>(__VA_ARGS__);                   \
+                    default: return FN<double, 3, 16>(__VA_ARGS__);                 \
+                }                                                                   \
+            }                                                                       \
+        } else {                                                                    \
+            if ((P)->dim == 2) {                                                    \
+                switch (rj_) {                                                      \
+                    case 2: return FN<float, 2, 2>(__VA_ARGS__);                    \
+                    case 4: return FN<float, 2, 4>(__VA_ARGS__);                    \
+                    case 8: return FN<float, 2, 8>(__VA_ARGS__);                    \
+                    default: return FN<float, 2, 16>(__VA_ARGS__);                  \
+                }                                                                   \
+            } else {                                                                \
+                switch (rj_) {                                                      \
+                    case 2: return FN<float, 3, 2>(__VA_ARGS__);                    \
+                    case 4: return FN<float, 3, 4>(__VA_ARGS__);                    \
+                    case 8: return FN<float, 3, 8>(__VA_ARGS__);                    \
+                    default: return FN<float, 3, 16>(__VA_ARGS__);                  \
+                }                                                                   \
+            }                                                                       \
+        }                                                                           \
+    } while (0)
+
+template <typename T, int DIM, int RJ>
+static int upd_minv(const wadg_problem *P, const void *rhs, void *out, cudaStream_t st) {
+    return launch_update<T, DIM, RJ, 0>(P, rhs, out, nullptr, 0.0, 0.0, 0.0, st);
+}
+template <typename T, int DIM, int RJ>
+static int upd_lsrk(const wadg_problem *P, const void *rhs, void *res, void *Q, double a, double b,
+                    double dt, cudaStream_t st) {
+    return launch_update<T, DIM, RJ, 1>(P, rhs, res, Q, a, b, dt, st);
+}
+
+extern "C" {
+
+int wadg_abi_version(void) { return WADG_ABI_VERSION; }
+
+const char *wadg_last_error(void) { return g_err; }
+
+int wadg_volume(const wadg_problem *P, const void *Q, void *rhs, void *stream) {
+    if (validate(P)) return 1;
+    WADG_DISPATCH(P, launch_volume, P, Q, rhs, (cudaStream_t)stream);
+}
+
+int wadg_surface(const wadg_problem *P, const void *Q, void *rhs, double tau_p, double tau_u,
+                 int accumulate, int block_begin, int block_end, void *stream) {
+    if (validate(P)) return 1;
+    if (P->n_halo > 0 && !P->halo) return fail("n_halo > 0 but halo is NULL");
+    WADG_DISPATCH(P, launch_surface, P, Q, rhs, tau_p, tau_u, accumulate, block_begin, block_end,
+                  (cudaStream_t)stream);
+}
+
+int wadg_mass_inverse(const wadg_problem *P, const void *rhs, void *out, void *stream) {
+    if (validate(P)) return 1;
+    WADG_DISPATCH(P, upd_minv, P, rhs, out, (cudaStream_t)stream);
+}
+
+int wadg_update_lsrk(const wadg_problem *P, const void *rhs, void *res, void *Q, double a, double b,
+                     double dt, void *stream) {
+    if (validate(P)) return 1;
+    WADG_DISPATCH(P, upd_lsrk, P, rhs, res, Q, a, b, dt, (cudaStream_t)stream);
+}
+
+int wadg_stage(const wadg_problem *P, void *Q, void *res, void *rhs, double tau_p, double tau_u,
+               double a, double b, double dt, void *stream) {
+    int rc = wadg_volume(P, Q, rhs, stream);
+    if (rc) return rc;
+    rc = wadg_surface(P, Q, rhs, tau_p, tau_u, 1, 0, -1, stream);
+    if (rc) return rc;
+    return wadg_update_lsrk(P, rhs, res, Q, a, b, dt, stream);
+}
+
+int wadg_lsrk_axpy(int dtype, int64_t n, const void *d, void *res, void *Q, double a, double b,
+                   double dt, void *stream) {
+    const int threads = 256;
+    int64_t blocks = (n + threads - 1) / threads;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    if (dtype == WADG_F64)
+        k_axpy<double><<<(int)blocks, threads, 0, (cudaStream_t)stream>>>(
+            n, (const double *)d, (double *)res, (double *)Q, a, b, dt);
+    else if (dtype == WADG_F32)
+        k_axpy<float><<<(int)blocks, threads, 0, (cudaStream_t)stream>>>(
+            n, (const float *)d, (float *)res, (float *)Q, (float)a, (float)b, (float)dt);
+    else
+        return fail("bad dtype");
+    return check_launch("wadg_lsrk_axpy");
+}
+
+int wadg_energy(const wadg_problem *P, const void *Q, double *partials, double *out_dev, void *stream) {
+    if (validate(P)) return 1;
+    if (!P->Ve || !P->we || !P->ewp || !P->ewu) return fail("energy quadrature data missing");
+    const int nblk = P->Kpad / KB;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (P->dtype == WADG_F64) {
+        if (P->dim == 2) k_energy<double, 2><<<nblk, NT, 0, st>>>(make_prob<double>(*P), (const double *)Q, partials);
+        else k_energy<double, 3><<<nblk, NT, 0, st>>>(make_prob<double>(*P), (const double *)Q, partials);
+    } else {
+        if (P->dim == 2) k_energy<float, 2><<<nblk, NT, 0, st>>>(make_prob<float>(*P), (const float *)Q, partials);
+        else k_energy<float, 3><<<nblk, NT, 0, st>>>(make_prob<float>(*P), (const float *)Q, partials);
+    }
+    if (check_launch("wadg_energy")) return 2;
+    k_reduce<<<1, 1024, 0, st>>>(partials, nblk, out_dev);
+    return check_launch("wadg_energy_reduce");
+}
+
+int wadg_pack_halo(const wadg_problem *P, const void *Q, const int32_t *send_k, const int32_t *send_f,
+                   int32_t n_send, void *buf, void *stream) {
+    if (validate(P)) return 1;
+    if (n_send <= 0) return 0;
+    const int64_t total = (int64_t)n_send * (P->dim + 1) * P->Nfp;
+    int blocks = (int)((total + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (P->dtype == WADG_F64) {
+        if (P->dim == 2) k_pack_halo<double, 2><<<blocks, 256, 0, st>>>(make_prob<double>(*P), (const double *)Q, send_k, send_f, n_send, (double *)buf);
+        else k_pack_halo<double, 3><<<blocks, 256, 0, st>>>(make_prob<double>(*P), (const double *)Q, send_k, send_f, n_send, (double *)buf);
+    } else {
+        if (P->dim == 2) k_pack_halo<float, 2><<<blocks, 256, 0, st>>>(make_prob<float>(*P), (const float *)Q, send_k, send_f, n_send, (float *)buf);
+        else k_pack_halo<float, 3><<<blocks, 256, 0, st>>>(make_prob<float>(*P), (const float *)Q, send_k, send_f, n_send, (float *)buf);
+    }
+    return check_launch("wadg_pack_halo");
+}
+
+}  // extern "C"

@@ -1,0 +1,238 @@
+"""Device-resident problem data: packs reference operators and per-element
+geometry into the HBM layout the kernels expect and fills the
+``wadg_problem`` C struct (include/wadg_b200.h).
+
+Layout (element index fastest, padded to Kpad, a multiple of 128):
+
+* fields        Q, res, rhs    (dim+1, Np, Kpad)
+* volume geo    (dr_a/dx_i) J  (dim*dim, Nq, Kpad)
+* face geo      n_i, sJ/2      (dim+1, Nf*Nfq, Kpad)
+* update wts    1/J, c^2/J     (Nqu, Kpad) each (c^2/J only for a variable c^2)
+* neighbours    nbr, ncode     (Nf, Kpad) int32
+
+Per-element geometry is computed on the target device in element chunks
+straight from the map nodes, so million-element meshes never materialise
+(K, Nq) float64 arrays on the host (SURVEY.md §7 hard part 5).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native, geometry, refelem
+
+PAD = 128
+CHUNK = 1 << 16
+
+
+def roundup(n, m):
+    return ((n + m - 1) // m) * m
+
+
+def torch_dtype(name):
+    return {"float64": torch.float64, "float32": torch.float32}[str(name)]
+
+
+class HaloPlan:
+    """Halo description for an element range of a partitioned mesh.
+
+    recv_slot: dict (local k, f) -> halo slot; send_k/send_f: int32 arrays of
+    the faces this rank packs (in message order); peers: list of
+    (rank, n_send, n_recv) in message order."""
+
+    def __init__(self, recv_slot, send_k, send_f, peers):
+        self.recv_slot = recv_slot
+        self.send_k = np.asarray(send_k, dtype=np.int32)
+        self.send_f = np.asarray(send_f, dtype=np.int32)
+        self.peers = peers
+
+    @property
+    def n_recv(self):
+        return len(self.recv_slot)
+
+
+def neighbour_tables(mesh, n_orient, k0=0, k1=None, halo=None):
+    """nbr / ncode (Nf, K_local) for elements [k0, k1) of ``mesh``."""
+    k1 = mesh.K if k1 is None else k1
+    conn = mesh.face_connectivity[k0:k1]
+    orient = mesh.face_orientation[k0:k1]
+    kk = conn[:, :, 0]
+    nbr = np.where(kk >= 0, kk - k0, -1).astype(np.int64)
+    ncode = np.where(kk >= 0, conn[:, :, 1] * n_orient + orient, 0).astype(np.int64)
+    outside = (kk >= 0) & ((kk < k0) | (kk >= k1))
+    if np.any(outside):
+        if halo is None:
+            raise ValueError("element range has off-range neighbours but no halo plan")
+        for k, f in zip(*np.nonzero(outside)):
+            nbr[k, f] = -2 - halo.recv_slot[(int(k), int(f))]
+    return nbr.T.astype(np.int32), ncode.T.astype(np.int32)
+
+
+class DeviceProblem:
+    """All device arrays of one (mesh range, reference elements, medium) and
+    the C struct pointing at them."""
+
+    def __init__(self, mesh, ref, ref_upd, c2, formulation_sw, dtype="float64", device="cuda",
+                 k0=0, k1=None, halo=None):
+        if not torch.cuda.is_available() and str(device).startswith("cuda"):
+            raise RuntimeError("paper_1608_03836_b200 needs a CUDA device (no CPU fallback)")
+        _native.load()
+        self.device = torch.device(device)
+        self.dtype = torch_dtype(dtype)
+        self.mesh, self.ref, self.ref_upd = mesh, ref, ref_upd
+        self.k0 = k0
+        self.k1 = mesh.K if k1 is None else k1
+        K = self.k1 - self.k0
+        self.K, self.Kpad = K, roundup(max(K, 1), PAD)
+        self.dim = mesh.shape.dim
+        self.fld = self.dim + 1
+        self.n_orient = len(refelem.orientation_permutations(mesh.shape))
+        self.sw = bool(formulation_sw)
+        self.halo = halo
+        self._keep = {}
+        self._ops()
+        self._elements(c2)
+        self.halo_buf = None
+        if halo is not None and halo.n_recv:
+            self.halo_buf = torch.zeros((halo.n_recv, self.fld, ref.nfp), dtype=self.dtype,
+                                        device=self.device)
+        self.struct = self._make_struct()
+        self._energy_ready = False
+        self.energy_partials = torch.empty(self.Kpad // _native.ELEMS_PER_BLOCK, dtype=torch.float64,
+                                           device=self.device)
+        self.energy_out = torch.empty(1, dtype=torch.float64, device=self.device)
+
+    # -- operators -----------------------------------------------------------
+    def _t(self, a, dtype=None):
+        return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype or self.dtype,
+                               device=self.device)
+
+    def _ops(self):
+        ref, ru = self.ref, self.ref_upd
+        DTW = np.stack([ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq])
+        fmask = np.array(ref.face_nodes, dtype=np.int64)
+        ext = np.empty((ref.n_faces * self.n_orient, ref.nfp), dtype=np.int64)
+        for f2 in range(ref.n_faces):
+            for o in range(self.n_orient):
+                ext[f2 * self.n_orient + o] = fmask[f2][ref.face_perms[o]]
+        self.ops = {
+            "Vq": self._t(ref.Vq), "Dq": self._t(np.stack(ref.Dq)), "Pq": self._t(ref.Pq),
+            "DTW": self._t(DTW), "Vu": self._t(ru.Vq), "Pu": self._t(ru.Pq),
+            "Vfi": self._t(ref.face_interp), "Pf": self._t(ref.Pfq),
+            "fmask": self._t(fmask, torch.int32), "ext_node": self._t(ext, torch.int32),
+            "fperm": self._t(ref.face_perms, torch.int32),
+        }
+
+    # -- per-element data ----------------------------------------------------
+    def _elements(self, c2):
+        ref, ru, dev, dt = self.ref, self.ref_upd, self.device, self.dtype
+        dim, K, Kp = self.dim, self.K, self.Kpad
+        Nq, F, Nqu = ref.Nq, ref.n_faces * ref.nfq, ru.Nq
+        self.geo = torch.zeros((dim * dim, Nq, Kp), dtype=dt, device=dev)
+        self.fgeo = torch.zeros((dim + 1, F, Kp), dtype=dt, device=dev)
+        self.wu = torch.ones((Nqu, Kp), dtype=dt, device=dev)
+        self.variable_c2 = callable(c2)
+        self.c2 = 1.0 if self.variable_c2 else float(c2)
+        self.wp = torch.ones((Nqu, Kp), dtype=dt, device=dev) if self.variable_c2 else None
+        mv = geometry.map_operators(self.mesh.shape, self.mesh.N_geo, ref).to(dev)
+        mu = geometry.map_operators(self.mesh.shape, self.mesh.N_geo, ru).to(dev)
+        X_all = self.mesh.elem_map_nodes
+        for c0 in range(0, K, CHUNK):
+            c1 = min(K, c0 + CHUNK)
+            X = torch.as_tensor(np.asarray(X_all[self.k0 + c0:self.k0 + c1], dtype=np.float64),
+                                device=dev)
+            g = geometry.geometric_factors(X, mv, k_offset=self.k0 + c0)
+            self.geo[:, :, c0:c1] = g["GJ"].reshape(dim * dim, c1 - c0, Nq).transpose(1, 2).to(dt)
+            for i in range(dim):
+                self.fgeo[i, :, c0:c1] = g["n"][i].T.to(dt)
+            self.fgeo[dim, :, c0:c1] = (0.5 * g["sJ"]).T.to(dt)
+            gu = geometry.geometric_factors(X, mu, k_offset=self.k0 + c0)
+            Ju = gu["J"]
+            self.wu[:, c0:c1] = (1.0 / Ju).T.to(dt)
+            if self.variable_c2:
+                xyz = [a.cpu().numpy() for a in gu["xq"]]
+                cv = np.array(np.broadcast_to(np.asarray(c2(*xyz), dtype=float), Ju.shape))
+                if np.any(cv <= 0) or not np.all(np.isfinite(cv)):
+                    raise ValueError("wavespeed squared must be positive")
+                self.wp[:, c0:c1] = (torch.as_tensor(cv, device=dev) / Ju).T.to(dt)
+            del g, gu, X
+        nbr, ncode = neighbour_tables(self.mesh, self.n_orient, self.k0, self.k1, self.halo)
+        self.nbr = torch.full((ref.n_faces, Kp), -1, dtype=torch.int32, device=dev)
+        self.ncode = torch.zeros((ref.n_faces, Kp), dtype=torch.int32, device=dev)
+        self.nbr[:, :K] = torch.as_tensor(nbr, device=dev)
+        self.ncode[:, :K] = torch.as_tensor(ncode, device=dev)
+        if self.halo is not None and len(self.halo.send_k):
+            self.send_k = torch.as_tensor(self.halo.send_k, device=dev)
+            self.send_f = torch.as_tensor(self.halo.send_f, device=dev)
+            self.send_buf = torch.zeros((len(self.halo.send_k), self.fld, ref.nfp), dtype=dt,
+                                        device=dev)
+
+    def prepare_energy(self, c2):
+        """Energy weights w J / c^2 and w J at the volume rule (diagnostics)."""
+        if self._energy_ready:
+            return
+        ref, dev, dt = self.ref, self.device, self.dtype
+        K, Kp, Nq = self.K, self.Kpad, ref.Nq
+        self.ewp = torch.zeros((Nq, Kp), dtype=dt, device=dev)
+        self.ewu = torch.zeros((Nq, Kp), dtype=dt, device=dev)
+        mv = geometry.map_operators(self.mesh.shape, self.mesh.N_geo, ref).to(dev)
+        for c0 in range(0, K, CHUNK):
+            c1 = min(K, c0 + CHUNK)
+            X = torch.as_tensor(np.asarray(self.mesh.elem_map_nodes[self.k0 + c0:self.k0 + c1],
+                                           dtype=np.float64), device=dev)
+            g = geometry.geometric_factors(X, mv, check=False)
+            J = g["J"]
+            if callable(c2):
+                xyz = [a.cpu().numpy() for a in g["xq"]]
+                cv = torch.as_tensor(np.broadcast_to(np.asarray(c2(*xyz), dtype=float), J.shape),
+                                     device=dev)
+            else:
+                cv = float(c2)
+            self.ewp[:, c0:c1] = (J / cv).T.to(dt)
+            self.ewu[:, c0:c1] = J.T.to(dt)
+        self.ops["Ve"] = self._t(ref.Vq)
+        self.ops["we"] = self._t(ref.wq)
+        s = self.struct
+        s.Ne = ref.Nq
+        s.Ve, s.we = self.ops["Ve"].data_ptr(), self.ops["we"].data_ptr()
+        s.ewp, s.ewu, s.e_recip = self.ewp.data_ptr(), self.ewu.data_ptr(), 0
+        self._energy_ready = True
+
+    # -- C struct ------------------------------------------------------------
+    def _make_struct(self):
+        ref, o = self.ref, self.ops
+        s = _native.WadgProblem()
+        s.dim, s.dtype = self.dim, (_native.WADG_F64 if self.dtype == torch.float64 else _native.WADG_F32)
+        s.K, s.Kpad = self.K, self.Kpad
+        s.Np, s.Nq, s.Nqu = ref.Np, ref.Nq, self.ref_upd.Nq
+        s.Nf, s.Nfp, s.Nfq = ref.n_faces, ref.nfp, ref.nfq
+        s.n_orient = self.n_orient
+        s.formulation = _native.WADG_STRONG_WEAK if self.sw else _native.WADG_STRONG
+        for name in ("Vq", "Dq", "Pq", "DTW", "Vu", "Pu", "Vfi", "Pf", "fmask", "ext_node", "fperm"):
+            setattr(s, name, o[name].data_ptr())
+        s.geo, s.fgeo, s.wu = self.geo.data_ptr(), self.fgeo.data_ptr(), self.wu.data_ptr()
+        s.wp = self.wp.data_ptr() if self.wp is not None else None
+        s.c2 = self.c2
+        s.nbr, s.ncode = self.nbr.data_ptr(), self.ncode.data_ptr()
+        s.halo = self.halo_buf.data_ptr() if self.halo_buf is not None else None
+        s.n_halo = self.halo.n_recv if self.halo is not None else 0
+        return s
+
+    def with_formulation(self, strong_weak):
+        s = _native.WadgProblem.from_buffer_copy(self.struct)
+        s.formulation = _native.WADG_STRONG_WEAK if strong_weak else _native.WADG_STRONG
+        return s
+
+    # -- fields ----------------------------------------------------------------
+    def empty_fields(self):
+        return torch.zeros((self.fld, self.ref.Np, self.Kpad), dtype=self.dtype, device=self.device)
+
+    @property
+    def n_blocks(self):
+        return self.Kpad // _native.ELEMS_PER_BLOCK
+
+    def nbytes(self):
+        tensors = [self.geo, self.fgeo, self.wu, self.nbr, self.ncode] + (
+            [self.wp] if self.wp is not None else [])
+        return sum(t.numel() * t.element_size() for t in tensors)

@@ -96,7 +96,14 @@ def build_connectivity(elem_vertices, shape):
     nbr = fverts[conn[kk, ff, 0], conn[kk, ff, 1]]
     match = nbr[:, :, None] == mine[:, None, :]                  # [n, m]
     pi = np.argmax(match, axis=2)
-    codes = np.array([lut[tuple(p)] for p in map(tuple, pi)], dtype=np.int64) if len(pi) else []
+    # encode each permutation in base nvf and map through a lookup table
+    table = np.full(nvf ** nvf, -1, dtype=np.int64)
+    for p, c in lut.items():
+        table[sum(v * nvf ** n for n, v in enumerate(p))] = c
+    key = (pi * (nvf ** np.arange(nvf))[None, :]).sum(axis=1)
+    codes = table[key]
+    if np.any(codes < 0):
+        raise ValueError("inconsistent face vertex matching")
     orient[kk, ff] = codes
     return conn, tags, orient
 

@@ -1,0 +1,177 @@
+"""Parity of the CUDA path (through the C ABI via the drop-in solver API)
+against the reference's golden vectors (2D) and the CPU oracle (2D + 3D).
+
+Bars (BASELINE.json north_star): relative L2 of (p, u) after the stated
+steps <= 1e-11 in fp64 and <= 1e-5 in fp32.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import wadg_oracle as O
+from conftest import GOLDEN_CASES, golden_mesh, load_golden
+from paper_1608_03836_b200 import meshgen, solver
+from paper_1608_03836_b200.solver import FieldState, FluxParams, Formulation, SolverConfig
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"float64": 1e-11, "float32": 1e-5}
+
+
+def rel(got, want):
+    """max over fields of ||got - want|| / ||want|| (coefficient 2-norm)."""
+    num = sum(float(np.sum((np.asarray(a) - np.asarray(b)) ** 2)) for a, b in zip(got, want))
+    den = sum(float(np.sum(np.asarray(b) ** 2)) for b in want)
+    return np.sqrt(num / den)
+
+
+def golden_disc(name, dtype="float64"):
+    g = load_golden(name)
+    mesh = golden_mesh(g)
+    form = Formulation.StrongWeak if int(g["strong_weak"]) else Formulation.Strong
+    cfg = SolverConfig(N=int(g["N"]), formulation=form,
+                       flux=FluxParams(float(g["tau_p"]), float(g["tau_u"])), dtype=dtype)
+    disc = solver.Discretization(mesh, cfg, solver.MediumField(GOLDEN_CASES[name]))
+    return g, mesh, disc
+
+
+def gfields(g, pfx):
+    return [g[f"{pfx}_p"], g[f"{pfx}_u1"], g[f"{pfx}_u2"]]
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN_CASES))
+def test_rhs_phases_match_reference(name):
+    g, mesh, disc = golden_disc(name)
+    st = FieldState(*gfields(g, "rand"))
+    sw = bool(g["strong_weak"])
+    assert rel(solver._volume_terms(st, disc, sw), gfields(g, "vol")) < 1e-13
+    assert rel(solver._surface_terms(st, disc, sw), gfields(g, "sur")) < 1e-13
+    assert rel(solver.rhs_pre_mass(st, disc).fields(), gfields(g, "pre")) < 1e-13
+    assert rel(solver.apply_mass_inverse(st, disc).fields(), gfields(g, "minv")) < 1e-13
+    assert rel(solver.rhs_full(st, disc).fields(), gfields(g, "full")) < 1e-13
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("name", sorted(GOLDEN_CASES))
+def test_lsrk_steps_match_reference(name, dtype):
+    g, mesh, disc = golden_disc(name, dtype)
+    st = FieldState(*gfields(g, "ic"))
+    for _ in range(int(g["steps"])):
+        st = solver.lsrk_step(st, float(g["dt"]), disc.rhs)
+    assert st.t == pytest.approx(float(g["end_t"]), abs=1e-15)
+    assert rel(st.fields(), gfields(g, "end")) < TOL[dtype]
+
+
+def test_config1_device_resident_20_steps_and_energy():
+    """Config 1 exactly as BASELINE.json states it: 20 steps of dt =
+    0.5 h/(N+1)^2 from the projected cos-mode, fields resident on device."""
+    g, mesh, disc = golden_disc("config1_tri")
+    Q = disc.to_device(FieldState(*gfields(g, "ic")))
+    stepper = solver.DeviceStepper(disc)
+    for _ in range(20):
+        stepper.step(Q, float(g["dt"]))
+    out = disc.from_device(Q, FieldState(*gfields(g, "ic")), 0.0)
+    assert rel(out.fields(), gfields(g, "end")) < 1e-11
+    e = solver.device_energy(disc, Q)
+    assert e == pytest.approx(float(g["energy_end"]), rel=1e-12)
+
+
+def test_run_matches_reference_diagnostics():
+    g, mesh, disc = golden_disc("config1_tri")
+    cfg = disc.config
+
+    def ic(x, y):
+        p = np.cos(np.pi * x / 2) * np.cos(np.pi * y / 2)
+        return p, 0 * p, 0 * p
+
+    def exact(x, y, t):
+        return np.cos(np.pi * x / 2) * np.cos(np.pi * y / 2) * np.cos(np.pi * np.sqrt(2) / 2 * t)
+
+    state, diag = solver.run(mesh, cfg, ic, float(g["run_T"]), exact_p=exact, n_outputs=2,
+                             dt=float(g["dt"]))
+    np.testing.assert_allclose(diag["t"], g["run_t"], atol=1e-15)
+    np.testing.assert_allclose(diag["energy"], g["run_energy"], rtol=1e-11)
+    np.testing.assert_allclose(diag["l2_error_p"], g["run_l2"], rtol=1e-6)
+
+
+def test_generic_rhs_fn_and_scalar_lsrk():
+    """lsrk_step with an arbitrary callable goes through wadg_lsrk_axpy."""
+    lam, dt = -0.37, 0.21
+    st = FieldState(np.array([[1.0]]), np.zeros((1, 1)), np.zeros((1, 1)))
+    out = solver.lsrk_step(st, dt, lambda s: FieldState(lam * s.p, 0 * s.u1, 0 * s.u2))
+    want = O.lsrk_step(O.State(np.array([[1.0]]), [np.zeros((1, 1))] * 2), dt,
+                       lambda s: O.State(lam * s.p, [0 * a for a in s.u]))
+    assert out.p[0, 0] == pytest.approx(want.p[0, 0], abs=1e-15)
+    g, mesh, disc = golden_disc("tri_strong_het")
+    st = FieldState(*gfields(g, "ic"))
+    a = solver.lsrk_step(st, 1e-3, lambda s: solver.rhs_full(s, disc))
+    b = solver.lsrk_step(st, 1e-3, disc.rhs)
+    assert rel(a.fields(), b.fields()) < 1e-14
+
+
+# ---------------------------------------------------------------------------
+# 3D: device vs oracle (no reference implementation exists)
+
+def _state3(K, Np, rng):
+    return [rng.standard_normal((K, Np)) for _ in range(4)]
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7])
+def test_3d_rhs_full_vs_oracle_degree_sweep(N, rng):
+    mesh = meshgen.warped_cube_tet_mesh(2, N)
+    for form, sw in ((Formulation.StrongWeak, True), (Formulation.Strong, False)):
+        disc = solver.Discretization(mesh, SolverConfig(N=N, formulation=form,
+                                                        flux=FluxParams(0.8, 1.1)))
+        od = O.OracleDiscretization(mesh, N, sw, 0.8, 1.1)
+        fl = _state3(mesh.K, disc.ref.Np, rng)
+        got = solver.rhs_full(FieldState.from_fields(fl), disc).fields()
+        want = O.rhs_full(O.State(fl[0], fl[1:]), od).fields()
+        assert rel(got, want) < 1e-12, (N, form)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_config2_10_steps_vs_oracle(dtype):
+    """Config 2: 8^3 x 6 warped tets (K=3072), N=3, cos-mode IC, 10 steps."""
+    mesh = meshgen.warped_cube_tet_mesh(8, 3)
+    N = 3
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype=dtype)
+    disc = solver.Discretization(mesh, cfg)
+
+    def ic(x, y, z):
+        p = np.cos(np.pi * x / 2) * np.cos(np.pi * y / 2) * np.cos(np.pi * z / 2)
+        return p, 0 * p, 0 * p, 0 * p
+
+    st = solver.project_initial_condition(mesh, cfg, ic)
+    od = O.OracleDiscretization(mesh, N, True)
+    ost = O.State(st.p, st.fields()[1:])
+    dt = 0.5 * (2.0 / 8) / (N + 1) ** 2
+    for _ in range(10):
+        st = solver.lsrk_step(st, dt, disc.rhs)
+        ost = O.lsrk_step(ost, dt, lambda y: O.rhs_full(y, od))
+    assert rel(st.fields(), ost.fields()) < TOL[dtype]
+
+
+def test_3d_heterogeneous_medium_vs_oracle(rng):
+    c2 = lambda x, y, z: 1 + 0.5 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y) * np.sin(2 * np.pi * z)
+    mesh = meshgen.warped_cube_tet_mesh(3, 3)
+    disc = solver.Discretization(mesh, SolverConfig(N=3, formulation=Formulation.StrongWeak),
+                                 solver.MediumField(c2))
+    od = O.OracleDiscretization(mesh, 3, True, c2=c2)
+    fl = _state3(mesh.K, disc.ref.Np, rng)
+    got = solver.rhs_full(FieldState.from_fields(fl), disc).fields()
+    want = O.rhs_full(O.State(fl[0], fl[1:]), od).fields()
+    assert rel(got, want) < 1e-12
+    e = solver.energy(FieldState.from_fields(fl), disc)
+    assert e == pytest.approx(O.energy(O.State(fl[0], fl[1:]), od), rel=1e-12)
+
+
+def test_device_tensor_states_stay_on_device(rng):
+    mesh = meshgen.warped_cube_tet_mesh(2, 2)
+    disc = solver.Discretization(mesh, SolverConfig(N=2, formulation=Formulation.StrongWeak))
+    fl = _state3(mesh.K, disc.ref.Np, rng)
+    dst = FieldState.from_fields([torch.as_tensor(a, device="cuda") for a in fl])
+    out = solver.rhs_full(dst, disc)
+    assert isinstance(out.p, torch.Tensor) and out.p.is_cuda
+    host = solver.rhs_full(FieldState.from_fields(fl), disc)
+    assert rel([a.cpu().numpy() for a in out.fields()], host.fields()) < 1e-15
