@@ -205,6 +205,7 @@ def main():
     ap.add_argument("--impl", default="wadg", choices=["wadg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--split", action="store_true", help="three kernels per stage instead of the fused one")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -237,22 +238,38 @@ def main():
     fl = disc.flux
     exch = getattr(disc, "exchange", None)
 
+    fused = d.fused is not None and not args.split
+    other = d.empty_fields() if fused else None
+    bufs = {"Q": Q, "other": other}
+
     def stage(a, b, ev=None):
+        Qc = bufs["Q"]
         if exch is not None:
-            exch.start(Q)
+            exch.start(Qc)
         if ev is not None:
             ev[0].record(stream)
-        _native.call("wadg_volume", ctypes.byref(d.struct), vp(Q), vp(rhs), sp)
+        if fused:
+            out = bufs["other"]
+            if exch is not None:
+                exch.fused_stage(Qc, out, res, fl.tau_p, fl.tau_u, a, b, dt, sp)
+            else:
+                _native.call("wadg_stage_fused", ctypes.byref(d.struct), vp(Qc), vp(out), vp(res),
+                             fl.tau_p, fl.tau_u, a, b, dt, 0, -1, sp)
+            bufs["Q"], bufs["other"] = out, Qc
+            if ev is not None:
+                ev[1].record(stream)
+            return
+        _native.call("wadg_volume", ctypes.byref(d.struct), vp(Qc), vp(rhs), sp)
         if ev is not None:
             ev[1].record(stream)
         if exch is not None:
-            exch.surface(Q, rhs, fl.tau_p, fl.tau_u, sp)
+            exch.surface(Qc, rhs, fl.tau_p, fl.tau_u, sp)
         else:
-            _native.call("wadg_surface", ctypes.byref(d.struct), vp(Q), vp(rhs), fl.tau_p, fl.tau_u,
+            _native.call("wadg_surface", ctypes.byref(d.struct), vp(Qc), vp(rhs), fl.tau_p, fl.tau_u,
                          1, 0, -1, sp)
         if ev is not None:
             ev[2].record(stream)
-        _native.call("wadg_update_lsrk", ctypes.byref(d.struct), vp(rhs), vp(res), vp(Q), a, b, dt, sp)
+        _native.call("wadg_update_lsrk", ctypes.byref(d.struct), vp(rhs), vp(res), vp(Qc), a, b, dt, sp)
         if ev is not None:
             ev[3].record(stream)
 
@@ -282,13 +299,13 @@ def main():
     torch.cuda.synchronize()
     ms_total = t0.elapsed_time(t1)
     clk = clocks.stop()
-    kern = {"volume": [], "surface": [], "update": []}
+    names = ["stage_fused"] if fused else ["volume", "surface", "update"]
+    kern = {k: [] for k in names}
     for i in range(args.steps):
         for s in range(5):
             e = evs[i][s]
-            kern["volume"].append(e[0].elapsed_time(e[1]))
-            kern["surface"].append(e[1].elapsed_time(e[2]))
-            kern["update"].append(e[2].elapsed_time(e[3]))
+            for m, k in enumerate(names):
+                kern[k].append(e[m].elapsed_time(e[m + 1]))
     if world > 1:
         tt = torch.tensor([ms_total], device="cuda")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -306,6 +323,13 @@ def main():
     w = 4 if cfg.dtype == "float32" else 8
     B, FL = algorithmic_model(mesh.dim, K_local, Np, ref.Nq, disc.ref_upd.Nq,
                               ref.n_faces * ref.nfq, w, 2 if callable(medium.c2) else 1)
+    if fused:
+        fldn = mesh.dim + 1
+        n_om = 2 if callable(medium.c2) else 1
+        F = ref.n_faces * ref.nfq
+        B = {"stage_fused": K_local * (w * (4 * fldn * Np + mesh.dim ** 2 * ref.Nq + n_om * disc.ref_upd.Nq
+                                            + (mesh.dim + 1) * F) + 4 * ref.n_faces)}
+        FL = {"stage_fused": sum(FL.values())}
     avg = {k: float(np.mean(v)) for k, v in kern.items()}
     top = max(avg, key=avg.get)
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -326,7 +350,7 @@ def main():
         import torch as _t
         host = [_t.empty((K_local, Np), dtype=d.dtype).pin_memory() for _ in range(mesh.dim + 1)]
         for i in range(mesh.dim + 1):
-            host[i].copy_(Q[i, :, :K_local].T.cpu())
+            host[i].copy_(bufs["Q"][i, :, :K_local].T.cpu())
         hstate = solver.FieldState.from_fields(host)
         n_e2e = max(2, min(args.steps, 5))
         hstate = solver.lsrk_step(hstate, dt, disc.rhs)
@@ -369,7 +393,8 @@ def main():
             "kernels": kernels,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": 15 * args.steps * (1 if exch is None else 1),
+            "gpu_launches": (5 if fused else 15) * args.steps,
+            "stage_kernel": "wadg_stage_fused" if fused else "wadg_volume+wadg_surface+wadg_update_lsrk",
             "clocks": clk,
             "storage_words_per_element": {"wadg_weights": 2 * Nqu, "dense_inverse": 2 * Np2,
                                           "ratio": Np2 / Nqu},

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define WADG_ABI_VERSION 1
+#define WADG_ABI_VERSION 2
 #define WADG_ELEMS_PER_BLOCK 32
 
 enum { WADG_F64 = 0, WADG_F32 = 1 };
@@ -82,6 +82,15 @@ typedef struct wadg_problem {
     const void *ewp;      /* [Ne][Kpad] */
     const void *ewu;      /* [Ne][Kpad] */
     int32_t e_recip;      /* 1: weights are we/ew*, 0: we*ew*                     */
+    /* fused tetrahedral stage (wadg_stage_fused): polynomial order and the
+     * operators repacked into quadrature chunks of QC points (see
+     * wadg_fused_config), NPP = Np rounded up to 4, zero padded:          */
+    int32_t order;
+    const void *opVA;     /* [nch][NPP][QC][4]: D_r, D_s, D_t, Vq at (q, j)       */
+    const void *opVB;     /* [nch][QC][NPP][4]: DTW_r, DTW_s, DTW_t, Pq at (j, q)  */
+    const void *opU1;     /* [nch][NPP][QC]: Vu                                    */
+    const void *opU2;     /* [nch][QC][NPP]: Pu                                    */
+    const void *liftT;    /* [Nf*Nfq][NPP]: Pf transposed                          */
 } wadg_problem;
 
 int wadg_abi_version(void);
@@ -115,6 +124,23 @@ int wadg_lsrk_axpy(int dtype, int64_t n, const void *d, void *res, void *Q,
  * out_dev[0] (device double) */
 int wadg_energy(const wadg_problem *P, const void *Q, double *partials,
                 double *out_dev, void *stream);
+
+/* Tiling of the fused tetrahedral stage for (dtype, order): elements per CTA
+ * and quadrature chunk; returns nonzero if the pair is not compiled. */
+int wadg_fused_config(int dtype, int order, int32_t *elems_per_block, int32_t *qchunk,
+                      int32_t *n_chunks, int64_t *smem_bytes);
+
+/* One whole LSRK stage for strong-weak tetrahedra in a single kernel:
+ * Q_out = Q_in + b*res, res = a*res + dt*Minv(volume + surface)(Q_in).
+ * Q_in and Q_out must be different buffers (ping-pong).  Blocks are in units
+ * of the fused elems_per_block; block_end < 0 means all. */
+int wadg_stage_fused(const wadg_problem *P, const void *Q_in, void *Q_out, void *res,
+                     double tau_p, double tau_u, double a, double b, double dt,
+                     int block_begin, int block_end, void *stream);
+
+/* Debug: when buf != NULL, each CTA of subsequent wadg_stage_fused launches
+ * writes clock64() at 7 phase boundaries to buf[cta*8 + 0..6] (int64). */
+int wadg_debug_set_phase_clock_buffer(void *buf);
 
 /* buf[(s*(dim+1) + fld)*Nfp + i] = Q[fld][fmask[send_f[s]][i]][send_k[s]] */
 int wadg_pack_halo(const wadg_problem *P, const void *Q, const int32_t *send_k,

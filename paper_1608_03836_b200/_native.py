@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 WADG_F64, WADG_F32 = 0, 1
 WADG_STRONG, WADG_STRONG_WEAK = 0, 1
 ELEMS_PER_BLOCK = 32
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -34,6 +34,7 @@ class WadgProblem(ctypes.Structure):
         ("nbr", _vp), ("ncode", _vp),
         ("halo", _vp), ("n_halo", _i32),
         ("Ne", _i32), ("Ve", _vp), ("we", _vp), ("ewp", _vp), ("ewu", _vp), ("e_recip", _i32),
+        ("order", _i32), ("opVA", _vp), ("opVB", _vp), ("opU1", _vp), ("opU2", _vp), ("liftT", _vp),
     ]
 
 
@@ -51,6 +52,12 @@ EXPORTS = {
     "wadg_lsrk_axpy": ([ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp, ctypes.c_double,
                         ctypes.c_double, ctypes.c_double, _vp], ctypes.c_int),
     "wadg_energy": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, _vp], ctypes.c_int),
+    "wadg_fused_config": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                           ctypes.POINTER(_i32), ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "wadg_stage_fused": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, ctypes.c_double, ctypes.c_double,
+                          ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                          _vp], ctypes.c_int),
+    "wadg_debug_set_phase_clock_buffer": ([_vp], ctypes.c_int),
     "wadg_pack_halo": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, _i32, _vp, _vp], ctypes.c_int),
 }
 
@@ -85,3 +92,16 @@ def call(name, *args):
     rc = getattr(lib, name)(*args)
     if rc != 0:
         raise NativeError(f"{name} failed ({rc}): {lib.wadg_last_error().decode()}")
+
+
+def fused_config(dtype_code, order):
+    """(elems_per_block, qchunk, n_chunks, smem_bytes) of the fused stage, or
+    None when (dtype, order) is not compiled / does not fit."""
+    lib = load()
+    kb, qc, nch = _i32(), _i32(), _i32()
+    smem = ctypes.c_int64()
+    rc = lib.wadg_fused_config(dtype_code, order, ctypes.byref(kb), ctypes.byref(qc),
+                               ctypes.byref(nch), ctypes.byref(smem))
+    if rc != 0:
+        return None
+    return kb.value, qc.value, nch.value, smem.value

@@ -24,6 +24,10 @@
 #include "wadg_b200.h"
 
 namespace wadg {
+}
+#include "wadg_fused.cuh"
+
+namespace wadg {
 
 constexpr int KB = WADG_ELEMS_PER_BLOCK;
 constexpr int NT = 256;
@@ -631,6 +635,67 @@ static int upd_lsrk(const wadg_problem *P, const void *rhs, void *res, void *Q, 
     return launch_update<T, DIM, RJ, 1>(P, rhs, res, Q, a, b, dt, st);
 }
 
+// ---- fused tetrahedral stage -------------------------------------------------
+static long long *g_prof = nullptr;   // debug: per-CTA phase clocks of the next fused launches
+
+template <typename T>
+static fused::FProb<T> make_fprob(const wadg_problem &p) {
+    fused::FProb<T> q;
+    q.K = p.K; q.Kpad = p.Kpad;
+    q.opVA = (const T *)p.opVA; q.opVB = (const T *)p.opVB; q.opU1 = (const T *)p.opU1;
+    q.opU2 = (const T *)p.opU2; q.liftT = (const T *)p.liftT; q.Vfi = (const T *)p.Vfi;
+    q.fmask = p.fmask; q.ext_node = p.ext_node; q.fperm = p.fperm;
+    q.geo = (const T *)p.geo; q.fgeo = (const T *)p.fgeo; q.wu = (const T *)p.wu;
+    q.wp = (const T *)p.wp; q.c2 = (T)p.c2; q.nbr = p.nbr; q.ncode = p.ncode;
+    q.halo = (const T *)p.halo; q.nor = p.n_orient;
+    q.prof = g_prof;
+    return q;
+}
+
+template <typename T, int N>
+static int fused_cfg(int32_t *kb, int32_t *qc, int32_t *nch, int64_t *smem) {
+    using C = fused::Cfg<T, N>;
+    if (kb) *kb = C::KB;
+    if (qc) *qc = C::QC;
+    if (nch) *nch = C::NCH;
+    if (smem) *smem = (int64_t)C::SMEM;
+    return C::SMEM <= 227 * 1024 ? 0 : 1;
+}
+
+template <typename T, int N>
+static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
+                        double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
+    using C = fused::Cfg<T, N>;
+    if (C::SMEM > 227 * 1024) return fail("fused stage does not fit shared memory for this order");
+    if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
+    const int nblk = Pc->Kpad / C::KB;
+    if (b1 < 0 || b1 > nblk) b1 = nblk;
+    if (b0 < 0) b0 = 0;
+    if (b1 <= b0) return 0;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(fused::k_stage_fused<T, N>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        if (e != cudaSuccess) return fail(cudaGetErrorString(e));
+        attr_set = true;
+    }
+    fused::k_stage_fused<T, N><<<b1 - b0, fused::NTF, C::SMEM, st>>>(
+        make_fprob<T>(*Pc), (const T *)Qin, (T *)Qout, (T *)res, (T)tp, (T)tu, (T)a, (T)b, (T)dt, b0);
+    return check_launch("wadg_stage_fused");
+}
+
+#define WADG_FUSED_SWITCH(T, N, FN, ...)          \
+    switch (N) {                                  \
+        case 1: return FN<T, 1>(__VA_ARGS__);     \
+        case 2: return FN<T, 2>(__VA_ARGS__);     \
+        case 3: return FN<T, 3>(__VA_ARGS__);     \
+        case 4: return FN<T, 4>(__VA_ARGS__);     \
+        case 5: return FN<T, 5>(__VA_ARGS__);     \
+        case 6: return FN<T, 6>(__VA_ARGS__);     \
+        case 7: return FN<T, 7>(__VA_ARGS__);     \
+        default: return fail("fused stage compiled for N = 1..7 only"); \
+    }
+
 extern "C" {
 
 int wadg_abi_version(void) { return WADG_ABI_VERSION; }
@@ -720,6 +785,34 @@ int wadg_pack_halo(const wadg_problem *P, const void *Q, const int32_t *send_k, 
         else k_pack_halo<float, 3><<<blocks, 256, 0, st>>>(make_prob<float>(*P), (const float *)Q, send_k, send_f, n_send, (float *)buf);
     }
     return check_launch("wadg_pack_halo");
+}
+
+int wadg_debug_set_phase_clock_buffer(void *buf) {
+    g_prof = (long long *)buf;
+    return 0;
+}
+
+int wadg_fused_config(int dtype, int order, int32_t *kb, int32_t *qc, int32_t *nch, int64_t *smem) {
+    if (dtype == WADG_F64) { WADG_FUSED_SWITCH(double, order, fused_cfg, kb, qc, nch, smem); }
+    if (dtype == WADG_F32) { WADG_FUSED_SWITCH(float, order, fused_cfg, kb, qc, nch, smem); }
+    return fail("bad dtype");
+}
+
+int wadg_stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void *res, double tau_p,
+                     double tau_u, double a, double b, double dt, int block_begin, int block_end,
+                     void *stream) {
+    if (validate(P)) return 1;
+    if (P->dim != 3 || P->formulation != WADG_STRONG_WEAK) return fail("fused stage: 3D strong-weak only");
+    if (!P->opVA || !P->opVB || !P->opU1 || !P->opU2 || !P->liftT) return fail("fused operators not packed");
+    if (Qin == Qout) return fail("fused stage needs distinct Q_in / Q_out buffers");
+    if (P->n_halo > 0 && !P->halo) return fail("n_halo > 0 but halo is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (P->dtype == WADG_F64) {
+        WADG_FUSED_SWITCH(double, P->order, fused_launch, P, Qin, Qout, res, tau_p, tau_u, a, b, dt,
+                          block_begin, block_end, st);
+    }
+    WADG_FUSED_SWITCH(float, P->order, fused_launch, P, Qin, Qout, res, tau_p, tau_u, a, b, dt,
+                      block_begin, block_end, st);
 }
 
 }  // extern "C"

@@ -98,6 +98,7 @@ class DeviceProblem:
             self.halo_buf = torch.zeros((halo.n_recv, self.fld, ref.nfp), dtype=self.dtype,
                                         device=self.device)
         self.struct = self._make_struct()
+        self.fused = self._fused_ops()
         self._energy_ready = False
         self.energy_partials = torch.empty(self.Kpad // _native.ELEMS_PER_BLOCK, dtype=torch.float64,
                                            device=self.device)
@@ -167,6 +168,46 @@ class DeviceProblem:
             self.send_f = torch.as_tensor(self.halo.send_f, device=dev)
             self.send_buf = torch.zeros((len(self.halo.send_k), self.fld, ref.nfp), dtype=dt,
                                         device=dev)
+
+    def _fused_ops(self):
+        """Repack the operators for wadg_stage_fused (3D strong-weak with the
+        default (N+1)^3 volume/update rules); returns the fused block size or
+        None when the fused stage does not apply."""
+        ref, ru = self.ref, self.ref_upd
+        N = ref.N
+        if not (self.dim == 3 and self.sw and ref.Nq == (N + 1) ** 3 and ru.Nq == (N + 1) ** 3
+                and ref.nfq == (N + 1) ** 2):
+            return None
+        code = _native.WADG_F64 if self.dtype == torch.float64 else _native.WADG_F32
+        cfg = _native.fused_config(code, N)
+        if cfg is None:
+            return None
+        kb, qc, nch, _ = cfg
+        NP, NQ = ref.Np, ref.Nq
+        NPP = roundup(NP, 4)
+        NQP = nch * qc
+        DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
+        A = np.zeros((NQP, NPP, 4))
+        A[:NQ, :NP] = np.stack(list(ref.Dq) + [ref.Vq], axis=-1)
+        opVA = A.reshape(nch, qc, NPP, 4).transpose(0, 2, 1, 3)
+        B = np.zeros((NPP, NQP, 4))
+        B[:NP, :NQ] = np.stack(DTW + [ref.Pq], axis=-1)
+        opVB = B.reshape(NPP, nch, qc, 4).transpose(1, 2, 0, 3)
+        U1 = np.zeros((NQP, NPP))
+        U1[:NQ, :NP] = ru.Vq
+        opU1 = U1.reshape(nch, qc, NPP).transpose(0, 2, 1)
+        U2 = np.zeros((NPP, NQP))
+        U2[:NP, :NQ] = ru.Pq
+        opU2 = U2.reshape(NPP, nch, qc).transpose(1, 2, 0)
+        L = np.zeros((ref.n_faces * ref.nfq, NPP))
+        L[:, :NP] = ref.Pfq.T
+        for name, arr in (("opVA", opVA), ("opVB", opVB), ("opU1", opU1), ("opU2", opU2), ("liftT", L)):
+            self.ops[name] = self._t(arr)
+            setattr(self.struct, name, self.ops[name].data_ptr())
+        self.struct.order = N
+        if self.Kpad % kb:
+            return None
+        return kb
 
     def prepare_energy(self, c2):
         """Energy weights w J / c^2 and w J at the volume rule (diagnostics)."""

@@ -107,6 +107,10 @@ class HaloExchange:
         blk = halo_blocks(d, _native.ELEMS_PER_BLOCK)
         self.free_runs = _runs(blk, False)
         self.halo_runs = _runs(blk, True)
+        if d.fused is not None:
+            fblk = halo_blocks(d, d.fused)
+            self.free_runs_f = _runs(fblk, False)
+            self.halo_runs_f = _runs(fblk, True)
         self.reqs = []
 
     def start(self, Q):
@@ -137,6 +141,21 @@ class HaloExchange:
         for b0, b1 in self.halo_runs:
             self.native.call("wadg_surface", ctypes.byref(d.struct), vp(Q), vp(rhs), tau_p, tau_u,
                              1, b0, b1, sp)
+
+
+    def fused_stage(self, Qin, Qout, res, tau_p, tau_u, a, b, dt, sp):
+        """Fused stage: interface-free element blocks while the halo is in
+        flight, then the blocks that read halo slots."""
+        d = self.disc.dev
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())
+        args = (ctypes.byref(d.struct), vp(Qin), vp(Qout), vp(res), tau_p, tau_u, a, b, dt)
+        for b0, b1 in self.free_runs_f:
+            self.native.call("wadg_stage_fused", *args, b0, b1, sp)
+        for r in self.reqs:
+            r.wait()
+        self.reqs = []
+        for b0, b1 in self.halo_runs_f:
+            self.native.call("wadg_stage_fused", *args, b0, b1, sp)
 
 
 def slab_discretization(mesh, config, medium, rank, world, n_layers, group=None):

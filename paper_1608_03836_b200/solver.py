@@ -438,25 +438,38 @@ LSRK4C = (
 
 
 class DeviceStepper:
-    """Device-resident LSRK45 driver: Q, res and rhs scratch live in HBM; one
-    step is 5 stages of (volume, surface, update+axpy) kernel launches."""
+    """Device-resident LSRK45 driver.  For 3D strong-weak problems each stage
+    is one fused kernel (wadg_stage_fused) reading Q from one buffer and
+    writing the other; otherwise a stage is the volume, surface and
+    update+axpy kernels in place.  ``step`` returns the buffer that holds the
+    new state."""
 
-    def __init__(self, disc):
+    def __init__(self, disc, fused=None):
         self.disc = disc
         d = disc.dev
+        self.fused = (d.fused is not None) if fused is None else (fused and d.fused is not None)
         self.res = d.empty_fields()
-        self.rhs = d.empty_fields()
+        self.rhs = None if self.fused else d.empty_fields()
+        self.other = d.empty_fields() if self.fused else None
 
     def stage(self, Q, a, b, dt):
         import ctypes
         d = self.disc.dev
         fl = self.disc.flux
+        if self.fused:
+            out = self.other
+            _native.call("wadg_stage_fused", ctypes.byref(d.struct), _vp(Q), _vp(out), _vp(self.res),
+                         fl.tau_p, fl.tau_u, a, b, dt, 0, -1, _stream())
+            self.other = Q
+            return out
         _native.call("wadg_stage", ctypes.byref(d.struct), _vp(Q), _vp(self.res), _vp(self.rhs),
                      fl.tau_p, fl.tau_u, a, b, dt, _stream())
+        return Q
 
     def step(self, Q, dt):
         for a, b in zip(LSRK4A, LSRK4B):
-            self.stage(Q, a, b, dt)
+            Q = self.stage(Q, a, b, dt)
+        return Q
 
 
 def lsrk_step(state, dt, rhs_fn):
@@ -465,7 +478,7 @@ def lsrk_step(state, dt, rhs_fn):
         disc = rhs_fn.disc
         _check_state(state, disc)
         Q = disc.to_device(state)
-        DeviceStepper(disc).step(Q, dt)
+        Q = DeviceStepper(disc).step(Q, dt)
         return disc.from_device(Q, state, state.t + dt)
     return _generic_lsrk_step(state, dt, rhs_fn)
 
@@ -616,7 +629,7 @@ def run(mesh, config, initial_fn, T, medium=MediumField(), exact_p=None, n_outpu
     for target in sample_ts[1:]:
         while t < target - 1e-12:
             step = min(dt, target - t)
-            stepper.step(Q, step)
+            Q = stepper.step(Q, step)
             t = t + step
         t = float(target)
         e = record(t)

@@ -1,0 +1,61 @@
+"""Per-phase SM-clock breakdown of the fused stage kernel (debug tool).
+
+    python scripts/phase_clock.py --n 32 --order 4 --dtype float32
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import __graft_entry__  # noqa: E402
+
+__graft_entry__.build()
+from paper_1608_03836_b200 import _native, meshgen, solver  # noqa: E402
+
+PHASES = ["stage Q", "volume", "gather", "flux+lift", "update", "write"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=32)
+    ap.add_argument("--order", type=int, default=4)
+    ap.add_argument("--dtype", default="float32")
+    args = ap.parse_args()
+    mesh = meshgen.warped_cube_tet_mesh(args.n, args.order)
+    cfg = solver.SolverConfig(N=args.order, formulation=solver.Formulation.StrongWeak, dtype=args.dtype)
+    disc = solver.Discretization(mesh, cfg)
+    d = disc.dev
+    kb = d.fused
+    nblk = d.Kpad // kb
+    buf = torch.zeros(nblk * 8, dtype=torch.int64, device="cuda")
+    Q = d.empty_fields().normal_()
+    Q2, res = d.empty_fields(), d.empty_fields()
+    sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    vp = lambda t: ctypes.c_void_p(t.data_ptr())
+    for it in range(3):
+        if it == 2:
+            _native.call("wadg_debug_set_phase_clock_buffer", vp(buf))
+        _native.call("wadg_stage_fused", ctypes.byref(d.struct), vp(Q), vp(Q2), vp(res), 1.0, 1.0,
+                     0.0, 0.1, 1e-3, 0, -1, sp)
+    _native.call("wadg_debug_set_phase_clock_buffer", ctypes.c_void_p(0))
+    torch.cuda.synchronize()
+    t = buf.view(nblk, 8)[:, :7].cpu().numpy().astype(np.float64)
+    dur = np.diff(t, axis=1)
+    med = np.median(dur, axis=0)
+    tot = med.sum()
+    out = {"K": mesh.K, "N": args.order, "dtype": args.dtype, "elems_per_block": kb,
+           "cycles_per_cta_median": float(tot),
+           "phases": {p: {"cycles": float(c), "share": float(c / tot)} for p, c in zip(PHASES, med)}}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -70,7 +70,7 @@ def test_config1_device_resident_20_steps_and_energy():
     Q = disc.to_device(FieldState(*gfields(g, "ic")))
     stepper = solver.DeviceStepper(disc)
     for _ in range(20):
-        stepper.step(Q, float(g["dt"]))
+        Q = stepper.step(Q, float(g["dt"]))
     out = disc.from_device(Q, FieldState(*gfields(g, "ic")), 0.0)
     assert rel(out.fields(), gfields(g, "end")) < 1e-11
     e = solver.device_energy(disc, Q)
@@ -175,3 +175,33 @@ def test_device_tensor_states_stay_on_device(rng):
     assert isinstance(out.p, torch.Tensor) and out.p.is_cuda
     host = solver.rhs_full(FieldState.from_fields(fl), disc)
     assert rel([a.cpu().numpy() for a in out.fields()], host.fields()) < 1e-15
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7])
+def test_fused_stage_matches_split_kernels_and_oracle(N, dtype, rng):
+    """wadg_stage_fused (one kernel per stage, ping-pong Q) against the
+    three-kernel stage and the oracle, heterogeneous medium, 2 steps."""
+    c2 = lambda x, y, z: 1 + 0.5 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y) * np.sin(2 * np.pi * z)
+    mesh = meshgen.warped_cube_tet_mesh(3, N)
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, flux=FluxParams(0.9, 1.2), dtype=dtype)
+    disc = solver.Discretization(mesh, cfg, solver.MediumField(c2))
+    assert disc.dev.fused is not None
+    fl = _state3(mesh.K, disc.ref.Np, rng)
+    st = FieldState.from_fields(fl)
+    Qf = disc.to_device(st)
+    Qs = Qf.clone()
+    sf, ss = solver.DeviceStepper(disc, fused=True), solver.DeviceStepper(disc, fused=False)
+    assert sf.fused and not ss.fused
+    dt = 2e-3
+    for _ in range(2):
+        Qf = sf.step(Qf, dt)
+        Qs = ss.step(Qs, dt)
+    a = disc.from_device(Qf, st, 0.0).fields()
+    b = disc.from_device(Qs, st, 0.0).fields()
+    assert rel(a, b) < (1e-13 if dtype == "float64" else 2e-6)
+    od = O.OracleDiscretization(mesh, N, True, 0.9, 1.2, c2=c2)
+    ost = O.State(fl[0], fl[1:])
+    for _ in range(2):
+        ost = O.lsrk_step(ost, dt, lambda y: O.rhs_full(y, od))
+    assert rel(a, ost.fields()) < TOL[dtype]
