@@ -160,6 +160,47 @@ def cpu_oracle_rate(cfg_name, n_sample, steps, N_override=None):
     return dof * 5 * steps / el / 1e9, mesh.K, el
 
 
+def reference_2d_calibration(K1D=64, N=4, steps=2):
+    """Time the UNMODIFIED reference package (baseline/_ref, 2D only) and the
+    numpy oracle port on the same warped-triangle mesh, so the port timing
+    used for the 3D workload is calibrated against the real reference."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "wadg")):
+        return {"unavailable": "baseline/_ref not installed"}
+    sys.path.insert(0, ref_dir)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        from wadg import meshgen as rmg, refelem as rrf, solver as rsv
+    except Exception as exc:                     # pragma: no cover
+        return {"unavailable": f"reference import failed: {exc}"}
+    import wadg_oracle as O
+    from paper_1608_03836_b200 import meshgen
+    m = meshgen.warped_triangle_mesh(K1D, N)
+    rm = rmg.CurvedMesh2D(shape=rrf.ElementShape.Triangle, N_geo=m.N_geo, elem_map_nodes=m.elem_map_nodes,
+                          face_connectivity=m.face_connectivity, boundary_tags=m.boundary_tags, h=m.h)
+    cfg = rsv.SolverConfig(N=N, formulation=rsv.Formulation.StrongWeak)
+    rd = rsv.Discretization(rm, cfg)
+    rng = np.random.default_rng(0)
+    st = rsv.FieldState(*(rng.standard_normal((m.K, rd.ref.Np)) for _ in range(3)))
+    dt = 1e-4
+    st = rsv.lsrk_step(st, dt, lambda y: rsv.rhs_full(y, rd))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st = rsv.lsrk_step(st, dt, lambda y: rsv.rhs_full(y, rd))
+    t_ref = (time.perf_counter() - t0) / steps
+    od = O.OracleDiscretization(m, N, True)
+    ost = O.State(st.p, [st.u1, st.u2])
+    ost = O.lsrk_step(ost, dt, lambda y: O.rhs_full(y, od))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        ost = O.lsrk_step(ost, dt, lambda y: O.rhs_full(y, od))
+    t_port = (time.perf_counter() - t0) / steps
+    dof = 3 * m.K * rd.ref.Np * 5
+    return {"mesh": f"warped triangles {K1D}x{K1D}x2 = {m.K}, N={N}, strong-weak",
+            "reference_gdofs": dof / t_ref / 1e9, "port_gdofs": dof / t_port / 1e9,
+            "port_over_reference_speed": t_ref / t_port}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -190,6 +231,7 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_2d_calibration": reference_2d_calibration(),
     }
     print(json.dumps(line))
 
@@ -339,6 +381,14 @@ def main():
             hbm_peak = float(json.load(f)["hbm_gbs"])
         peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     achieved = B[top] / (avg[top] * 1e-3) / 1e9
+    # measured DRAM traffic per launch from the committed ncu --set full capture
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"r01_ncu_stage_fused_{'f32' if cfg.dtype == 'float32' else 'f64'}"
+                         f"_N{N}_{args.config}.json")
+    if fused and world == 1 and os.path.exists(tpath):
+        with open(tpath) as f:
+            nd = json.load(f)
+        traffic = (float(nd["dram__bytes_read.sum"][0]) + float(nd["dram__bytes_write.sum"][0])) * 1e9
     kernels = {k: {"ms": avg[k], "GB/s": B[k] / (avg[k] * 1e-3) / 1e9,
                    "hbm_frac": B[k] / (avg[k] * 1e-3) / 1e9 / hbm_peak,
                    "TFLOP/s": FL[k] / (avg[k] * 1e-3) / 1e12,
@@ -387,7 +437,7 @@ def main():
                        "dt": dt, "l2": "inputs > L2 (fields+geometry ~GBs); no flush needed",
                        "parallelism": f"z-slabs x{world}", "setup_s": round(setup_s, 1)},
             "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": B[top],
                          "fp_achieved_tflops": FL[top] / (avg[top] * 1e-3) / 1e12},
             "kernels": kernels,

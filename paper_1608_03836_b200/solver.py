@@ -273,21 +273,20 @@ class Discretization:
         return Q
 
     def from_device(self, Q, like, t):
-        """Inverse of to_device, returning the container type of ``like``."""
+        """Inverse of to_device, returning the container type of ``like``.
+        The (dim+1, Np, K) -> (dim+1, K, Np) transpose happens on the device so
+        the device-to-host copy is one contiguous transfer."""
         d = self.dev
-        out = []
-        for i in range(d.fld):
-            a = Q[i, :, :d.K].T
-            if isinstance(like.p, torch.Tensor) and like.p.is_cuda:
-                out.append(a.contiguous())
-            elif isinstance(like.p, torch.Tensor):
-                h = torch.empty((d.K, a.shape[1]), dtype=like.p.dtype,
-                                pin_memory=like.p.is_pinned())
-                h.copy_(a)
-                out.append(h)
-            else:
-                out.append(a.to(torch.float64).cpu().numpy())
-        return FieldState.from_fields(out, t)
+        Qt = Q[:, :, :d.K].transpose(1, 2)
+        if isinstance(like.p, torch.Tensor) and like.p.is_cuda:
+            return FieldState.from_fields([a.contiguous() for a in Qt], t)
+        if isinstance(like.p, torch.Tensor):
+            dev = Qt.to(like.p.dtype).contiguous()
+            h = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=like.p.is_pinned())
+            h.copy_(dev)
+            return FieldState.from_fields(list(h.unbind(0)), t)
+        h = Qt.to(torch.float64).contiguous().cpu().numpy()
+        return FieldState.from_fields([h[i] for i in range(d.fld)], t)
 
 
 def _stream():
