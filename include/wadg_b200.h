@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define WADG_ABI_VERSION 2
+#define WADG_ABI_VERSION 3
 #define WADG_ELEMS_PER_BLOCK 32
 
 enum { WADG_F64 = 0, WADG_F32 = 1 };
@@ -86,11 +86,11 @@ typedef struct wadg_problem {
      * operators repacked into quadrature chunks of QC points (see
      * wadg_fused_config), NPP = Np rounded up to 4, zero padded:          */
     int32_t order;
-    const void *opVA;     /* [nch][NPP][QC][4]: D_r, D_s, D_t, Vq at (q, j)       */
-    const void *opVB;     /* [nch][QC][NPP][4]: DTW_r, DTW_s, DTW_t, Pq at (j, q)  */
-    const void *opU1;     /* [nch][NPP][QC]: Vu                                    */
-    const void *opU2;     /* [nch][QC][NPP]: Pu                                    */
-    const void *liftT;    /* [Nf*Nfq][NPP]: Pf transposed                          */
+    const void *opVA;     /* D_r, D_s, D_t, Vq at (q, j)   (layout: wadg_fused_config) */
+    const void *opVB;     /* DTW_r, DTW_s, DTW_t, Pq at (j, q)                         */
+    const void *opU1;     /* Vu                                                        */
+    const void *opU2;     /* Pu                                                        */
+    const void *liftT;    /* Pf transposed                                             */
 } wadg_problem;
 
 int wadg_abi_version(void);
@@ -125,10 +125,21 @@ int wadg_lsrk_axpy(int dtype, int64_t n, const void *d, void *res, void *Q,
 int wadg_energy(const wadg_problem *P, const void *Q, double *partials,
                 double *out_dev, void *stream);
 
-/* Tiling of the fused tetrahedral stage for (dtype, order): elements per CTA
- * and quadrature chunk; returns nonzero if the pair is not compiled. */
-int wadg_fused_config(int dtype, int order, int32_t *elems_per_block, int32_t *qchunk,
-                      int32_t *n_chunks, int64_t *smem_bytes);
+/* Layout of the fused tetrahedral stage for (dtype, order), which decides how
+ * the host packs opVA/opVB/opU1/opU2/liftT:
+ *   info[0] kind: 0 = CUDA-core kernel ([nch][NPP][QC][4], [nch][QC][NPP][4],
+ *                 [nch][NPP][QC], [nch][QC][NPP], [Nf*Nfq][NPP]);
+ *                 1 = tensor-core kernel ([nch][4][NPP][QCS], [nch][4][QC][NJS],
+ *                 [nch][NPP][QCS], [nch][QC][NJS], [Nf][NFQ8][NJS])
+ *   info[1] elements per CTA, [2] QC, [3] nch, [4] NPP (K extent over nodes),
+ *   info[5] QCS, [6] NJS (row strides), [7] NFQ8 (padded face points).
+ * Returns nonzero if the pair is not compiled / does not fit. */
+int wadg_fused_config(int dtype, int order, int32_t *info, int64_t *smem_bytes);
+
+/* Debug: force the fused-stage kernel (0: CUDA-core FMA tiles, 1: split-TF32
+ * tensor-core MMA where available); -1 restores the default.  Affects
+ * wadg_fused_config, so set it before building a problem. */
+int wadg_debug_set_fused_variant(int variant);
 
 /* One whole LSRK stage for strong-weak tetrahedra in a single kernel:
  * Q_out = Q_in + b*res, res = a*res + dt*Minv(volume + surface)(Q_in).
@@ -141,6 +152,11 @@ int wadg_stage_fused(const wadg_problem *P, const void *Q_in, void *Q_out, void 
 /* Debug: when buf != NULL, each CTA of subsequent wadg_stage_fused launches
  * writes clock64() at 7 phase boundaries to buf[cta*8 + 0..6] (int64). */
 int wadg_debug_set_phase_clock_buffer(void *buf);
+
+/* Measurement support: `blocks` x 256 threads, each running 16 independent
+ * register-operand FMA chains for `iters` iterations (2*16*iters flops per
+ * thread); `in` holds >= 32 values of the dtype, `out` >= 256. */
+int wadg_microbench_fma(int dtype, int blocks, int iters, const void *in, void *out, void *stream);
 
 /* buf[(s*(dim+1) + fld)*Nfp + i] = Q[fld][fmask[send_f[s]][i]][send_k[s]] */
 int wadg_pack_halo(const wadg_problem *P, const void *Q, const int32_t *send_k,

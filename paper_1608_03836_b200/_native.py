@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 WADG_F64, WADG_F32 = 0, 1
 WADG_STRONG, WADG_STRONG_WEAK = 0, 1
 ELEMS_PER_BLOCK = 32
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -52,12 +52,14 @@ EXPORTS = {
     "wadg_lsrk_axpy": ([ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp, ctypes.c_double,
                         ctypes.c_double, ctypes.c_double, _vp], ctypes.c_int),
     "wadg_energy": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, _vp], ctypes.c_int),
-    "wadg_fused_config": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i32), ctypes.POINTER(_i32),
-                           ctypes.POINTER(_i32), ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "wadg_fused_config": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i32),
+                           ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "wadg_debug_set_fused_variant": ([ctypes.c_int], ctypes.c_int),
     "wadg_stage_fused": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, ctypes.c_double, ctypes.c_double,
                           ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                           _vp], ctypes.c_int),
     "wadg_debug_set_phase_clock_buffer": ([_vp], ctypes.c_int),
+    "wadg_microbench_fma": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
     "wadg_pack_halo": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, _i32, _vp, _vp], ctypes.c_int),
 }
 
@@ -73,10 +75,11 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("WADG_LIB", LIB_PATH)    # experiments: alternative in-tree build
+    if not os.path.exists(path):
         raise NativeError(
-            f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
-    lib = ctypes.CDLL(LIB_PATH)
+            f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
     for name, (args, res) in EXPORTS.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -95,13 +98,14 @@ def call(name, *args):
 
 
 def fused_config(dtype_code, order):
-    """(elems_per_block, qchunk, n_chunks, smem_bytes) of the fused stage, or
-    None when (dtype, order) is not compiled / does not fit."""
+    """Layout of the fused stage for (dtype, order) as a dict, or None when
+    the pair is not compiled / does not fit (see include/wadg_b200.h)."""
     lib = load()
-    kb, qc, nch = _i32(), _i32(), _i32()
+    info = (_i32 * 8)()
     smem = ctypes.c_int64()
-    rc = lib.wadg_fused_config(dtype_code, order, ctypes.byref(kb), ctypes.byref(qc),
-                               ctypes.byref(nch), ctypes.byref(smem))
-    if rc != 0:
+    if lib.wadg_fused_config(dtype_code, order, info, ctypes.byref(smem)) != 0:
         return None
-    return kb.value, qc.value, nch.value, smem.value
+    keys = ("kind", "kb", "qc", "nch", "npp", "qcs", "njs", "nfq8")
+    out = dict(zip(keys, list(info)))
+    out["smem"] = smem.value
+    return out

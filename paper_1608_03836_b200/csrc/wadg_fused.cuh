@@ -23,6 +23,14 @@
 
 #pragma once
 
+// unroll factor of the GEMM k-loops (compile-time trip counts)
+#ifndef WADG_KUNROLL_N
+#define WADG_KUNROLL_N 8
+#endif
+#define WADG_PRAGMA(x) _Pragma(#x)
+#define WADG_KUNROLL_I(n) WADG_PRAGMA(unroll n)
+#define WADG_KUNROLL WADG_KUNROLL_I(WADG_KUNROLL_N)
+
 namespace wadg {
 namespace fused {
 
@@ -30,6 +38,7 @@ __host__ __device__ constexpr int np_tet(int N) { return (N + 1) * (N + 2) * (N 
 __host__ __device__ constexpr int nfp_tri(int N) { return (N + 1) * (N + 2) / 2; }
 __host__ __device__ constexpr int rup(int a, int b) { return ((a + b - 1) / b) * b; }
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ constexpr size_t maxz(size_t a, size_t b) { return a > b ? a : b; }
 
 constexpr int NTF = 256;   // threads per CTA
 
@@ -183,6 +192,9 @@ __device__ __forceinline__ void cp_async_elem(T *dst, const T *src) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
     }
 }
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int PENDING>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(PENDING) : "memory"); }
@@ -307,7 +319,7 @@ k_stage_fused(const FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Qout,
                 for (int t = 0; t < TE; ++t)
 #pragma unroll
                     for (int s = 0; s < TQ; ++s) av[m][t][s] = T(0);
-#pragma unroll 2
+WADG_KUNROLL
             for (int j = 0; j < NPP; ++j) {
                 T x[4][TE];
 #pragma unroll
@@ -365,7 +377,7 @@ k_stage_fused(const FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Qout,
             const int tile = tid + sl * NTF;
             if (tile < C::TILES_B) {
                 const int e0 = (tile % C::EG2) * TE2, j0 = (tile / C::EG2) * TJ;
-#pragma unroll 2
+WADG_KUNROLL
                 for (int qq = 0; qq < QC; ++qq) {
                     T w[6][TE2];
 #pragma unroll
@@ -522,7 +534,7 @@ k_stage_fused(const FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Qout,
             const int tile = tid + sl * NTF;
             if (tile < C::TILES_B) {
                 const int e0 = (tile % C::EG2) * TE2, j0 = (tile / C::EG2) * TJ;
-#pragma unroll 2
+WADG_KUNROLL
                 for (int fq = 0; fq < NFQ; ++fq) {
                     T L[TJ];
                     ldv<T, TJ>(L, sLift + fq * NPP + j0);
@@ -573,7 +585,7 @@ k_stage_fused(const FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Qout,
                 for (int t = 0; t < TE; ++t)
 #pragma unroll
                     for (int s = 0; s < TQ; ++s) z[c][t][s] = T(0);
-#pragma unroll 2
+WADG_KUNROLL
             for (int j = 0; j < NPP; ++j) {
                 T o[TQ];
                 ldv<T, TQ>(o, sU1 + j * QC + q0);
@@ -621,7 +633,7 @@ k_stage_fused(const FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Qout,
             const int tile = tid + sl * NTF;
             if (tile < C::TILES_B) {
                 const int e0 = (tile % C::EG2) * TE2, j0 = (tile / C::EG2) * TJ;
-#pragma unroll 2
+WADG_KUNROLL
                 for (int qq = 0; qq < QC; ++qq) {
                     T o[TJ];
                     ldv<T, TJ>(o, sU2 + qq * NPP + j0);

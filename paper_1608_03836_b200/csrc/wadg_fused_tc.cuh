@@ -1,0 +1,513 @@
+// Fused LSRK45 stage for fp32 tetrahedra with tensor-core GEMM phases.
+//
+// Same dataflow as k_stage_fused (wadg_fused.cuh): one kernel per stage,
+// ping-pong Q, neighbour face nodes by cp.async, operator chunks by TMA bulk
+// copies, and the strong-weak volume, surface and WADG update/LSRK algebra of
+// R/pkg/src/wadg/solver.py:207-301, 348-363.  The difference is that every
+// dense contraction runs on the tensor cores as warp-level split-TF32 MMA
+// (wadg_mma.cuh): x = hi + lo in registers, C += A_hi B_hi + A_hi B_lo +
+// A_lo B_hi, so no extra shared memory holds split operands and the result
+// keeps fp32 accuracy.
+//
+// A CTA owns KB = 64 elements = 4 MMA M-tiles of 16; the 8 warps are
+// (M-tile) x (group), group 0 working on the pressure and group 1 on the
+// velocity side of each phase, which balances the MMA counts:
+//   volume A:  g0: dp_a = D_a p (3 B-operands), g1: U_i = Vq u_i (3 A-operands)
+//   volume B:  g0: r_p += sum_a DTW_a F_a,      g1: r_u_i -= Pq gp_i
+//   lift:      g0: r_p -= Pf_f g_p,             g1: r_u_i -= Pf_f g_u_i
+//   update A:  g0: fields p, u1,  g1: u2, u3  (Vq, then the WADG weights)
+//   update B:  same split, Pq
+// Element-indexed shared arrays use a row stride of KB + 8 floats and the
+// operator tiles strides = 8 (mod 32) so that every fragment load is
+// bank-conflict free.
+
+#pragma once
+
+namespace wadg {
+namespace tc {
+
+using fused::cdiv;
+using fused::rup;
+
+__host__ __device__ constexpr int pad8mod32(int n) {   // smallest m >= n with m % 32 == 8
+    return n + ((40 - (n % 32)) % 32);
+}
+__host__ __device__ constexpr int pad4mod32(int n) {   // smallest m >= n with m % 32 == 4
+    return n + ((36 - (n % 32)) % 32);
+}
+
+template <int N>
+struct CfgTC {
+    static constexpr int NP = fused::np_tet(N);
+    static constexpr int NPP = rup(NP, 8);                 // K extent over nodes (multiple of 8)
+    static constexpr int NJT = NPP / 8;                    // N-tiles over nodes
+    static constexpr int NJS = pad8mod32(NPP);             // row stride of [k][j] operator tiles
+    static constexpr int NQ = (N + 1) * (N + 1) * (N + 1);
+    static constexpr int NFP = fused::nfp_tri(N);
+    static constexpr int NFQ = (N + 1) * (N + 1);
+    static constexpr int NFQ8 = rup(NFQ, 8);
+    static constexpr int NF = 4, FLD = 4;
+    static constexpr int KB = 64, MT = KB / 16;            // elements per CTA, M-tiles
+    static constexpr int QS = pad8mod32(KB);               // row stride of element-indexed arrays
+    static constexpr int QC = 32, QCT = QC / 8;            // quadrature chunk, its N-tiles
+    static constexpr int QCS = pad8mod32(QC);
+    static constexpr int NCH = cdiv(NQ, QC);
+    static constexpr size_t W = 4;
+    static constexpr size_t SQ = (size_t)FLD * NPP * QS * W;
+    // volume
+    static constexpr size_t S_OPA = (size_t)4 * NPP * QCS * W;      // [m][j][QCS]
+    static constexpr size_t S_OPB = (size_t)4 * QC * NJS * W;       // [m][q][NJS]
+    static constexpr size_t S_W = (size_t)6 * QC * QS * W;          // [6][q][QS]
+    static constexpr int GS = pad4mod32(KB);                       // row stride of prefetched factors
+    static constexpr size_t S_GEO = (size_t)9 * QC * GS * W;        // [9][q][GS] geometric factors
+    static constexpr size_t PH_V = S_OPA + S_OPB + S_W + S_GEO;
+    // surface
+    static constexpr size_t S_P1 = (size_t)FLD * NFP * KB * W;
+    static constexpr size_t S_G = (size_t)FLD * NFQ8 * QS * W;      // [c][fq][QS]
+    static constexpr size_t S_LIFT = (size_t)NFQ8 * NJS * W;        // [fq][NJS]
+    static constexpr size_t S_VFI = (size_t)rup(NFP * rup(NFQ, 2), 4) * W;
+    static constexpr size_t S_TAB = (size_t)rup(2 * NF * KB + NF * NFP + NF * 6 * NFP + 6 * NFP, 4) * 4;
+    static constexpr size_t PH_S = 2 * S_P1 + S_G + S_LIFT + S_VFI + S_TAB;
+    // update
+    static constexpr size_t S_R = SQ;
+    static constexpr size_t S_U1 = (size_t)NPP * QCS * W;           // [j][QCS]
+    static constexpr size_t S_U2 = (size_t)QC * NJS * W;            // [q][NJS]
+    static constexpr size_t S_W2 = (size_t)FLD * QC * QS * W;
+    static constexpr size_t S_OM = (size_t)2 * QC * GS * W;         // [wu|wp][q][GS]
+    static constexpr size_t PH_U = S_R + S_U1 + S_U2 + S_W2 + S_OM;
+    static constexpr size_t PH = fused::maxz(PH_V, fused::maxz(PH_S, PH_U));
+    static constexpr size_t SMEM = 16 + SQ + PH;
+};
+
+template <int N>
+__global__ void __launch_bounds__(256, 1)
+k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, float *__restrict__ Qout,
+                 float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt,
+                 int block0) {
+    using C = CfgTC<N>;
+    using namespace fused;
+    using namespace mma;
+    constexpr int NP = C::NP, NPP = C::NPP, NJT = C::NJT, NJS = C::NJS, NQ = C::NQ;
+    constexpr int NFP = C::NFP, NFQ = C::NFQ, NFQ8 = C::NFQ8, NF = C::NF, FLD = 4;
+    constexpr int KB = C::KB, QS = C::QS, QC = C::QC, QCT = C::QCT, QCS = C::QCS;
+    constexpr int FSQ = NPP * QS;                          // one field of sQ / sR
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
+    float *sQ = reinterpret_cast<float *>(smem_raw + 16);
+    unsigned char *ph = smem_raw + 16 + C::SQ;
+    float *sOpA = reinterpret_cast<float *>(ph);
+    float *sOpB = reinterpret_cast<float *>(ph + C::S_OPA);
+    float *sW = reinterpret_cast<float *>(ph + C::S_OPA + C::S_OPB);
+    float *sGeo = reinterpret_cast<float *>(ph + C::S_OPA + C::S_OPB + C::S_W);
+    float *sP = reinterpret_cast<float *>(ph);
+    float *sG = reinterpret_cast<float *>(ph + 2 * C::S_P1);
+    float *sLift = reinterpret_cast<float *>(ph + 2 * C::S_P1 + C::S_G);
+    float *sVfi = reinterpret_cast<float *>(ph + 2 * C::S_P1 + C::S_G + C::S_LIFT);
+    int32_t *sNbr = reinterpret_cast<int32_t *>(ph + 2 * C::S_P1 + C::S_G + C::S_LIFT + C::S_VFI);
+    int32_t *sCode = sNbr + NF * KB;
+    int32_t *sFmask = sCode + NF * KB;
+    int32_t *sExt = sFmask + NF * NFP;
+    int32_t *sPerm = sExt + NF * 6 * NFP;
+    float *sR = reinterpret_cast<float *>(ph);
+    float *sU1 = reinterpret_cast<float *>(ph + C::S_R);
+    float *sU2 = reinterpret_cast<float *>(ph + C::S_R + C::S_U1);
+    float *sW2 = reinterpret_cast<float *>(ph + C::S_R + C::S_U1 + C::S_U2);
+    float *sOm = reinterpret_cast<float *>(ph + C::S_R + C::S_U1 + C::S_U2 + C::S_W2);
+    constexpr int GS = C::GS;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int mt = warp & 3, grp = warp >> 2;              // M-tile, pressure / velocity group
+    const int e0 = mt * 16;
+    const int g = lane >> 2, t = lane & 3;
+    const size_t S = P.Kpad;
+    const size_t kblk = (size_t)(block0 + blockIdx.x) * KB;
+    WADG_PROF_MARK(0);
+
+    if (tid == 0) mbar_init(bar, 1);
+    // element fields via 16-byte cp.async, node rows >= NP zero
+    for (int r = tid; r < FLD * NPP * (KB / 4); r += 256) {
+        const int e4 = (r % (KB / 4)) * 4, row = r / (KB / 4);
+        const int c = row / NPP, j = row % NPP;
+        float *dst = sQ + row * QS + e4;
+        if (j < NP) {
+            cp_async16(dst, Qin + (size_t)(c * NP + j) * S + kblk + e4);
+        } else {
+            dst[0] = dst[1] = dst[2] = dst[3] = 0.f;
+        }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    BulkLoader ld{bar, 0u};
+    __syncthreads();
+    WADG_PROF_MARK(1);
+
+    // persistent nodal accumulators (MMA C layout): group 0 -> r_p (1 field),
+    // group 1 -> r_u (3 fields, stored with the opposite sign)
+    float acc[3][NJT][4];
+#pragma unroll
+    for (int f = 0; f < 3; ++f)
+#pragma unroll
+        for (int n = 0; n < NJT; ++n)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[f][n][i] = 0.f;
+
+    // ======================= volume =======================================
+    for (int ch = 0; ch < C::NCH; ++ch) {
+        {   // geometric factors of this chunk: cp.async, overlapped with the MMAs below
+            const int qn = min(QC, NQ - ch * QC);
+            __syncthreads();                   // previous chunk's epilogue is done with sGeo
+            for (int r = tid; r < 9 * qn * (KB / 4); r += 256) {
+                const int e4 = (r % (KB / 4)) * 4, row = r / (KB / 4);
+                const int rr = row / qn, qq = row % qn;
+                cp_async16(sGeo + (rr * QC + qq) * GS + e4, P.geo + (size_t)(rr * NQ + ch * QC + qq) * S + kblk + e4);
+            }
+            cp_async_commit();
+        }
+        ld.load2(sOpA, P.opVA + (size_t)ch * (C::S_OPA / 4), (uint32_t)C::S_OPA,
+                 sOpB, P.opVB + (size_t)ch * (C::S_OPB / 4), (uint32_t)C::S_OPB);
+        {
+            // A: quadrature values of dp_a (g0) or U_i (g1) for this warp's 16 elements
+            float c4[3][QCT][4];
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+                for (int n = 0; n < QCT; ++n)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) c4[m][n][i] = 0.f;
+#pragma unroll 2
+            for (int k0 = 0; k0 < NPP; k0 += 8) {
+                if (grp == 0) {
+                    AFrag a;
+                    load_a_colmajor(a, sQ + k0 * QS + e0, QS, lane);
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) {
+                        BFrag b[QCT];
+#pragma unroll
+                        for (int n = 0; n < QCT; ++n) load_b_rowmajor(b[n], sOpA + (m * NPP + k0) * QCS + n * 8, QCS, lane);
+                        mma3_row<QCT>(c4[m], a, b);
+                    }
+                } else {
+                    BFrag b[QCT];
+#pragma unroll
+                    for (int n = 0; n < QCT; ++n) load_b_rowmajor(b[n], sOpA + (3 * NPP + k0) * QCS + n * 8, QCS, lane);
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) {
+                        AFrag a;
+                        load_a_colmajor(a, sQ + (1 + m) * FSQ + k0 * QS + e0, QS, lane);
+                        mma3_row<QCT>(c4[m], a, b);
+                    }
+                }
+            }
+            // pointwise geometric factors: g0 gp_i = sum_a G_ai dp_a, g1 F_a = sum_i G_ai U_i
+            cp_async_wait<0>();
+            __syncthreads();
+#pragma unroll
+            for (int n = 0; n < QCT; ++n)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int qq = n * 8 + 2 * t + (i & 1);
+                    const int e = e0 + g + ((i >> 1) << 3);
+                    const int q = ch * QC + qq;
+                    float o[3] = {0.f, 0.f, 0.f};
+                    if (q < NQ) {
+                        float G[9];
+#pragma unroll
+                        for (int r = 0; r < 9; ++r) G[r] = sGeo[(r * QC + qq) * GS + e];
+#pragma unroll
+                        for (int m = 0; m < 3; ++m)
+                            o[m] = (grp == 0) ? G[0 * 3 + m] * c4[0][n][i] + G[1 * 3 + m] * c4[1][n][i] + G[2 * 3 + m] * c4[2][n][i]
+                                              : G[m * 3 + 0] * c4[0][n][i] + G[m * 3 + 1] * c4[1][n][i] + G[m * 3 + 2] * c4[2][n][i];
+                    }
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) sW[((grp * 3 + m) * QC + qq) * QS + e] = o[m];
+                }
+        }
+        __syncthreads();
+        // B: project to nodes with DTW_a (g0, from F_a) or Pq (g1, from gp_i)
+#pragma unroll
+        for (int k0 = 0; k0 < QC; k0 += 8) {
+            if (grp == 0) {
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    AFrag af;
+                    load_a_colmajor(af, sW + ((3 + a) * QC + k0) * QS + e0, QS, lane);
+                    BFrag b[NJT];
+#pragma unroll
+                    for (int n = 0; n < NJT; ++n) load_b_rowmajor(b[n], sOpB + (a * QC + k0) * NJS + n * 8, NJS, lane);
+                    mma3_row<NJT>(acc[0], af, b);
+                }
+            } else {
+                BFrag b[NJT];
+#pragma unroll
+                for (int n = 0; n < NJT; ++n) load_b_rowmajor(b[n], sOpB + (3 * QC + k0) * NJS + n * 8, NJS, lane);
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    AFrag af;
+                    load_a_colmajor(af, sW + (m * QC + k0) * QS + e0, QS, lane);
+                    mma3_row<NJT>(acc[m], af, b);
+                }
+            }
+        }
+    }
+
+    // ======================= surface ======================================
+    const int NFQT = NF * NFQ;
+    __syncthreads();
+    WADG_PROF_MARK(2);
+    for (int r = tid; r < NF * KB; r += 256) {
+        const int f = r / KB, e = r % KB;
+        sNbr[r] = P.nbr[(size_t)f * S + kblk + e];
+        sCode[r] = P.ncode[(size_t)f * S + kblk + e];
+    }
+    for (int r = tid; r < NF * NFP; r += 256) sFmask[r] = __ldg(P.fmask + r);
+    for (int r = tid; r < NF * 6 * NFP; r += 256) sExt[r] = __ldg(P.ext_node + r);
+    for (int r = tid; r < 6 * NFP; r += 256) sPerm[r] = __ldg(P.fperm + r);
+    for (int r = tid; r < NFP * NFQ; r += 256) {
+        const int i = r / NFQ, fq = r % NFQ;
+        sVfi[i * NFQ + fq] = __ldg(P.Vfi + fq * NFP + i);
+    }
+    if constexpr (NFQ8 > NFQ) {                      // zero K-padding rows of sG
+        constexpr int PADN = (NFQ8 - NFQ) * QS;
+        for (int r = tid; r < FLD * PADN; r += 256) sG[((r / PADN) * NFQ8 + NFQ) * QS + r % PADN] = 0.f;
+    }
+    __syncthreads();
+    auto gather = [&](int f, float *buf) {
+        for (int r = tid; r < FLD * NFP * KB; r += 256) {
+            const int e = r % KB, rest = r / KB;
+            const int i = rest % NFP, c = rest / NFP;
+            const int nb = sNbr[f * KB + e];
+            const int code = sCode[f * KB + e];
+            float *dst = buf + (c * NFP + i) * KB + e;
+            if (nb >= 0) {
+                cp_async_elem(dst, Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
+            } else if (nb == -1) {
+                const float m = sQ[(c * NPP + sFmask[f * NFP + i]) * QS + e];
+                *dst = (c == 0) ? -m : m;
+            } else {
+                cp_async_elem(dst, P.halo + ((size_t)(-nb - 2) * FLD + c) * NFP + sPerm[(code % P.nor) * NFP + i]);
+            }
+        }
+        cp_async_commit();
+    };
+    gather(0, sP);
+    for (int f = 0; f < NF; ++f) {
+        float *cur = sP + (f & 1) * (FLD * NFP * KB);
+        if (f + 1 < NF) {
+            gather(f + 1, sP + ((f + 1) & 1) * (FLD * NFP * KB));
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        if (tid == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(bar, (uint32_t)C::S_LIFT);
+            bulk_g2s(sLift, P.liftT + (size_t)f * NFQ8 * NJS, (uint32_t)C::S_LIFT, bar);
+        }
+        __syncthreads();
+        // traces at face quadrature points (2 face points x 4 elements per thread) and the flux
+        for (int tile = tid; tile < (KB / 4) * cdiv(NFQ, 2); tile += 256) {
+            const int ee = (tile % (KB / 4)) * 4, fq0 = (tile / (KB / 4)) * 2;
+            float fg[2][4][4];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const int fq = min(fq0 + s2, NFQ - 1);
+#pragma unroll
+                for (int d = 0; d < 4; ++d)
+                    ldg_v<float, 4>(fg[s2][d], P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + kblk + ee);
+            }
+            float mM[2][FLD][4], mP[2][FLD][4];
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                for (int c = 0; c < FLD; ++c)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) { mM[s2][c][u] = 0.f; mP[s2][c][u] = 0.f; }
+#pragma unroll 3
+            for (int i = 0; i < NFP; ++i) {
+                const float v0 = sVfi[i * NFQ + fq0];
+                const float v1 = (fq0 + 1 < NFQ) ? sVfi[i * NFQ + fq0 + 1] : 0.f;
+                const int node = sFmask[f * NFP + i];
+#pragma unroll
+                for (int c = 0; c < FLD; ++c) {
+                    float xm[4], xp[4];
+                    ldv<float, 4>(xm, sQ + (c * NPP + node) * QS + ee);
+                    ldv<float, 4>(xp, cur + (c * NFP + i) * KB + ee);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        mM[0][c][u] = fmaf(v0, xm[u], mM[0][c][u]);
+                        mP[0][c][u] = fmaf(v0, xp[u], mP[0][c][u]);
+                        mM[1][c][u] = fmaf(v1, xm[u], mM[1][c][u]);
+                        mP[1][c][u] = fmaf(v1, xp[u], mP[1][c][u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const int fq = fq0 + s2;
+                if (fq < NFQ) {
+                    float gv[FLD][4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float n0 = fg[s2][0][u], n1 = fg[s2][1][u], n2 = fg[s2][2][u], sJh = fg[s2][3][u];
+                        const float dp = mP[s2][0][u] - mM[s2][0][u];
+                        const float dUn = (mP[s2][1][u] - mM[s2][1][u]) * n0 + (mP[s2][2][u] - mM[s2][2][u]) * n1 +
+                                          (mP[s2][3][u] - mM[s2][3][u]) * n2;
+                        const float avg = (mP[s2][1][u] + mM[s2][1][u]) * n0 + (mP[s2][2][u] + mM[s2][2][u]) * n1 +
+                                          (mP[s2][3][u] + mM[s2][3][u]) * n2;
+                        const float fp = avg - tau_p * dp;
+                        const float fu = dp - tau_u * dUn;
+                        gv[0][u] = fp * sJh;
+                        gv[1][u] = fu * (sJh * n0);
+                        gv[2][u] = fu * (sJh * n1);
+                        gv[3][u] = fu * (sJh * n2);
+                    }
+#pragma unroll
+                    for (int c = 0; c < FLD; ++c) stv<float, 4>(sG + (c * NFQ8 + fq) * QS + ee, gv[c]);
+                }
+            }
+        }
+        __syncthreads();
+        mbar_wait(bar, ld.phase);
+        ld.phase ^= 1u;
+        // lift: r_p -= Pf g_p (accumulated as + (-g_p)), r_u stored negated: += Pf g_u
+#pragma unroll
+        for (int k0 = 0; k0 < NFQ8; k0 += 8) {
+            BFrag b[NJT];
+#pragma unroll
+            for (int n = 0; n < NJT; ++n) load_b_rowmajor(b[n], sLift + k0 * NJS + n * 8, NJS, lane);
+            if (grp == 0) {
+                AFrag af;
+                load_a_colmajor(af, sG + k0 * QS + e0, QS, lane);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {    // negate: r_p -= Pf g_p
+                    af.hi[i] ^= 0x80000000u;
+                    af.lo[i] ^= 0x80000000u;
+                }
+                mma3_row<NJT>(acc[0], af, b);
+            } else {
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    AFrag af;
+                    load_a_colmajor(af, sG + ((1 + m) * NFQ8 + k0) * QS + e0, QS, lane);
+                    mma3_row<NJT>(acc[m], af, b);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ======================= WADG update + LSRK ===========================
+    WADG_PROF_MARK(3);
+    // rhs into sR: g0 writes r_p, g1 writes r_u = -acc
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+        if (grp == 0 && m > 0) break;
+        const int c = grp == 0 ? 0 : 1 + m;
+        const float sg = grp == 0 ? 1.f : -1.f;
+#pragma unroll
+        for (int n = 0; n < NJT; ++n)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = n * 8 + 2 * t + (i & 1);
+                const int e = e0 + g + ((i >> 1) << 3);
+                sR[(c * NPP + j) * QS + e] = sg * acc[m][n][i];
+                acc[m][n][i] = 0.f;
+            }
+    }
+    // group 0 owns fields {0, 1}, group 1 fields {2, 3} in the update
+    const int cf0 = grp * 2;
+    for (int ch = 0; ch < C::NCH; ++ch) {
+        {   // WADG weights of this chunk
+            const int qn = min(QC, NQ - ch * QC);
+            const int nw = P.wp ? 2 : 1;
+            __syncthreads();
+            for (int r = tid; r < nw * qn * (KB / 4); r += 256) {
+                const int e4 = (r % (KB / 4)) * 4, row = r / (KB / 4);
+                const int w = row / qn, qq = row % qn;
+                const float *src = (w == 0 ? P.wu : P.wp) + (size_t)(ch * QC + qq) * S + kblk + e4;
+                cp_async16(sOm + (w * QC + qq) * GS + e4, src);
+            }
+            cp_async_commit();
+        }
+        ld.load2(sU1, P.opU1 + (size_t)ch * (C::S_U1 / 4), (uint32_t)C::S_U1,
+                 sU2, P.opU2 + (size_t)ch * (C::S_U2 / 4), (uint32_t)C::S_U2);
+        {
+            float z[2][QCT][4];
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int n = 0; n < QCT; ++n)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) z[m][n][i] = 0.f;
+#pragma unroll 2
+            for (int k0 = 0; k0 < NPP; k0 += 8) {
+                BFrag b[QCT];
+#pragma unroll
+                for (int n = 0; n < QCT; ++n) load_b_rowmajor(b[n], sU1 + k0 * QCS + n * 8, QCS, lane);
+#pragma unroll
+                for (int m = 0; m < 2; ++m) {
+                    AFrag af;
+                    load_a_colmajor(af, sR + (cf0 + m) * FSQ + k0 * QS + e0, QS, lane);
+                    mma3_row<QCT>(z[m], af, b);
+                }
+            }
+            cp_async_wait<0>();
+            __syncthreads();
+#pragma unroll
+            for (int n = 0; n < QCT; ++n)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int qq = n * 8 + 2 * t + (i & 1);
+                    const int e = e0 + g + ((i >> 1) << 3);
+                    const int q = ch * QC + qq;
+                    float wu = 0.f, wp = 0.f;
+                    if (q < NQ) {
+                        wu = sOm[qq * GS + e];
+                        wp = P.wp ? sOm[(QC + qq) * GS + e] : P.c2 * wu;
+                    }
+#pragma unroll
+                    for (int m = 0; m < 2; ++m)
+                        sW2[((cf0 + m) * QC + qq) * QS + e] = ((cf0 + m) == 0 ? wp : wu) * z[m][n][i];
+                }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k0 = 0; k0 < QC; k0 += 8) {
+            BFrag b[NJT];
+#pragma unroll
+            for (int n = 0; n < NJT; ++n) load_b_rowmajor(b[n], sU2 + k0 * NJS + n * 8, NJS, lane);
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                AFrag af;
+                load_a_colmajor(af, sW2 + ((cf0 + m) * QC + k0) * QS + e0, QS, lane);
+                mma3_row<NJT>(acc[m], af, b);
+            }
+        }
+    }
+    __syncthreads();
+    WADG_PROF_MARK(4);
+    // res = a res + dt Minv(rhs); Q_out = Q_in + b res
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+        const int c = cf0 + m;
+#pragma unroll
+        for (int n = 0; n < NJT; ++n)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = n * 8 + 2 * t + (i & 1);
+                const int e = e0 + g + ((i >> 1) << 3);
+                if (j < NP) {
+                    const size_t o = (size_t)(c * NP + j) * S + kblk + e;
+                    const float r = (a_rk == 0.f) ? dt * acc[m][n][i] : a_rk * res[o] + dt * acc[m][n][i];
+                    res[o] = r;
+                    Qout[o] = sQ[(c * NPP + j) * QS + e] + b_rk * r;
+                }
+            }
+    }
+    __syncthreads();
+    WADG_PROF_MARK(5);
+}
+
+}  // namespace tc
+}  // namespace wadg

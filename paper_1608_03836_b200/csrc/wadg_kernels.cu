@@ -26,6 +26,8 @@
 namespace wadg {
 }
 #include "wadg_fused.cuh"
+#include "wadg_mma.cuh"
+#include "wadg_fused_tc.cuh"
 
 namespace wadg {
 
@@ -652,19 +654,76 @@ static fused::FProb<T> make_fprob(const wadg_problem &p) {
     return q;
 }
 
+static int g_fused_variant = -1;   // debug override: 0 CUDA-core, 1 tensor-core, -1 default
+
+// tensor-core (split-TF32 mma.sync) fused stage: fp32, orders with a 64-element tile
 template <typename T, int N>
-static int fused_cfg(int32_t *kb, int32_t *qc, int32_t *nch, int64_t *smem) {
-    using C = fused::Cfg<T, N>;
-    if (kb) *kb = C::KB;
-    if (qc) *qc = C::QC;
-    if (nch) *nch = C::NCH;
-    if (smem) *smem = (int64_t)C::SMEM;
-    return C::SMEM <= 227 * 1024 ? 0 : 1;
+static constexpr bool tc_available() {
+    return sizeof(T) == 4 && N >= 2 && N <= 4;
+}
+
+template <typename T, int N>
+static bool use_tc() {
+    if (!tc_available<T, N>()) return false;
+    return g_fused_variant != 0;
+}
+
+// info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),
+//            quad-chunk row stride, node row stride, padded face points}
+template <typename T, int N>
+static int fused_cfg(int32_t *info, int64_t *smem) {
+    size_t sm = 0;
+    int32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool done = false;
+    if constexpr (tc_available<T, N>()) {
+        if (use_tc<T, N>()) {
+            using C = tc::CfgTC<N>;
+            const int32_t w[8] = {1, C::KB, C::QC, C::NCH, C::NPP, C::QCS, C::NJS, C::NFQ8};
+            for (int i = 0; i < 8; ++i) v[i] = w[i];
+            sm = C::SMEM;
+            done = true;
+        }
+    }
+    if (!done) {
+        using C = fused::Cfg<T, N>;
+        const int32_t w[8] = {0, C::KB, C::QC, C::NCH, C::NPP, C::QC, C::NPP, C::NFQ};
+        for (int i = 0; i < 8; ++i) v[i] = w[i];
+        sm = C::SMEM;
+    }
+    if (info)
+        for (int i = 0; i < 8; ++i) info[i] = v[i];
+    if (smem) *smem = (int64_t)sm;
+    return sm <= 227 * 1024 ? 0 : 1;
+}
+
+template <int N>
+static int fused_launch_tc(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
+                           double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
+    using C = tc::CfgTC<N>;
+    if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
+    const int nblk = Pc->Kpad / C::KB;
+    if (b1 < 0 || b1 > nblk) b1 = nblk;
+    if (b0 < 0) b0 = 0;
+    if (b1 <= b0) return 0;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(tc::k_stage_fused_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::SMEM);
+        if (e != cudaSuccess) return fail(cudaGetErrorString(e));
+        attr_set = true;
+    }
+    tc::k_stage_fused_tc<N><<<b1 - b0, 256, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin,
+                                                           (float *)Qout, (float *)res, (float)tp, (float)tu,
+                                                           (float)a, (float)b, (float)dt, b0);
+    return check_launch("wadg_stage_fused(tc)");
 }
 
 template <typename T, int N>
 static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
                         double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
+    if constexpr (tc_available<T, N>()) {
+        if (use_tc<T, N>()) return fused_launch_tc<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+    }
     using C = fused::Cfg<T, N>;
     if (C::SMEM > 227 * 1024) return fail("fused stage does not fit shared memory for this order");
     if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
@@ -792,9 +851,15 @@ int wadg_debug_set_phase_clock_buffer(void *buf) {
     return 0;
 }
 
-int wadg_fused_config(int dtype, int order, int32_t *kb, int32_t *qc, int32_t *nch, int64_t *smem) {
-    if (dtype == WADG_F64) { WADG_FUSED_SWITCH(double, order, fused_cfg, kb, qc, nch, smem); }
-    if (dtype == WADG_F32) { WADG_FUSED_SWITCH(float, order, fused_cfg, kb, qc, nch, smem); }
+int wadg_debug_set_fused_variant(int variant) {
+    if (variant < -1 || variant > 1) return fail("variant must be -1, 0 or 1");
+    g_fused_variant = variant;
+    return 0;
+}
+
+int wadg_fused_config(int dtype, int order, int32_t *info, int64_t *smem) {
+    if (dtype == WADG_F64) { WADG_FUSED_SWITCH(double, order, fused_cfg, info, smem); }
+    if (dtype == WADG_F32) { WADG_FUSED_SWITCH(float, order, fused_cfg, info, smem); }
     return fail("bad dtype");
 }
 
@@ -816,3 +881,92 @@ int wadg_stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void *r
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// FMA-pipe peak microbenchmark (measurement support for the FP roofline):
+// every thread runs 16 independent register-operand FMA chains.
+namespace wadg {
+template <typename T>
+__global__ void __launch_bounds__(256) k_fma_peak(const T *__restrict__ in, T *__restrict__ out, int iters) {
+    T a[16];
+    const T b = in[threadIdx.x & 7], c = in[8 + (threadIdx.x & 7)];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = in[16 + i] + (T)threadIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) a[i] = fma(a[i], b, c);
+    }
+    T s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += a[i];
+    if (s == (T)12345.678) out[threadIdx.x] = s;
+}
+}  // namespace wadg
+
+extern "C" int wadg_microbench_fma(int dtype, int blocks, int iters, const void *in, void *out, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == WADG_F64)
+        wadg::k_fma_peak<double><<<blocks, 256, 0, st>>>((const double *)in, (double *)out, iters);
+    else
+        wadg::k_fma_peak<float><<<blocks, 256, 0, st>>>((const float *)in, (float *)out, iters);
+    return check_launch("wadg_microbench_fma");
+}
+
+// mma.sync m16n8k8 TF32 throughput probe (design input for the split-TF32 question).
+namespace wadg {
+__global__ void __launch_bounds__(256) k_mma_tf32_peak(const float *__restrict__ in, float *__restrict__ out, int iters) {
+    uint32_t a[4], b[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = __float_as_uint(in[i + (threadIdx.x & 3)]);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) b[i] = __float_as_uint(in[8 + i + (threadIdx.x & 3)]);
+    float c[8][4];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c[k][i] = 0.f;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                         : "+f"(c[k][0]), "+f"(c[k][1]), "+f"(c[k][2]), "+f"(c[k][3])
+                         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += c[k][0] + c[k][1] + c[k][2] + c[k][3];
+    if (s == 12345.678f) out[threadIdx.x] = s;
+}
+}  // namespace wadg
+
+extern "C" int wadg_microbench_mma_tf32(int blocks, int iters, const void *in, void *out, void *stream) {
+    wadg::k_mma_tf32_peak<<<blocks, 256, 0, (cudaStream_t)stream>>>((const float *)in, (float *)out, iters);
+    return check_launch("wadg_microbench_mma_tf32");
+}
+
+// Debug: one warp, C(16 x 8) = A(16 x K) B(K x 8) with 3xTF32 mma.sync; A given
+// column-major (A[k*16 + r]), B row-major (B[k*8 + n]), K a multiple of 8.
+namespace wadg {
+__global__ void k_mma_test(const float *A, const float *B, float *C, int K) {
+    const int lane = threadIdx.x;
+    float c[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int k0 = 0; k0 < K; k0 += 8) {
+        mma::AFrag a;
+        mma::BFrag b;
+        mma::load_a_colmajor(a, A + k0 * 16, 16, lane);
+        mma::load_b_rowmajor(b, B + k0 * 8, 8, lane);
+        mma::mma3(c, a, b);
+    }
+    const int g = lane >> 2, t = lane & 3;
+    C[g * 8 + 2 * t] = c[0];
+    C[g * 8 + 2 * t + 1] = c[1];
+    C[(g + 8) * 8 + 2 * t] = c[2];
+    C[(g + 8) * 8 + 2 * t + 1] = c[3];
+}
+}  // namespace wadg
+
+extern "C" int wadg_debug_mma_test(const void *A, const void *B, void *C, int K, void *stream) {
+    wadg::k_mma_test<<<1, 32, 0, (cudaStream_t)stream>>>((const float *)A, (const float *)B, (float *)C, K);
+    return check_launch("wadg_debug_mma_test");
+}

@@ -182,28 +182,48 @@ class DeviceProblem:
         cfg = _native.fused_config(code, N)
         if cfg is None:
             return None
-        kb, qc, nch, _ = cfg
+        kb, qc, nch = cfg["kb"], cfg["qc"], cfg["nch"]
         NP, NQ = ref.Np, ref.Nq
-        NPP = roundup(NP, 4)
-        NQP = nch * qc
+        nf, nfq = ref.n_faces, ref.nfq
         DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
-        A = np.zeros((NQP, NPP, 4))
-        A[:NQ, :NP] = np.stack(list(ref.Dq) + [ref.Vq], axis=-1)
-        opVA = A.reshape(nch, qc, NPP, 4).transpose(0, 2, 1, 3)
-        B = np.zeros((NPP, NQP, 4))
-        B[:NP, :NQ] = np.stack(DTW + [ref.Pq], axis=-1)
-        opVB = B.reshape(NPP, nch, qc, 4).transpose(1, 2, 0, 3)
-        U1 = np.zeros((NQP, NPP))
-        U1[:NQ, :NP] = ru.Vq
-        opU1 = U1.reshape(nch, qc, NPP).transpose(0, 2, 1)
-        U2 = np.zeros((NPP, NQP))
-        U2[:NP, :NQ] = ru.Pq
-        opU2 = U2.reshape(NPP, nch, qc).transpose(1, 2, 0)
-        L = np.zeros((ref.n_faces * ref.nfq, NPP))
-        L[:, :NP] = ref.Pfq.T
+        if cfg["kind"] == 0:                    # CUDA-core kernel layouts
+            NPP = roundup(NP, 4)
+            NQP = nch * qc
+            A = np.zeros((NQP, NPP, 4))
+            A[:NQ, :NP] = np.stack(list(ref.Dq) + [ref.Vq], axis=-1)
+            opVA = A.reshape(nch, qc, NPP, 4).transpose(0, 2, 1, 3)
+            B = np.zeros((NPP, NQP, 4))
+            B[:NP, :NQ] = np.stack(DTW + [ref.Pq], axis=-1)
+            opVB = B.reshape(NPP, nch, qc, 4).transpose(1, 2, 0, 3)
+            U1 = np.zeros((NQP, NPP))
+            U1[:NQ, :NP] = ru.Vq
+            opU1 = U1.reshape(nch, qc, NPP).transpose(0, 2, 1)
+            U2 = np.zeros((NPP, NQP))
+            U2[:NP, :NQ] = ru.Pq
+            opU2 = U2.reshape(NPP, nch, qc).transpose(1, 2, 0)
+            L = np.zeros((nf * nfq, NPP))
+            L[:, :NP] = ref.Pfq.T
+        else:                                   # tensor-core kernel layouts (padded strides)
+            NPP, QCS, NJS, NFQ8 = cfg["npp"], cfg["qcs"], cfg["njs"], cfg["nfq8"]
+            opVA = np.zeros((nch, 4, NPP, QCS))
+            opVB = np.zeros((nch, 4, qc, NJS))
+            opU1 = np.zeros((nch, NPP, QCS))
+            opU2 = np.zeros((nch, qc, NJS))
+            ops_q = list(ref.Dq) + [ref.Vq]              # (NQ, NP) each
+            ops_j = DTW + [ref.Pq]                       # (NP, NQ) each
+            for ch in range(nch):
+                q0, q1 = ch * qc, min(NQ, (ch + 1) * qc)
+                for m in range(4):
+                    opVA[ch, m, :NP, :q1 - q0] = ops_q[m][q0:q1].T
+                    opVB[ch, m, :q1 - q0, :NP] = ops_j[m][:, q0:q1].T
+                opU1[ch, :NP, :q1 - q0] = ru.Vq[q0:q1].T
+                opU2[ch, :q1 - q0, :NP] = ru.Pq[:, q0:q1].T
+            L = np.zeros((nf, NFQ8, NJS))
+            L[:, :nfq, :NP] = ref.Pfq.T.reshape(nf, nfq, NP)
         for name, arr in (("opVA", opVA), ("opVB", opVB), ("opU1", opU1), ("opU2", opU2), ("liftT", L)):
             self.ops[name] = self._t(arr)
             setattr(self.struct, name, self.ops[name].data_ptr())
+        self.fused_kind = cfg["kind"]
         self.struct.order = N
         if self.Kpad % kb:
             return None

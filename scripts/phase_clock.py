@@ -47,13 +47,16 @@ def main():
                      0.0, 0.1, 1e-3, 0, -1, sp)
     _native.call("wadg_debug_set_phase_clock_buffer", ctypes.c_void_p(0))
     torch.cuda.synchronize()
-    t = buf.view(nblk, 8)[:, :7].cpu().numpy().astype(np.float64)
+    t = buf.view(nblk, 8).cpu().numpy().astype(np.float64)
+    nm = int(np.max(np.nonzero(t[0])[0])) + 1          # marks written by this kernel
+    t = t[:, :nm]
     dur = np.diff(t, axis=1)
+    phases = PHASES if d.fused_kind == 0 else ["stage Q", "volume", "surface", "update", "write"]
     med = np.median(dur, axis=0)
     tot = med.sum()
     out = {"K": mesh.K, "N": args.order, "dtype": args.dtype, "elems_per_block": kb,
            "cycles_per_cta_median": float(tot),
-           "phases": {p: {"cycles": float(c), "share": float(c / tot)} for p, c in zip(PHASES, med)}}
+           "phases": {p: {"cycles": float(c), "share": float(c / tot)} for p, c in zip(phases, med)}}
     print(json.dumps(out))
 
 

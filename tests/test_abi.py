@@ -65,4 +65,4 @@ def test_fused_configs_fit_shared_memory():
         for N in range(1, 8):
             cfg = _native.fused_config(code, N)
             assert cfg is not None, (code, N)
-            assert cfg[3] <= 227 * 1024
+            assert cfg["smem"] <= 227 * 1024
