@@ -62,12 +62,17 @@ struct CfgTC {
     static constexpr size_t S_GEO = (size_t)9 * QC * GS * W;        // [9][q][GS] geometric factors
     static constexpr size_t PH_V = S_OPA + S_OPB + S_W + S_GEO;
     // surface
-    static constexpr size_t S_P1 = (size_t)FLD * NFP * KB * W;
-    static constexpr size_t S_G = (size_t)FLD * NFQ8 * QS * W;      // [c][fq][QS]
+    static constexpr int NFP8 = rup(NFP, 8);                       // K extent over face nodes
+    static constexpr int NFQT8 = NFQ8 / 8;                         // N-tiles over face points
+    static constexpr int VS = pad8mod32(NFQ8);                     // row stride of Vfi^T
+    static constexpr size_t S_P1 = (size_t)FLD * NFP8 * QS * W;     // exterior face nodes [c][i][QS]
+    static constexpr size_t S_TR = (size_t)2 * FLD * NFQ8 * QS * W; // traces [in|ex][c][fq][QS]
+    static constexpr size_t S_FG = (size_t)4 * NFQ * QS * W;        // face factors [d][fq][QS]
     static constexpr size_t S_LIFT = (size_t)NFQ8 * NJS * W;        // [fq][NJS]
-    static constexpr size_t S_VFI = (size_t)rup(NFP * rup(NFQ, 2), 4) * W;
-    static constexpr size_t S_TAB = (size_t)rup(2 * NF * KB + NF * NFP + NF * 6 * NFP + 6 * NFP, 4) * 4;
-    static constexpr size_t PH_S = 2 * S_P1 + S_G + S_LIFT + S_VFI + S_TAB;
+    static constexpr size_t S_VFI = (size_t)NFP8 * VS * W;          // Vfi^T [i][VS]
+    static constexpr size_t S_TAB = (size_t)rup(2 * NF * KB + NF * NFP8 + NF * 6 * NFP + 6 * NFP, 4) * 4;
+    // the flux g_c overwrites the interior traces in place (sG == sTr[0])
+    static constexpr size_t PH_S = 2 * S_P1 + S_TR + S_FG + S_LIFT + S_VFI + S_TAB;
     // update
     static constexpr size_t S_R = SQ;
     static constexpr size_t S_U1 = (size_t)NPP * QCS * W;           // [j][QCS]
@@ -101,13 +106,15 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
     float *sW = reinterpret_cast<float *>(ph + C::S_OPA + C::S_OPB);
     float *sGeo = reinterpret_cast<float *>(ph + C::S_OPA + C::S_OPB + C::S_W);
     float *sP = reinterpret_cast<float *>(ph);
-    float *sG = reinterpret_cast<float *>(ph + 2 * C::S_P1);
-    float *sLift = reinterpret_cast<float *>(ph + 2 * C::S_P1 + C::S_G);
-    float *sVfi = reinterpret_cast<float *>(ph + 2 * C::S_P1 + C::S_G + C::S_LIFT);
-    int32_t *sNbr = reinterpret_cast<int32_t *>(ph + 2 * C::S_P1 + C::S_G + C::S_LIFT + C::S_VFI);
+    float *sTr = reinterpret_cast<float *>(ph + 2 * C::S_P1);
+    float *sFG = reinterpret_cast<float *>(ph + 2 * C::S_P1 + C::S_TR);
+    float *sG = sTr;                                   // [c][fq][QS], written over the interior traces
+    float *sLift = reinterpret_cast<float *>(ph + 2 * C::S_P1 + C::S_TR + C::S_FG);
+    float *sVfi = reinterpret_cast<float *>(ph + 2 * C::S_P1 + C::S_TR + C::S_FG + C::S_LIFT);
+    int32_t *sNbr = reinterpret_cast<int32_t *>(ph + 2 * C::S_P1 + C::S_TR + C::S_FG + C::S_LIFT + C::S_VFI);
     int32_t *sCode = sNbr + NF * KB;
-    int32_t *sFmask = sCode + NF * KB;
-    int32_t *sExt = sFmask + NF * NFP;
+    int32_t *sFmask = sCode + NF * KB;               // [f][NFP8], padding -> a zero row of sQ
+    int32_t *sExt = sFmask + NF * C::NFP8;
     int32_t *sPerm = sExt + NF * 6 * NFP;
     float *sR = reinterpret_cast<float *>(ph);
     float *sU1 = reinterpret_cast<float *>(ph + C::S_R);
@@ -252,6 +259,7 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
     }
 
     // ======================= surface ======================================
+    constexpr int NFP8 = C::NFP8, NFQT8 = C::NFQT8, VS = C::VS;
     const int NFQT = NF * NFQ;
     __syncthreads();
     WADG_PROF_MARK(2);
@@ -260,16 +268,22 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
         sNbr[r] = P.nbr[(size_t)f * S + kblk + e];
         sCode[r] = P.ncode[(size_t)f * S + kblk + e];
     }
-    for (int r = tid; r < NF * NFP; r += 256) sFmask[r] = __ldg(P.fmask + r);
+    for (int r = tid; r < NF * NFP8; r += 256) {
+        const int f = r / NFP8, i = r % NFP8;
+        sFmask[r] = i < NFP ? __ldg(P.fmask + f * NFP + i) : NP;     // row NP of sQ is zero padding
+    }
     for (int r = tid; r < NF * 6 * NFP; r += 256) sExt[r] = __ldg(P.ext_node + r);
     for (int r = tid; r < 6 * NFP; r += 256) sPerm[r] = __ldg(P.fperm + r);
-    for (int r = tid; r < NFP * NFQ; r += 256) {
-        const int i = r / NFQ, fq = r % NFQ;
-        sVfi[i * NFQ + fq] = __ldg(P.Vfi + fq * NFP + i);
+    for (int r = tid; r < NFP8 * VS; r += 256) {                 // Vfi^T, zero padded
+        const int i = r / VS, fq = r % VS;
+        sVfi[r] = (i < NFP && fq < NFQ) ? __ldg(P.Vfi + fq * NFP + i) : 0.f;
     }
-    if constexpr (NFQ8 > NFQ) {                      // zero K-padding rows of sG
-        constexpr int PADN = (NFQ8 - NFQ) * QS;
-        for (int r = tid; r < FLD * PADN; r += 256) sG[((r / PADN) * NFQ8 + NFQ) * QS + r % PADN] = 0.f;
+    if constexpr (NFP8 > NFP) {                                  // K-padding rows of both sP buffers
+        constexpr int PADN = (NFP8 - NFP) * QS;
+        for (int r = tid; r < 2 * FLD * PADN; r += 256) {
+            const int bc = r / PADN;                             // buffer * FLD + field
+            sP[(bc * NFP8 + NFP) * QS + r % PADN] = 0.f;
+        }
     }
     __syncthreads();
     auto gather = [&](int f, float *buf) {
@@ -278,23 +292,31 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
             const int i = rest % NFP, c = rest / NFP;
             const int nb = sNbr[f * KB + e];
             const int code = sCode[f * KB + e];
-            float *dst = buf + (c * NFP + i) * KB + e;
+            float *dst = buf + (c * NFP8 + i) * QS + e;
             if (nb >= 0) {
                 cp_async_elem(dst, Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
             } else if (nb == -1) {
-                const float m = sQ[(c * NPP + sFmask[f * NFP + i]) * QS + e];
+                const float m = sQ[(c * NPP + sFmask[f * NFP8 + i]) * QS + e];
                 *dst = (c == 0) ? -m : m;
             } else {
                 cp_async_elem(dst, P.halo + ((size_t)(-nb - 2) * FLD + c) * NFP + sPerm[(code % P.nor) * NFP + i]);
             }
         }
-        cp_async_commit();
     };
     gather(0, sP);
+    cp_async_commit();
     for (int f = 0; f < NF; ++f) {
-        float *cur = sP + (f & 1) * (FLD * NFP * KB);
+        float *cur = sP + (f & 1) * (FLD * NFP8 * QS);
+        // this face's normals and sJ/2, then the next face's neighbour nodes
+        for (int r = tid; r < 4 * NFQ * (KB / 4); r += 256) {
+            const int e4 = (r % (KB / 4)) * 4, row = r / (KB / 4);
+            const int d = row / NFQ, fq = row % NFQ;
+            cp_async16(sFG + row * QS + e4, P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + kblk + e4);
+        }
+        cp_async_commit();
         if (f + 1 < NF) {
-            gather(f + 1, sP + ((f + 1) & 1) * (FLD * NFP * KB));
+            gather(f + 1, sP + ((f + 1) & 1) * (FLD * NFP8 * QS));
+            cp_async_commit();
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
@@ -305,67 +327,68 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
             bulk_g2s(sLift, P.liftT + (size_t)f * NFQ8 * NJS, (uint32_t)C::S_LIFT, bar);
         }
         __syncthreads();
-        // traces at face quadrature points (2 face points x 4 elements per thread) and the flux
-        for (int tile = tid; tile < (KB / 4) * cdiv(NFQ, 2); tile += 256) {
-            const int ee = (tile % (KB / 4)) * 4, fq0 = (tile / (KB / 4)) * 2;
-            float fg[2][4][4];
+        // traces at face quadrature points on the tensor cores:
+        // group 0 interior (face nodes of sQ via fmask), group 1 exterior (cur)
+        {
+            float tr[FLD][NFQT8][4];
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
-                const int fq = min(fq0 + s2, NFQ - 1);
+            for (int c = 0; c < FLD; ++c)
 #pragma unroll
-                for (int d = 0; d < 4; ++d)
-                    ldg_v<float, 4>(fg[s2][d], P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + kblk + ee);
-            }
-            float mM[2][FLD][4], mP[2][FLD][4];
+                for (int n = 0; n < NFQT8; ++n)
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2)
+                    for (int i = 0; i < 4; ++i) tr[c][n][i] = 0.f;
 #pragma unroll
-                for (int c = 0; c < FLD; ++c)
+            for (int k0 = 0; k0 < NFP8; k0 += 8) {
+                BFrag b[NFQT8];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) { mM[s2][c][u] = 0.f; mP[s2][c][u] = 0.f; }
-#pragma unroll 3
-            for (int i = 0; i < NFP; ++i) {
-                const float v0 = sVfi[i * NFQ + fq0];
-                const float v1 = (fq0 + 1 < NFQ) ? sVfi[i * NFQ + fq0 + 1] : 0.f;
-                const int node = sFmask[f * NFP + i];
+                for (int n = 0; n < NFQT8; ++n) load_b_rowmajor(b[n], sVfi + k0 * VS + n * 8, VS, lane);
+                const int r0 = (grp == 0) ? sFmask[f * NFP8 + k0 + t] : k0 + t;
+                const int r1 = (grp == 0) ? sFmask[f * NFP8 + k0 + t + 4] : k0 + t + 4;
 #pragma unroll
                 for (int c = 0; c < FLD; ++c) {
-                    float xm[4], xp[4];
-                    ldv<float, 4>(xm, sQ + (c * NPP + node) * QS + ee);
-                    ldv<float, 4>(xp, cur + (c * NFP + i) * KB + ee);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        mM[0][c][u] = fmaf(v0, xm[u], mM[0][c][u]);
-                        mP[0][c][u] = fmaf(v0, xp[u], mP[0][c][u]);
-                        mM[1][c][u] = fmaf(v1, xm[u], mM[1][c][u]);
-                        mP[1][c][u] = fmaf(v1, xp[u], mP[1][c][u]);
-                    }
+                    const float *base = (grp == 0) ? sQ + c * FSQ : cur + c * NFP8 * QS;
+                    const float *p0 = base + r0 * QS + e0 + g, *p1 = base + r1 * QS + e0 + g;
+                    AFrag af;
+                    Split sp;
+                    sp = split(p0[0]); af.hi[0] = sp.hi; af.lo[0] = sp.lo;
+                    sp = split(p0[8]); af.hi[1] = sp.hi; af.lo[1] = sp.lo;
+                    sp = split(p1[0]); af.hi[2] = sp.hi; af.lo[2] = sp.lo;
+                    sp = split(p1[8]); af.hi[3] = sp.hi; af.lo[3] = sp.lo;
+                    mma3_row<NFQT8>(tr[c], af, b);
                 }
             }
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
-                const int fq = fq0 + s2;
-                if (fq < NFQ) {
-                    float gv[FLD][4];
+            for (int c = 0; c < FLD; ++c)
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float n0 = fg[s2][0][u], n1 = fg[s2][1][u], n2 = fg[s2][2][u], sJh = fg[s2][3][u];
-                        const float dp = mP[s2][0][u] - mM[s2][0][u];
-                        const float dUn = (mP[s2][1][u] - mM[s2][1][u]) * n0 + (mP[s2][2][u] - mM[s2][2][u]) * n1 +
-                                          (mP[s2][3][u] - mM[s2][3][u]) * n2;
-                        const float avg = (mP[s2][1][u] + mM[s2][1][u]) * n0 + (mP[s2][2][u] + mM[s2][2][u]) * n1 +
-                                          (mP[s2][3][u] + mM[s2][3][u]) * n2;
-                        const float fp = avg - tau_p * dp;
-                        const float fu = dp - tau_u * dUn;
-                        gv[0][u] = fp * sJh;
-                        gv[1][u] = fu * (sJh * n0);
-                        gv[2][u] = fu * (sJh * n1);
-                        gv[3][u] = fu * (sJh * n2);
+                for (int n = 0; n < NFQT8; ++n)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int fq = n * 8 + 2 * t + (i & 1);
+                        const int e = e0 + g + ((i >> 1) << 3);
+                        sTr[((grp * FLD + c) * NFQ8 + fq) * QS + e] = tr[c][n][i];
                     }
+        }
+        __syncthreads();
+        // penalty flux, pointwise
+        for (int r = tid; r < NFQ * KB; r += 256) {
+            const int e = r % KB, fq = r / KB;
+            float mM[FLD], mP[FLD];
 #pragma unroll
-                    for (int c = 0; c < FLD; ++c) stv<float, 4>(sG + (c * NFQ8 + fq) * QS + ee, gv[c]);
-                }
+            for (int c = 0; c < FLD; ++c) {
+                mM[c] = sTr[((0 * FLD + c) * NFQ8 + fq) * QS + e];
+                mP[c] = sTr[((1 * FLD + c) * NFQ8 + fq) * QS + e];
             }
+            const float n0 = sFG[(0 * NFQ + fq) * QS + e], n1 = sFG[(1 * NFQ + fq) * QS + e];
+            const float n2 = sFG[(2 * NFQ + fq) * QS + e], sJh = sFG[(3 * NFQ + fq) * QS + e];
+            const float dp = mP[0] - mM[0];
+            const float dUn = (mP[1] - mM[1]) * n0 + (mP[2] - mM[2]) * n1 + (mP[3] - mM[3]) * n2;
+            const float avg = (mP[1] + mM[1]) * n0 + (mP[2] + mM[2]) * n1 + (mP[3] + mM[3]) * n2;
+            const float fp = avg - tau_p * dp;
+            const float fu = dp - tau_u * dUn;
+            sG[(0 * NFQ8 + fq) * QS + e] = fp * sJh;
+            sG[(1 * NFQ8 + fq) * QS + e] = fu * (sJh * n0);
+            sG[(2 * NFQ8 + fq) * QS + e] = fu * (sJh * n1);
+            sG[(3 * NFQ8 + fq) * QS + e] = fu * (sJh * n2);
         }
         __syncthreads();
         mbar_wait(bar, ld.phase);

@@ -528,7 +528,7 @@ def stable_dt(mesh, ref, medium, cfl):
     return float(cfl * np.min(hmin / (c_max * (ref.N + 1) ** 2)))
 
 
-def _projection_chunks(mesh, N, initial_fn, dev, k0=0, k1=None, chunk=1 << 15):
+def _projection_chunks(mesh, N, initial_fn, dev, k0=0, k1=None, chunk=None):
     """Yield (c0, c1, [coefficients (Kc, Np) per field]) of the J-weighted L2
     projection at the mass-exact degree 2N + 2 N_geo (R/.../solver.py:379-389,
     operators.py:64-73).  initial_fn gets torch tensors first (so a torch
@@ -539,6 +539,8 @@ def _projection_chunks(mesh, N, initial_fn, dev, k0=0, k1=None, chunk=1 << 15):
     mops = geometry.map_operators(mesh.shape, mesh.N_geo, ref_m).to(dev)
     Vq = torch.as_tensor(ref_m.Vq, device=dev)
     wq = torch.as_tensor(ref_m.wq, device=dev)
+    if chunk is None:       # bound the (chunk, Np, Nq) float64 temporaries to ~1 GB
+        chunk = int(max(256, min(1 << 15, 2 ** 30 // (8 * ref_m.Np * ref_m.Nq))))
     for c0 in range(k0, k1, chunk):
         c1 = min(k1, c0 + chunk)
         X = torch.as_tensor(np.asarray(mesh.elem_map_nodes[c0:c1], dtype=np.float64), device=dev)
@@ -551,7 +553,7 @@ def _projection_chunks(mesh, N, initial_fn, dev, k0=0, k1=None, chunk=1 << 15):
             vals = [torch.as_tensor(np.broadcast_to(np.asarray(v, dtype=float), g["J"].shape).copy(),
                                     device=dev) for v in initial_fn(*xyz)]
         W = wq[None, :] * g["J"]
-        M = torch.einsum("kq,qi,qj->kij", W, Vq, Vq)
+        M = (Vq.T[None, :, :] * W[:, None, :]) @ Vq
         M = 0.5 * (M + M.transpose(1, 2))
         L = torch.linalg.cholesky(M)
         out = []
