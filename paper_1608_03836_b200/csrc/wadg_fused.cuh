@@ -53,7 +53,9 @@ struct Cfg {
     static constexpr int NFQ = (N + 1) * (N + 1);
     static constexpr int NF = 4, FLD = 4;
     static constexpr int KB = F32 ? (N <= 5 ? 64 : 32) : (N <= 5 ? 32 : 16);
-    static constexpr int QC = F32 ? (N <= 4 ? 64 : 32) : (N <= 3 ? 64 : (N <= 5 ? 32 : 16));
+    static constexpr int QC0 = F32 ? (N <= 4 ? 64 : 32) : (N <= 3 ? 64 : (N <= 5 ? 32 : 16));
+    static constexpr int QC = QC0 < rup(NQ, 8) ? QC0 : rup(NQ, 8);   // never wider than Nq
+    static constexpr int MINB = N == 1 ? 3 : 1;                       // low order: several CTAs / SM
     static constexpr int NCH = cdiv(NQ, QC);
     // phase A (interp-to-quadrature GEMMs): TE elements x TQ quad points
     static constexpr int TE = F32 ? (QC == 64 ? 4 : 2) : 2;
@@ -235,7 +237,7 @@ struct FProb {
     } while (0)
 
 template <typename T, int N>
-__global__ void __launch_bounds__(NTF, 1)
+__global__ void __launch_bounds__(NTF, (Cfg<T, N>::MINB))
 k_stage_fused(const FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Qout, T *__restrict__ res,
               T tau_p, T tau_u, T a_rk, T b_rk, T dt, int block0) {
     using C = Cfg<T, N>;

@@ -47,9 +47,13 @@ struct CfgTC {
     static constexpr int NFQ = (N + 1) * (N + 1);
     static constexpr int NFQ8 = rup(NFQ, 8);
     static constexpr int NF = 4, FLD = 4;
-    static constexpr int KB = 64, MT = KB / 16;            // elements per CTA, M-tiles
+    // 32 elements (2 MMA M-tiles) and 4 warps per CTA keep shared memory near
+    // 106 KB so two independent CTAs share an SM and overlap each other's
+    // barrier / memory phases
+    static constexpr int KB = 32, MT = KB / 16;            // elements per CTA, M-tiles
+    static constexpr int NTH = MT * 2 * 32;                 // (M-tile) x (group) warps
     static constexpr int QS = pad8mod32(KB);               // row stride of element-indexed arrays
-    static constexpr int QC = 32, QCT = QC / 8;            // quadrature chunk, its N-tiles
+    static constexpr int QC = 16, QCT = QC / 8;            // quadrature chunk, its N-tiles
     static constexpr int QCS = pad8mod32(QC);
     static constexpr int NCH = cdiv(NQ, QC);
     static constexpr size_t W = 4;
@@ -85,7 +89,7 @@ struct CfgTC {
 };
 
 template <int N>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(CfgTC<N>::NTH, 2)
 k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, float *__restrict__ Qout,
                  float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt,
                  int block0) {
@@ -96,6 +100,7 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
     constexpr int NFP = C::NFP, NFQ = C::NFQ, NFQ8 = C::NFQ8, NF = C::NF, FLD = 4;
     constexpr int KB = C::KB, QS = C::QS, QC = C::QC, QCT = C::QCT, QCS = C::QCS;
     constexpr int FSQ = NPP * QS;                          // one field of sQ / sR
+    constexpr int NTH = C::NTH, MT = C::MT;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
@@ -124,7 +129,7 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
     constexpr int GS = C::GS;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int mt = warp & 3, grp = warp >> 2;              // M-tile, pressure / velocity group
+    const int mt = warp % MT, grp = warp / MT;             // M-tile, pressure / velocity group
     const int e0 = mt * 16;
     const int g = lane >> 2, t = lane & 3;
     const size_t S = P.Kpad;
@@ -133,7 +138,7 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
 
     if (tid == 0) mbar_init(bar, 1);
     // element fields via 16-byte cp.async, node rows >= NP zero
-    for (int r = tid; r < FLD * NPP * (KB / 4); r += 256) {
+    for (int r = tid; r < FLD * NPP * (KB / 4); r += NTH) {
         const int e4 = (r % (KB / 4)) * 4, row = r / (KB / 4);
         const int c = row / NPP, j = row % NPP;
         float *dst = sQ + row * QS + e4;
@@ -164,7 +169,7 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
         {   // geometric factors of this chunk: cp.async, overlapped with the MMAs below
             const int qn = min(QC, NQ - ch * QC);
             __syncthreads();                   // previous chunk's epilogue is done with sGeo
-            for (int r = tid; r < 9 * qn * (KB / 4); r += 256) {
+            for (int r = tid; r < 9 * qn * (KB / 4); r += NTH) {
                 const int e4 = (r % (KB / 4)) * 4, row = r / (KB / 4);
                 const int rr = row / qn, qq = row % qn;
                 cp_async16(sGeo + (rr * QC + qq) * GS + e4, P.geo + (size_t)(rr * NQ + ch * QC + qq) * S + kblk + e4);
@@ -187,23 +192,20 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
                 if (grp == 0) {
                     AFrag a;
                     load_a_colmajor(a, sQ + k0 * QS + e0, QS, lane);
+                    BFrag b[3][QCT];
 #pragma unroll
-                    for (int m = 0; m < 3; ++m) {
-                        BFrag b[QCT];
+                    for (int m = 0; m < 3; ++m)
 #pragma unroll
-                        for (int n = 0; n < QCT; ++n) load_b_rowmajor(b[n], sOpA + (m * NPP + k0) * QCS + n * 8, QCS, lane);
-                        mma3_row<QCT>(c4[m], a, b);
-                    }
+                        for (int n = 0; n < QCT; ++n) load_b_rowmajor(b[m][n], sOpA + (m * NPP + k0) * QCS + n * 8, QCS, lane);
+                    mma3_aB<3, QCT>(c4, a, b);
                 } else {
                     BFrag b[QCT];
 #pragma unroll
                     for (int n = 0; n < QCT; ++n) load_b_rowmajor(b[n], sOpA + (3 * NPP + k0) * QCS + n * 8, QCS, lane);
+                    AFrag a[3];
 #pragma unroll
-                    for (int m = 0; m < 3; ++m) {
-                        AFrag a;
-                        load_a_colmajor(a, sQ + (1 + m) * FSQ + k0 * QS + e0, QS, lane);
-                        mma3_row<QCT>(c4[m], a, b);
-                    }
+                    for (int m = 0; m < 3; ++m) load_a_colmajor(a[m], sQ + (1 + m) * FSQ + k0 * QS + e0, QS, lane);
+                    mma3_AB<3, QCT>(c4, a, b);
                 }
             }
             // pointwise geometric factors: g0 gp_i = sum_a G_ai dp_a, g1 F_a = sum_i G_ai U_i
@@ -235,25 +237,23 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
 #pragma unroll
         for (int k0 = 0; k0 < QC; k0 += 8) {
             if (grp == 0) {
+                AFrag af[3];
+                BFrag b[3][NJT];
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    AFrag af;
-                    load_a_colmajor(af, sW + ((3 + a) * QC + k0) * QS + e0, QS, lane);
-                    BFrag b[NJT];
+                    load_a_colmajor(af[a], sW + ((3 + a) * QC + k0) * QS + e0, QS, lane);
 #pragma unroll
-                    for (int n = 0; n < NJT; ++n) load_b_rowmajor(b[n], sOpB + (a * QC + k0) * NJS + n * 8, NJS, lane);
-                    mma3_row<NJT>(acc[0], af, b);
+                    for (int n = 0; n < NJT; ++n) load_b_rowmajor(b[a][n], sOpB + (a * QC + k0) * NJS + n * 8, NJS, lane);
                 }
+                mma3_sum<3, NJT>(acc[0], af, b);
             } else {
                 BFrag b[NJT];
 #pragma unroll
                 for (int n = 0; n < NJT; ++n) load_b_rowmajor(b[n], sOpB + (3 * QC + k0) * NJS + n * 8, NJS, lane);
+                AFrag af[3];
 #pragma unroll
-                for (int m = 0; m < 3; ++m) {
-                    AFrag af;
-                    load_a_colmajor(af, sW + (m * QC + k0) * QS + e0, QS, lane);
-                    mma3_row<NJT>(acc[m], af, b);
-                }
+                for (int m = 0; m < 3; ++m) load_a_colmajor(af[m], sW + (m * QC + k0) * QS + e0, QS, lane);
+                mma3_AB<3, NJT>(acc, af, b);
             }
         }
     }
@@ -263,31 +263,31 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
     const int NFQT = NF * NFQ;
     __syncthreads();
     WADG_PROF_MARK(2);
-    for (int r = tid; r < NF * KB; r += 256) {
+    for (int r = tid; r < NF * KB; r += NTH) {
         const int f = r / KB, e = r % KB;
         sNbr[r] = P.nbr[(size_t)f * S + kblk + e];
         sCode[r] = P.ncode[(size_t)f * S + kblk + e];
     }
-    for (int r = tid; r < NF * NFP8; r += 256) {
+    for (int r = tid; r < NF * NFP8; r += NTH) {
         const int f = r / NFP8, i = r % NFP8;
         sFmask[r] = i < NFP ? __ldg(P.fmask + f * NFP + i) : NP;     // row NP of sQ is zero padding
     }
-    for (int r = tid; r < NF * 6 * NFP; r += 256) sExt[r] = __ldg(P.ext_node + r);
-    for (int r = tid; r < 6 * NFP; r += 256) sPerm[r] = __ldg(P.fperm + r);
-    for (int r = tid; r < NFP8 * VS; r += 256) {                 // Vfi^T, zero padded
+    for (int r = tid; r < NF * 6 * NFP; r += NTH) sExt[r] = __ldg(P.ext_node + r);
+    for (int r = tid; r < 6 * NFP; r += NTH) sPerm[r] = __ldg(P.fperm + r);
+    for (int r = tid; r < NFP8 * VS; r += NTH) {                 // Vfi^T, zero padded
         const int i = r / VS, fq = r % VS;
         sVfi[r] = (i < NFP && fq < NFQ) ? __ldg(P.Vfi + fq * NFP + i) : 0.f;
     }
     if constexpr (NFP8 > NFP) {                                  // K-padding rows of both sP buffers
         constexpr int PADN = (NFP8 - NFP) * QS;
-        for (int r = tid; r < 2 * FLD * PADN; r += 256) {
+        for (int r = tid; r < 2 * FLD * PADN; r += NTH) {
             const int bc = r / PADN;                             // buffer * FLD + field
             sP[(bc * NFP8 + NFP) * QS + r % PADN] = 0.f;
         }
     }
     __syncthreads();
     auto gather = [&](int f, float *buf) {
-        for (int r = tid; r < FLD * NFP * KB; r += 256) {
+        for (int r = tid; r < FLD * NFP * KB; r += NTH) {
             const int e = r % KB, rest = r / KB;
             const int i = rest % NFP, c = rest / NFP;
             const int nb = sNbr[f * KB + e];
@@ -308,7 +308,7 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
     for (int f = 0; f < NF; ++f) {
         float *cur = sP + (f & 1) * (FLD * NFP8 * QS);
         // this face's normals and sJ/2, then the next face's neighbour nodes
-        for (int r = tid; r < 4 * NFQ * (KB / 4); r += 256) {
+        for (int r = tid; r < 4 * NFQ * (KB / 4); r += NTH) {
             const int e4 = (r % (KB / 4)) * 4, row = r / (KB / 4);
             const int d = row / NFQ, fq = row % NFQ;
             cp_async16(sFG + row * QS + e4, P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + kblk + e4);
@@ -344,18 +344,18 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
                 for (int n = 0; n < NFQT8; ++n) load_b_rowmajor(b[n], sVfi + k0 * VS + n * 8, VS, lane);
                 const int r0 = (grp == 0) ? sFmask[f * NFP8 + k0 + t] : k0 + t;
                 const int r1 = (grp == 0) ? sFmask[f * NFP8 + k0 + t + 4] : k0 + t + 4;
+                AFrag af[FLD];
 #pragma unroll
                 for (int c = 0; c < FLD; ++c) {
                     const float *base = (grp == 0) ? sQ + c * FSQ : cur + c * NFP8 * QS;
                     const float *p0 = base + r0 * QS + e0 + g, *p1 = base + r1 * QS + e0 + g;
-                    AFrag af;
                     Split sp;
-                    sp = split(p0[0]); af.hi[0] = sp.hi; af.lo[0] = sp.lo;
-                    sp = split(p0[8]); af.hi[1] = sp.hi; af.lo[1] = sp.lo;
-                    sp = split(p1[0]); af.hi[2] = sp.hi; af.lo[2] = sp.lo;
-                    sp = split(p1[8]); af.hi[3] = sp.hi; af.lo[3] = sp.lo;
-                    mma3_row<NFQT8>(tr[c], af, b);
+                    sp = split(p0[0]); af[c].hi[0] = sp.hi; af[c].lo[0] = sp.lo;
+                    sp = split(p0[8]); af[c].hi[1] = sp.hi; af[c].lo[1] = sp.lo;
+                    sp = split(p1[0]); af[c].hi[2] = sp.hi; af[c].lo[2] = sp.lo;
+                    sp = split(p1[8]); af[c].hi[3] = sp.hi; af[c].lo[3] = sp.lo;
                 }
+                mma3_AB<FLD, NFQT8>(tr, af, b);
             }
 #pragma unroll
             for (int c = 0; c < FLD; ++c)
@@ -370,7 +370,7 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
         }
         __syncthreads();
         // penalty flux, pointwise
-        for (int r = tid; r < NFQ * KB; r += 256) {
+        for (int r = tid; r < NFQ * KB; r += NTH) {
             const int e = r % KB, fq = r / KB;
             float mM[FLD], mP[FLD];
 #pragma unroll
@@ -409,12 +409,10 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
                 }
                 mma3_row<NJT>(acc[0], af, b);
             } else {
+                AFrag af[3];
 #pragma unroll
-                for (int m = 0; m < 3; ++m) {
-                    AFrag af;
-                    load_a_colmajor(af, sG + ((1 + m) * NFQ8 + k0) * QS + e0, QS, lane);
-                    mma3_row<NJT>(acc[m], af, b);
-                }
+                for (int m = 0; m < 3; ++m) load_a_colmajor(af[m], sG + ((1 + m) * NFQ8 + k0) * QS + e0, QS, lane);
+                mma3_AB<3, NJT>(acc, af, b);
             }
         }
         __syncthreads();
@@ -445,7 +443,7 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
             const int qn = min(QC, NQ - ch * QC);
             const int nw = P.wp ? 2 : 1;
             __syncthreads();
-            for (int r = tid; r < nw * qn * (KB / 4); r += 256) {
+            for (int r = tid; r < nw * qn * (KB / 4); r += NTH) {
                 const int e4 = (r % (KB / 4)) * 4, row = r / (KB / 4);
                 const int w = row / qn, qq = row % qn;
                 const float *src = (w == 0 ? P.wu : P.wp) + (size_t)(ch * QC + qq) * S + kblk + e4;
@@ -468,12 +466,10 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
                 BFrag b[QCT];
 #pragma unroll
                 for (int n = 0; n < QCT; ++n) load_b_rowmajor(b[n], sU1 + k0 * QCS + n * 8, QCS, lane);
+                AFrag af[2];
 #pragma unroll
-                for (int m = 0; m < 2; ++m) {
-                    AFrag af;
-                    load_a_colmajor(af, sR + (cf0 + m) * FSQ + k0 * QS + e0, QS, lane);
-                    mma3_row<QCT>(z[m], af, b);
-                }
+                for (int m = 0; m < 2; ++m) load_a_colmajor(af[m], sR + (cf0 + m) * FSQ + k0 * QS + e0, QS, lane);
+                mma3_AB<2, QCT>(z, af, b);
             }
             cp_async_wait<0>();
             __syncthreads();
@@ -500,12 +496,10 @@ k_stage_fused_tc(const fused::FProb<float> P, const float *__restrict__ Qin, flo
             BFrag b[NJT];
 #pragma unroll
             for (int n = 0; n < NJT; ++n) load_b_rowmajor(b[n], sU2 + k0 * NJS + n * 8, NJS, lane);
+            AFrag af[2];
 #pragma unroll
-            for (int m = 0; m < 2; ++m) {
-                AFrag af;
-                load_a_colmajor(af, sW2 + ((cf0 + m) * QC + k0) * QS + e0, QS, lane);
-                mma3_row<NJT>(acc[m], af, b);
-            }
+            for (int m = 0; m < 2; ++m) load_a_colmajor(af[m], sW2 + ((cf0 + m) * QC + k0) * QS + e0, QS, lane);
+            mma3_AB<2, NJT>(reinterpret_cast<float (&)[2][NJT][4]>(acc), af, b);
         }
     }
     __syncthreads();

@@ -662,10 +662,13 @@ static constexpr bool tc_available() {
     return sizeof(T) == 4 && N >= 2 && N <= 4;
 }
 
+// default per order, from B200 A/B timings: the
+// tensor-core kernel wins at N = 2 and 4, the CUDA-core kernel at N = 3
 template <typename T, int N>
 static bool use_tc() {
     if (!tc_available<T, N>()) return false;
-    return g_fused_variant != 0;
+    if (g_fused_variant >= 0) return g_fused_variant == 1;
+    return N != 3;
 }
 
 // info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),
@@ -712,7 +715,7 @@ static int fused_launch_tc(const wadg_problem *Pc, const void *Qin, void *Qout, 
         if (e != cudaSuccess) return fail(cudaGetErrorString(e));
         attr_set = true;
     }
-    tc::k_stage_fused_tc<N><<<b1 - b0, 256, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin,
+    tc::k_stage_fused_tc<N><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin,
                                                            (float *)Qout, (float *)res, (float)tp, (float)tu,
                                                            (float)a, (float)b, (float)dt, b0);
     return check_launch("wadg_stage_fused(tc)");

@@ -83,3 +83,61 @@ __device__ __forceinline__ void mma3_row(float (&c)[NT][4], const AFrag &a, cons
 
 }  // namespace mma
 }  // namespace wadg
+
+namespace wadg {
+namespace mma {
+
+// c[m][n] += A[m] B[n]: MF x NT independent accumulators, split passes
+// interleaved across all of them (no back-to-back dependent MMAs)
+template <int MF, int NT>
+__device__ __forceinline__ void mma3_AB(float (&c)[MF][NT][4], const AFrag (&a)[MF], const BFrag (&b)[NT]) {
+#pragma unroll
+    for (int m = 0; m < MF; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) mma_tf32(c[m][n], a[m].lo, b[n].hi);
+#pragma unroll
+    for (int m = 0; m < MF; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) mma_tf32(c[m][n], a[m].hi, b[n].lo);
+#pragma unroll
+    for (int m = 0; m < MF; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) mma_tf32(c[m][n], a[m].hi, b[n].hi);
+}
+
+// c[m][n] += A B[m][n]
+template <int MF, int NT>
+__device__ __forceinline__ void mma3_aB(float (&c)[MF][NT][4], const AFrag &a, const BFrag (&b)[MF][NT]) {
+#pragma unroll
+    for (int m = 0; m < MF; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) mma_tf32(c[m][n], a.lo, b[m][n].hi);
+#pragma unroll
+    for (int m = 0; m < MF; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) mma_tf32(c[m][n], a.hi, b[m][n].lo);
+#pragma unroll
+    for (int m = 0; m < MF; ++m)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) mma_tf32(c[m][n], a.hi, b[m][n].hi);
+}
+
+// c[n] += sum_k A[k] B[k][n]
+template <int KA, int NT>
+__device__ __forceinline__ void mma3_sum(float (&c)[NT][4], const AFrag (&a)[KA], const BFrag (&b)[KA][NT]) {
+#pragma unroll
+    for (int k = 0; k < KA; ++k)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) mma_tf32(c[n], a[k].lo, b[k][n].hi);
+#pragma unroll
+    for (int k = 0; k < KA; ++k)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) mma_tf32(c[n], a[k].hi, b[k][n].lo);
+#pragma unroll
+    for (int k = 0; k < KA; ++k)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) mma_tf32(c[n], a[k].hi, b[k][n].hi);
+}
+
+}  // namespace mma
+}  // namespace wadg

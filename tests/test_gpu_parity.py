@@ -244,3 +244,35 @@ def test_two_slab_halo_path_is_bitwise_single_domain(dtype, fused, rng):
     whole_out = Qw[:, :, :mesh.K]
     split_out = torch.cat([Q[:, :, :hi - lo] for Q, (lo, hi) in zip(Qp, ranges)], dim=2)
     assert torch.equal(whole_out, split_out)
+
+
+@pytest.mark.parametrize("N", [2, 3, 4])
+def test_tensor_core_and_cuda_core_fused_kernels_agree(N, rng):
+    """fp32: the split-TF32 tensor-core fused stage and the CUDA-core FMA one
+    give the same 2 steps to fp32 rounding, and both match the oracle."""
+    from paper_1608_03836_b200 import _native
+    mesh = meshgen.warped_cube_tet_mesh(3, N)
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype="float32")
+    fl = _state3(mesh.K, refelem_np(N), rng)
+    outs = {}
+    try:
+        for v in (0, 1):
+            _native.call("wadg_debug_set_fused_variant", v)
+            disc = solver.Discretization(mesh, cfg)
+            assert disc.dev.fused_kind == v
+            st = FieldState.from_fields(fl)
+            for _ in range(2):
+                st = solver.lsrk_step(st, 2e-3, disc.rhs)
+            outs[v] = st.fields()
+    finally:
+        _native.call("wadg_debug_set_fused_variant", -1)
+    assert rel(outs[0], outs[1]) < 2e-6
+    od = O.OracleDiscretization(mesh, N, True)
+    ost = O.State(fl[0], fl[1:])
+    for _ in range(2):
+        ost = O.lsrk_step(ost, 2e-3, lambda y: O.rhs_full(y, od))
+    assert rel(outs[1], ost.fields()) < 1e-5
+
+
+def refelem_np(N):
+    return (N + 1) * (N + 2) * (N + 3) // 6
