@@ -137,7 +137,8 @@ int wadg_energy(const wadg_problem *P, const void *Q, double *partials,
 int wadg_fused_config(int dtype, int order, int32_t *info, int64_t *smem_bytes);
 
 /* Debug: force the fused-stage kernel (0: CUDA-core FMA tiles, 1: split-TF32
- * tensor-core MMA where available); -1 restores the default.  Affects
+ * warp-level mma.sync, 2: split-TF32 tcgen05 with TMEM accumulators, where
+ * available); -1 restores the default.  Affects
  * wadg_fused_config, so set it before building a problem. */
 int wadg_debug_set_fused_variant(int variant);
 
@@ -157,6 +158,11 @@ int wadg_debug_set_phase_clock_buffer(void *buf);
  * register-operand FMA chains for `iters` iterations (2*16*iters flops per
  * thread); `in` holds >= 32 values of the dtype, `out` >= 256. */
 int wadg_microbench_fma(int dtype, int blocks, int iters, const void *in, void *out, void *stream);
+
+/* Debug: validate the tcgen05 split-TF32 primitives. One CTA computes
+ * C (128 x N) = A (128 x K) B^T (row-major fp32 device arrays); mode bit 0: raw
+ * fp32 hi operands, bit 1: A_lo from TMEM, bit 2: plain TF32 (one MMA). */
+int wadg_debug_umma_test(const void *A, const void *B, void *C, int N, int K, int mode, void *stream);
 
 /* buf[(s*(dim+1) + fld)*Nfp + i] = Q[fld][fmask[send_f[s]][i]][send_k[s]] */
 int wadg_pack_halo(const wadg_problem *P, const void *Q, const int32_t *send_k,

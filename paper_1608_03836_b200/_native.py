@@ -60,6 +60,7 @@ EXPORTS = {
                           _vp], ctypes.c_int),
     "wadg_debug_set_phase_clock_buffer": ([_vp], ctypes.c_int),
     "wadg_microbench_fma": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
+    "wadg_debug_umma_test": ([_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
     "wadg_pack_halo": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, _i32, _vp, _vp], ctypes.c_int),
 }
 

@@ -1,0 +1,603 @@
+// Fused LSRK45 stage for fp32 tetrahedra on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, accumulators in TMEM, operators staged by TMA bulk
+// copies).  Same algebra as k_stage_fused / k_stage_fused_tc (strong-weak
+// volume, upwind/penalty surface, WADG update and LSRK axpy of
+// R/pkg/src/wadg/solver.py:207-301, 348-363) in one kernel per stage with Q
+// ping-ponged.
+//
+// Every dense contraction is a CTA-wide GEMM with the 128 elements of the
+// CTA as the M dimension (one element per TMEM lane):
+//   D[e, n] (+)= sum_k A[e, k] B[n, k]
+// A = per-element data (fields, quadrature values, flux), B = a reference
+// operator tile.  fp32 accuracy comes from the split x = hi + lo (hi = x with
+// the low 13 mantissa bits cleared, lo = x - hi exactly): three MMAs
+// A_lo B_hi + A_hi B_lo + A_hi B_hi per product (the dropped A_lo B_lo is
+// O(2^-22) relative).  Operator hi/lo images are packed on the host in the
+// canonical K-major no-swizzle layout (wadg_umma.cuh) and arrive by one
+// cp.async.bulk per tile; per-element A operands are written by the threads,
+// either into shared memory (fields, neighbour face nodes) or straight into
+// TMEM with tcgen05.st (quadrature values, flux), which is where the
+// epilogue thread of an element already holds them.
+//
+// Phases per CTA (one CTA of 256 threads per SM, TMEM 512 columns):
+//   load    Q -> sQ (raw fp32 = tf32 hi operand) and sQlo
+//   volume  per 16-point quadrature chunk:
+//           V1: dp_a = D_a p (N = 48), U_i = Vq u_i (N = 16 each)        -> TMEM
+//           epilogue: gp_i = sum_a G_ai dp_a, F_a = sum_i G_ai U_i       -> TMEM (hi, lo)
+//           V2: R_p += sum_a DTW_a F_a, R_u_i += (-Pq) gp_i              -> TMEM R
+//   surface per face, per 16-point half of the face rule:
+//           own traces Vf Q, exterior traces Vfi (gathered neighbour face nodes)
+//           epilogue: upwind/penalty flux * sJ/2 (* n_i)                 -> TMEM (hi, lo)
+//           lift: R_c += (-Pf) g_c
+//   update  per field pair: R_c -> shared (hi, lo); per 32-point chunk
+//           z = Vu R_c, omega z (c^2/J or 1/J), R_c (+)= Pu (omega z)
+//   LSRK    res = a res + dt R, Q_out = Q_in + b res
+#pragma once
+
+namespace wadg {
+namespace uk {
+
+using fused::cdiv;
+using fused::rup;
+
+template <int N>
+struct CfgU {
+    static constexpr int NP = fused::np_tet(N);
+    static constexpr int NPK = rup(NP, 8);      // K extent over nodes (MMA K step 8)
+    static constexpr int NPN = rup(NP, 16);     // N extent over nodes (M = 128 needs N % 16 == 0)
+    static constexpr int NQ = (N + 1) * (N + 1) * (N + 1);
+    static constexpr int QC = 16, NCH = cdiv(NQ, QC);       // volume quadrature chunks
+    static constexpr int QU = 32, NCHU = cdiv(NQ, QU);      // update quadrature chunks
+    static constexpr int NFP = fused::nfp_tri(N);
+    static constexpr int NFPK = rup(NFP, 8);
+    static constexpr int NFQ = (N + 1) * (N + 1);
+    static constexpr int NFH = cdiv(NFQ, 16);               // 16-point halves of a face rule
+    static constexpr int NF = 4, FLD = 4, ME = 128, NTH = 256;
+    static_assert(NFPK <= 16, "exterior-trace K extent must fit 16 TMEM columns per field");
+    // operator tile images (floats, hi image then lo image)
+    static constexpr int OPV1 = 2 * 64 * NPK;               // rows: D_a (3 x 16 q), Vq (16 q)
+    static constexpr int OPV2 = 2 * 4 * NPN * QC;           // 4 blocks: DTW_a (3), -Pq; rows j, K = q
+    static constexpr int OPVF = 2 * 16 * NPK;               // rows: face points of one half
+    static constexpr int OPVFI = 2 * 16 * NFPK;
+    static constexpr int OPPF = 2 * NPN * 16;               // rows j, K = face points
+    static constexpr int OPU1 = 2 * QU * NPK;
+    static constexpr int OPU2 = 2 * NPN * QU;
+    static constexpr int OPS_FACE = OPVF + OPVFI + OPPF;
+    // offsets (floats) of the packed operator buffer
+    static constexpr size_t O_V1 = 0;
+    static constexpr size_t O_V2 = O_V1 + (size_t)NCH * OPV1;
+    static constexpr size_t O_FACE = O_V2 + (size_t)NCH * OPV2;        // [f][half]{Vf, Vfi, Pf}
+    static constexpr size_t O_U1 = O_FACE + (size_t)NF * NFH * OPS_FACE;
+    static constexpr size_t O_U2 = O_U1 + (size_t)NCHU * OPU1;
+    static constexpr size_t OP_TOTAL = O_U2 + (size_t)NCHU * OPU2;
+    // shared memory (bytes)
+    static constexpr size_t MISC = 2304;
+    static_assert(128 + 4 * (NF * 6 * NFP + NF * NFP + 6 * NFP) <= MISC, "index tables exceed MISC");
+    static constexpr size_t SQF = (size_t)FLD * ME * NPK;              // floats of one field set
+    static constexpr size_t S_VOL = (size_t)(2 * OPV1 + OPV2) * 4;
+    static constexpr size_t S_EXT = (size_t)FLD * ME * NFPK * 4;
+    static constexpr size_t S_SURF = S_EXT + (size_t)2 * OPS_FACE * 4;
+    static constexpr size_t S_UPD = (size_t)2 * (OPU1 + OPU2) * 4;
+    static constexpr size_t S_OPS = fused::maxz(S_VOL, fused::maxz(S_SURF, S_UPD));
+    static constexpr size_t SMEM = MISC + 2 * SQF * 4 + S_OPS;
+    // TMEM columns
+    static constexpr uint32_t RACC = 0, SCR = 4 * NPN;
+    static_assert(SCR + 288 <= 512, "TMEM budget");
+};
+
+// issue the three split-TF32 MMAs of one K step; A from shared memory (hi, lo)
+__device__ __forceinline__ void mma3_ss(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                        uint32_t id, uint32_t acc) {
+    umma::mma_ss(d, al, bh, id, acc);
+    umma::mma_ss(d, ah, bl, id, 1u);
+    umma::mma_ss(d, ah, bh, id, 1u);
+}
+// A_hi from shared memory, A_lo from TMEM
+__device__ __forceinline__ void mma3_st(uint32_t d, uint64_t ah, uint32_t al_t, uint64_t bh, uint64_t bl,
+                                        uint32_t id, uint32_t acc) {
+    umma::mma_ts(d, al_t, bh, id, acc);
+    umma::mma_ss(d, ah, bl, id, 1u);
+    umma::mma_ss(d, ah, bh, id, 1u);
+}
+// A (hi, lo) from TMEM
+__device__ __forceinline__ void mma3_tt(uint32_t d, uint32_t ah_t, uint32_t al_t, uint64_t bh, uint64_t bl,
+                                        uint32_t id, uint32_t acc) {
+    umma::mma_ts(d, al_t, bh, id, acc);
+    umma::mma_ts(d, ah_t, bl, id, 1u);
+    umma::mma_ts(d, ah_t, bh, id, 1u);
+}
+
+// split 8 values and store hi / lo to two TMEM column groups of this warp's lanes
+__device__ __forceinline__ void st_split8(uint32_t t_hi, uint32_t t_lo, const float (&v)[8]) {
+    float hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        hi[i] = umma::tf32_hi(v[i]);
+        lo[i] = v[i] - hi[i];
+    }
+    umma::st8(t_hi, hi);
+    umma::st8(t_lo, lo);
+}
+
+template <int N>
+__global__ void __launch_bounds__(256, 1)
+k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *__restrict__ Qout,
+             float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt, int block0) {
+    using C = CfgU<N>;
+    using namespace umma;
+    constexpr int NP = C::NP, NPK = C::NPK, NPN = C::NPN, NQ = C::NQ, QC = C::QC, QU = C::QU;
+    constexpr int NFP = C::NFP, NFPK = C::NFPK, NFQ = C::NFQ, NFH = C::NFH, NF = 4, ME = 128;
+    constexpr uint32_t SBO_Q = (NPK / 4) * 128;        // 8-row group stride of NPK-wide tiles
+    constexpr uint32_t SBO_16 = 4 * 128;                // ... of 16-wide tiles
+    constexpr uint32_t SBO_32 = 8 * 128;                // ... of 32-wide tiles
+    constexpr uint32_t SBO_FP = (NFPK / 4) * 128;
+    constexpr uint32_t RACC = C::RACC, SCR = C::SCR;
+
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);            // [0] MMA, [1..3] operator tiles
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + 64);
+    int32_t *sExt = reinterpret_cast<int32_t *>(smem + 128);       // [f2 * nor + o][i]
+    int32_t *sFmask = sExt + NF * 6 * NFP;                         // [f][i]
+    int32_t *sPerm = sFmask + NF * NFP;                            // [o][i]
+    float *sQ = reinterpret_cast<float *>(smem + C::MISC);
+    float *sQlo = sQ + C::SQF;
+    float *sOp = sQlo + C::SQF;
+    const float *ops = P.opVA;                                     // packed tile images (CfgU offsets)
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int qd = warp & 3, h = warp >> 2;
+    const int e = 32 * qd + lane;                                  // element row = TMEM lane
+    const size_t S = P.Kpad;
+    const size_t kblk = (size_t)(block0 + blockIdx.x) * ME;
+    uint32_t ph_mma = 0, ph_op[3] = {0, 0, 0};
+
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) fused::mbar_init(&bar[i], 1);
+    }
+    if (warp == 0) tmem_alloc<512>(tslot);
+    for (int r = tid; r < NF * 6 * NFP; r += C::NTH) sExt[r] = __ldg(P.ext_node + r);
+    for (int r = tid; r < NF * NFP; r += C::NTH) sFmask[r] = __ldg(P.fmask + r);
+    for (int r = tid; r < 6 * NFP; r += C::NTH) sPerm[r] = __ldg(P.fperm + r);
+
+    // ---- fields -> sQ (raw fp32, the tf32 hi operand) and sQlo ------------
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+        const int c = 2 * h + cc;
+#pragma unroll
+        for (int j0 = 0; j0 < NPK; j0 += 4) {
+            float4 v;
+            float *pv = reinterpret_cast<float *>(&v);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int j = j0 + i;
+                pv[i] = j < NP ? __ldg(Qin + (size_t)(c * NP + j) * S + kblk + e) : 0.f;
+            }
+            float4 l;
+            float *pl = reinterpret_cast<float *>(&l);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pl[i] = tf32_lo(pv[i]);
+            const uint32_t o = kmaj_off<NPK>(e, j0) / 4;
+            *reinterpret_cast<float4 *>(sQ + c * ME * NPK + o) = v;
+            *reinterpret_cast<float4 *>(sQlo + c * ME * NPK + o) = l;
+        }
+    }
+    fused::fence_proxy_async();
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tm = *tslot;
+    const uint32_t tl = tm + ((uint32_t)(32 * qd) << 16);         // this warp's lane quarter
+
+    auto mma_wait = [&]() {
+        fused::mbar_wait(&bar[0], ph_mma);
+        ph_mma ^= 1u;
+        fence_after();
+    };
+    auto op_load = [&](int slot, float *dst, const float *src, uint32_t bytes) {   // thread 0
+        fused::mbar_expect_tx(&bar[1 + slot], bytes);
+        fused::bulk_g2s(dst, src, bytes, &bar[1 + slot]);
+    };
+    auto op_wait = [&](int slot) {   // thread 0
+        fused::mbar_wait(&bar[1 + slot], ph_op[slot]);
+        ph_op[slot] ^= 1u;
+    };
+    auto sync_to_mma = [&]() {   // all threads: make smem / TMEM writes visible to the MMA issuer
+        fused::fence_proxy_async();
+        fence_before();
+        __syncthreads();
+    };
+
+    // ======================= volume =======================================
+    float *sV1[2] = {sOp, sOp + C::OPV1};
+    float *sV2 = sOp + 2 * C::OPV1;
+    const uint32_t V1OUT = SCR, V2AH = SCR + 96, V2AL = SCR + 192;
+    auto issue_v1 = [&](int ch) {
+        const float *b = sV1[ch & 1];
+        const uint32_t bh0 = su32(b), bl0 = su32(b + C::OPV1 / 2);
+        const uint32_t idD = idesc_tf32(128, 48), idU = idesc_tf32(128, 16);
+#pragma unroll
+        for (int ks = 0; ks < NPK / 8; ++ks) {
+            const uint32_t koff = ks * 256;
+            // dp_a = D_a p: rows 0..47 of the tile
+            mma3_ss(tm + V1OUT, desc_k(su32(sQ) + koff, 128, SBO_Q), desc_k(su32(sQlo) + koff, 128, SBO_Q),
+                    desc_k(bh0 + koff, 128, SBO_Q), desc_k(bl0 + koff, 128, SBO_Q), idD, ks > 0);
+            // U_i = Vq u_i: rows 48..63 (8-row groups 6, 7)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const uint32_t qa = su32(sQ + (1 + i) * ME * NPK) + koff;
+                const uint32_t ql = su32(sQlo + (1 + i) * ME * NPK) + koff;
+                mma3_ss(tm + V1OUT + 48 + 16 * i, desc_k(qa, 128, SBO_Q), desc_k(ql, 128, SBO_Q),
+                        desc_k(bh0 + 6 * SBO_Q + koff, 128, SBO_Q), desc_k(bl0 + 6 * SBO_Q + koff, 128, SBO_Q),
+                        idU, ks > 0);
+            }
+        }
+    };
+    auto issue_v2 = [&](int ch) {
+        const uint32_t bh0 = su32(sV2), bl0 = su32(sV2 + C::OPV2 / 2);
+        const uint32_t id = idesc_tf32(128, NPN);
+        constexpr uint32_t BLK = NPN * QC * 4;   // bytes of one operator block
+#pragma unroll
+        for (int ks = 0; ks < QC / 8; ++ks) {
+            const uint32_t koff = ks * 256;
+            // R_p += sum_a DTW_a F_a  (F_a = quantity 3 + a)
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                mma3_tt(tm + RACC, tm + V2AH + 16 * (3 + a) + 8 * ks, tm + V2AL + 16 * (3 + a) + 8 * ks,
+                        desc_k(bh0 + a * BLK + koff, 128, SBO_16), desc_k(bl0 + a * BLK + koff, 128, SBO_16), id,
+                        (ch > 0 || ks > 0 || a > 0) ? 1u : 0u);
+            // R_u_i += (-Pq) gp_i
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                mma3_tt(tm + RACC + NPN * (1 + i), tm + V2AH + 16 * i + 8 * ks, tm + V2AL + 16 * i + 8 * ks,
+                        desc_k(bh0 + 3 * BLK + koff, 128, SBO_16), desc_k(bl0 + 3 * BLK + koff, 128, SBO_16), id,
+                        (ch > 0 || ks > 0) ? 1u : 0u);
+        }
+    };
+
+    // geometric factors of this thread's 8 points of a chunk, prefetched one chunk ahead
+    float G[9][8];
+    auto load_G = [&](int ch) {
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            const int q = ch * QC + 8 * h + p;
+#pragma unroll
+            for (int r = 0; r < 9; ++r) G[r][p] = q < NQ ? __ldg(P.geo + (size_t)(r * NQ + q) * S + kblk + e) : 0.f;
+        }
+    };
+    load_G(0);
+    if (tid == 0) {
+        op_load(0, sV1[0], ops + C::O_V1, C::OPV1 * 4);
+        op_load(2, sV2, ops + C::O_V2, C::OPV2 * 4);
+        if (C::NCH > 1) op_load(1, sV1[1], ops + C::O_V1 + C::OPV1, C::OPV1 * 4);
+        op_wait(0);
+        issue_v1(0);
+        commit(&bar[0]);
+    }
+    for (int ch = 0; ch < C::NCH; ++ch) {
+        mma_wait();                     // V1(ch) and V2(ch-1) complete
+        if (tid == 0 && ch > 0) {       // their operator tiles are free: refill for V2(ch), V1(ch+1)
+            op_load(2, sV2, ops + C::O_V2 + (size_t)ch * C::OPV2, C::OPV2 * 4);
+            if (ch + 1 < C::NCH)
+                op_load((ch + 1) & 1, sV1[(ch + 1) & 1], ops + C::O_V1 + (size_t)(ch + 1) * C::OPV1, C::OPV1 * 4);
+        }
+        {
+            float dp[3][8], U[3][8];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) ld8(tl + V1OUT + 16 * a + 8 * h, dp[a]);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) ld8(tl + V1OUT + 48 + 16 * i + 8 * h, U[i]);
+            wait_ld();
+            float gp[3][8], F[3][8];
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    gp[m][p] = G[0 * 3 + m][p] * dp[0][p] + G[1 * 3 + m][p] * dp[1][p] + G[2 * 3 + m][p] * dp[2][p];
+                    F[m][p] = G[m * 3 + 0][p] * U[0][p] + G[m * 3 + 1][p] * U[1][p] + G[m * 3 + 2][p] * U[2][p];
+                }
+            }
+            if (ch + 1 < C::NCH) load_G(ch + 1);
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+                st_split8(tl + V2AH + 16 * m + 8 * h, tl + V2AL + 16 * m + 8 * h, gp[m]);
+                st_split8(tl + V2AH + 16 * (3 + m) + 8 * h, tl + V2AL + 16 * (3 + m) + 8 * h, F[m]);
+            }
+            wait_st();
+        }
+        sync_to_mma();
+        if (tid == 0) {
+            fence_after();
+            op_wait(2);
+            issue_v2(ch);
+            if (ch + 1 < C::NCH) {
+                op_wait((ch + 1) & 1);
+                issue_v1(ch + 1);
+            }
+            commit(&bar[0]);
+        }
+    }
+    mma_wait();                         // V2 of the last chunk
+
+    // ======================= surface ======================================
+    float *sExtHi = sOp;                                       // [c][K-major 128 x NFPK]
+    float *sFace[2] = {sOp + C::S_EXT / 4, sOp + C::S_EXT / 4 + C::OPS_FACE};
+    const uint32_t OWN = SCR, EXT = SCR + 64, EXTLO = SCR + 128;
+    const int NFQT = NF * NFQ;
+    // neighbour face nodes of face f for this thread's fields {2h, 2h+1}
+    float xn[2][NFP];
+    auto gather = [&](int f) {
+        const int nb = P.nbr[(size_t)f * S + kblk + e];
+        const int code = P.ncode[(size_t)f * S + kblk + e];
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * h + cc;
+#pragma unroll
+            for (int i = 0; i < NFP; ++i) {
+                float v;
+                if (nb >= 0) {
+                    v = __ldg(Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
+                } else if (nb == -1) {   // mirror BC (solver.py:214-217): p+ = -p-, u+ = u-
+                    const float m = sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4];
+                    v = c == 0 ? -m : m;
+                } else {
+                    v = P.halo[((size_t)(-nb - 2) * 4 + c) * NFP + sPerm[(code % P.nor) * NFP + i]];
+                }
+                xn[cc][i] = v;
+            }
+        }
+    };
+    gather(0);
+    int hstep = 0;   // running index of (face, half) steps: operator buffer = hstep & 1
+    if (tid == 0) op_load(0, sFace[0], ops + C::O_FACE, C::OPS_FACE * 4);
+    for (int f = 0; f < NF; ++f) {
+        // exterior nodes -> shared (hi) and TMEM (lo), zero K padding
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * h + cc;
+            float lo[16];
+#pragma unroll
+            for (int i0 = 0; i0 < NFPK; i0 += 4) {
+                float4 v;
+                float *pv = reinterpret_cast<float *>(&v);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float x = (i0 + i < NFP) ? xn[cc][i0 + i] : 0.f;
+                    pv[i] = tf32_hi(x);
+                    lo[i0 + i] = x - pv[i];
+                }
+                *reinterpret_cast<float4 *>(sExtHi + c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4) = v;
+            }
+#pragma unroll
+            for (int i = NFPK; i < 16; ++i) lo[i] = 0.f;
+            float l0[8], l1[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                l0[i] = lo[i];
+                l1[i] = lo[8 + i];
+            }
+            st8(tl + EXTLO + 16 * c, l0);
+            st8(tl + EXTLO + 16 * c + 8, l1);
+        }
+        wait_st();
+        if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
+        sync_to_mma();
+        for (int hh = 0; hh < NFH; ++hh, ++hstep) {
+            const int buf = hstep & 1;
+            const float *fo = sFace[buf];
+            if (tid == 0) {
+                fence_after();
+                op_wait(buf);
+                // next (face, half) operators into the other buffer (its last readers finished)
+                if (f * NFH + hh + 1 < NF * NFH)
+                    op_load(buf ^ 1, sFace[buf ^ 1], ops + C::O_FACE + (size_t)(f * NFH + hh + 1) * C::OPS_FACE,
+                            C::OPS_FACE * 4);
+                const uint32_t vfh = su32(fo), vfl = su32(fo + C::OPVF / 2);
+                const uint32_t vih = su32(fo + C::OPVF), vil = su32(fo + C::OPVF + C::OPVFI / 2);
+                const uint32_t id = idesc_tf32(128, 16);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+#pragma unroll
+                    for (int ks = 0; ks < NPK / 8; ++ks) {   // own traces
+                        const uint32_t koff = ks * 256;
+                        mma3_ss(tm + OWN + 16 * c, desc_k(su32(sQ + c * ME * NPK) + koff, 128, SBO_Q),
+                                desc_k(su32(sQlo + c * ME * NPK) + koff, 128, SBO_Q), desc_k(vfh + koff, 128, SBO_Q),
+                                desc_k(vfl + koff, 128, SBO_Q), id, ks > 0);
+                    }
+#pragma unroll
+                    for (int ks = 0; ks < NFPK / 8; ++ks) {  // exterior traces
+                        const uint32_t koff = ks * 256;
+                        mma3_st(tm + EXT + 16 * c, desc_k(su32(sExtHi + c * ME * NFPK) + koff, 128, SBO_FP),
+                                tm + EXTLO + 16 * c + 8 * ks, desc_k(vih + koff, 128, SBO_FP),
+                                desc_k(vil + koff, 128, SBO_FP), id, ks > 0);
+                    }
+                }
+                commit(&bar[0]);
+            }
+            // face factors of this thread's 8 points: n_0, n_1, n_2, sJ/2
+            float fg[4][8];
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                const int fq = 16 * hh + 8 * h + p;
+#pragma unroll
+                for (int d = 0; d < 4; ++d)
+                    fg[d][p] = fq < NFQ ? __ldg(P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + kblk + e) : 0.f;
+            }
+            mma_wait();
+            {
+                float mM[4][8], mP[4][8];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    ld8(tl + OWN + 16 * c + 8 * h, mM[c]);
+                    ld8(tl + EXT + 16 * c + 8 * h, mP[c]);
+                }
+                wait_ld();
+                float g[4][8];
+#pragma unroll
+                for (int p = 0; p < 8; ++p) {
+                    const float n0 = fg[0][p], n1 = fg[1][p], n2 = fg[2][p], sJh = fg[3][p];
+                    const float dpj = mP[0][p] - mM[0][p];
+                    const float dUn = (mP[1][p] - mM[1][p]) * n0 + (mP[2][p] - mM[2][p]) * n1 + (mP[3][p] - mM[3][p]) * n2;
+                    const float avg = (mP[1][p] + mM[1][p]) * n0 + (mP[2][p] + mM[2][p]) * n1 + (mP[3][p] + mM[3][p]) * n2;
+                    const float fpp = avg - tau_p * dpj;
+                    const float fuu = dpj - tau_u * dUn;
+                    g[0][p] = fpp * sJh;
+                    g[1][p] = fuu * (sJh * n0);
+                    g[2][p] = fuu * (sJh * n1);
+                    g[3][p] = fuu * (sJh * n2);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) st_split8(tl + OWN + 16 * c + 8 * h, tl + EXT + 16 * c + 8 * h, g[c]);
+                wait_st();
+            }
+            fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                fence_after();
+                const uint32_t pfh = su32(fo + C::OPVF + C::OPVFI), pfl = su32(fo + C::OPVF + C::OPVFI + C::OPPF / 2);
+                const uint32_t id = idesc_tf32(128, NPN);
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int ks = 0; ks < 2; ++ks)
+                        mma3_tt(tm + RACC + NPN * c, tm + OWN + 16 * c + 8 * ks, tm + EXT + 16 * c + 8 * ks,
+                                desc_k(pfh + ks * 256, 128, SBO_16), desc_k(pfl + ks * 256, 128, SBO_16), id, 1u);
+                commit(&bar[0]);
+            }
+            mma_wait();
+        }
+    }
+
+    // ======================= WADG update + LSRK ===========================
+    // the surface left no TMA in flight; sQlo now holds the update A operand
+    float *sA = sQlo;                                          // [hi f0, hi f1, lo f0, lo f1] x (128 x NPK)
+    float *sU[2] = {sOp, sOp + C::OPU1 + C::OPU2};
+    const uint32_t ZC = SCR, UAH = SCR + 64, UAL = SCR + 128;
+    int ustep = 0;
+    if (tid == 0) {
+        fused::mbar_expect_tx(&bar[1], (C::OPU1 + C::OPU2) * 4);
+        fused::bulk_g2s(sU[0], ops + C::O_U1, C::OPU1 * 4, &bar[1]);
+        fused::bulk_g2s(sU[0] + C::OPU1, ops + C::O_U2, C::OPU2 * 4, &bar[1]);
+    }
+    for (int pr = 0; pr < 2; ++pr) {
+        {   // R_c (c = 2 pr + h) -> shared hi / lo
+            const int lf = h, c = 2 * pr + h;
+#pragma unroll
+            for (int j0 = 0; j0 < NPK; j0 += 8) {
+                float v[8];
+                ld8(tl + RACC + NPN * c + j0, v);
+                wait_ld();
+#pragma unroll
+                for (int jj = 0; jj < 8; jj += 4) {
+                    float4 hv, lv;
+                    float *ph = reinterpret_cast<float *>(&hv), *pl = reinterpret_cast<float *>(&lv);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        ph[i] = tf32_hi(v[jj + i]);
+                        pl[i] = v[jj + i] - ph[i];
+                    }
+                    const uint32_t o = kmaj_off<NPK>(e, j0 + jj) / 4;
+                    *reinterpret_cast<float4 *>(sA + lf * ME * NPK + o) = hv;
+                    *reinterpret_cast<float4 *>(sA + (2 + lf) * ME * NPK + o) = lv;
+                }
+            }
+        }
+        sync_to_mma();
+        for (int u = 0; u < C::NCHU; ++u, ++ustep) {
+            const int buf = ustep & 1;
+            const float *uo = sU[buf];
+            if (tid == 0) {
+                fence_after();
+                op_wait(buf);
+                const int nx = ustep + 1;   // prefetch the next chunk's tiles
+                if (nx < 2 * C::NCHU) {
+                    const int un = nx % C::NCHU;
+                    float *d = sU[nx & 1];
+                    fused::mbar_expect_tx(&bar[1 + (nx & 1)], (C::OPU1 + C::OPU2) * 4);
+                    fused::bulk_g2s(d, ops + C::O_U1 + (size_t)un * C::OPU1, C::OPU1 * 4, &bar[1 + (nx & 1)]);
+                    fused::bulk_g2s(d + C::OPU1, ops + C::O_U2 + (size_t)un * C::OPU2, C::OPU2 * 4, &bar[1 + (nx & 1)]);
+                }
+                const uint32_t bh = su32(uo), bl = su32(uo + C::OPU1 / 2);
+                const uint32_t id = idesc_tf32(128, QU);
+#pragma unroll
+                for (int lf = 0; lf < 2; ++lf)
+#pragma unroll
+                    for (int ks = 0; ks < NPK / 8; ++ks) {
+                        const uint32_t koff = ks * 256;
+                        mma3_ss(tm + ZC + 32 * lf, desc_k(su32(sA + lf * ME * NPK) + koff, 128, SBO_Q),
+                                desc_k(su32(sA + (2 + lf) * ME * NPK) + koff, 128, SBO_Q), desc_k(bh + koff, 128, SBO_Q),
+                                desc_k(bl + koff, 128, SBO_Q), id, ks > 0);
+                    }
+                commit(&bar[0]);
+            }
+            {   // omega z for this thread's field (lf = h), all 32 points
+                const int c = 2 * pr + h;
+                float w[32];
+#pragma unroll
+                for (int p = 0; p < 32; ++p) {
+                    const int q = u * QU + p;
+                    float wv = 0.f;
+                    if (q < NQ) {
+                        const float wu = __ldg(P.wu + (size_t)q * S + kblk + e);
+                        wv = c > 0 ? wu : (P.wp ? __ldg(P.wp + (size_t)q * S + kblk + e) : P.c2 * wu);
+                    }
+                    w[p] = wv;
+                }
+                mma_wait();
+#pragma unroll
+                for (int p0 = 0; p0 < 32; p0 += 8) {
+                    float z[8];
+                    ld8(tl + ZC + 32 * h + p0, z);
+                    wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) z[i] *= w[p0 + i];
+                    st_split8(tl + UAH + 32 * h + p0, tl + UAL + 32 * h + p0, z);
+                }
+                wait_st();
+            }
+            fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                fence_after();
+                const uint32_t bh = su32(uo + C::OPU1), bl = su32(uo + C::OPU1 + C::OPU2 / 2);
+                const uint32_t id = idesc_tf32(128, NPN);
+#pragma unroll
+                for (int lf = 0; lf < 2; ++lf)
+#pragma unroll
+                    for (int ks = 0; ks < QU / 8; ++ks)
+                        mma3_tt(tm + RACC + NPN * (2 * pr + lf), tm + UAH + 32 * lf + 8 * ks, tm + UAL + 32 * lf + 8 * ks,
+                                desc_k(bh + ks * 256, 128, SBO_32), desc_k(bl + ks * 256, 128, SBO_32), id,
+                                (u > 0 || ks > 0) ? 1u : 0u);
+                commit(&bar[0]);
+            }
+            mma_wait();
+        }
+    }
+
+    // res = a res + dt Minv(rhs); Q_out = Q_in + b res   (fields 2h, 2h+1)
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+        const int c = 2 * h + cc;
+#pragma unroll
+        for (int j0 = 0; j0 < NPK; j0 += 8) {
+            float v[8];
+            ld8(tl + RACC + NPN * c + j0, v);
+            wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int j = j0 + i;
+                if (j < NP) {
+                    const size_t o = (size_t)(c * NP + j) * S + kblk + e;
+                    const float r = (a_rk == 0.f) ? dt * v[i] : a_rk * res[o] + dt * v[i];
+                    res[o] = r;
+                    Qout[o] = sQ[c * ME * NPK + kmaj_off<NPK>(e, j) / 4] + b_rk * r;
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tm);
+}
+
+}  // namespace uk
+}  // namespace wadg

@@ -28,6 +28,8 @@ namespace wadg {
 #include "wadg_fused.cuh"
 #include "wadg_mma.cuh"
 #include "wadg_fused_tc.cuh"
+#include "wadg_umma.cuh"
+#include "wadg_fused_umma.cuh"
 
 namespace wadg {
 
@@ -654,7 +656,21 @@ static fused::FProb<T> make_fprob(const wadg_problem &p) {
     return q;
 }
 
-static int g_fused_variant = -1;   // debug override: 0 CUDA-core, 1 tensor-core, -1 default
+static int g_fused_variant = -1;   // debug override: 0 CUDA-core, 1 mma.sync, 2 tcgen05, -1 default
+
+// tcgen05 (TMEM / TMA) fused stage: fp32, orders whose 128-element tile fits
+template <typename T, int N>
+static constexpr bool umma_available() {
+    if constexpr (sizeof(T) == 4 && N >= 2 && N <= 4) return uk::CfgU<N>::SMEM <= 227 * 1024;
+    return false;
+}
+
+template <typename T, int N>
+static bool use_umma() {
+    if (!umma_available<T, N>()) return false;
+    if (g_fused_variant >= 0) return g_fused_variant == 2;
+    return false;
+}
 
 // tensor-core (split-TF32 mma.sync) fused stage: fp32, orders with a 64-element tile
 template <typename T, int N>
@@ -678,8 +694,17 @@ static int fused_cfg(int32_t *info, int64_t *smem) {
     size_t sm = 0;
     int32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool done = false;
+    if constexpr (umma_available<T, N>()) {
+        if (use_umma<T, N>()) {
+            using C = uk::CfgU<N>;
+            const int32_t w[8] = {2, C::ME, C::QC, C::NCH, C::NPK, C::NPN, C::NFPK, C::NFH};
+            for (int i = 0; i < 8; ++i) v[i] = w[i];
+            sm = C::SMEM;
+            done = true;
+        }
+    }
     if constexpr (tc_available<T, N>()) {
-        if (use_tc<T, N>()) {
+        if (!done && use_tc<T, N>()) {
             using C = tc::CfgTC<N>;
             const int32_t w[8] = {1, C::KB, C::QC, C::NCH, C::NPP, C::QCS, C::NJS, C::NFQ8};
             for (int i = 0; i < 8; ++i) v[i] = w[i];
@@ -721,9 +746,34 @@ static int fused_launch_tc(const wadg_problem *Pc, const void *Qin, void *Qout, 
     return check_launch("wadg_stage_fused(tc)");
 }
 
+template <int N>
+static int fused_launch_umma(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
+                             double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
+    using C = uk::CfgU<N>;
+    if (Pc->Kpad % C::ME) return fail("Kpad must be a multiple of the fused block size");
+    const int nblk = Pc->Kpad / C::ME;
+    if (b1 < 0 || b1 > nblk) b1 = nblk;
+    if (b0 < 0) b0 = 0;
+    if (b1 <= b0) return 0;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(uk::k_stage_umma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::SMEM);
+        if (e != cudaSuccess) return fail(cudaGetErrorString(e));
+        attr_set = true;
+    }
+    uk::k_stage_umma<N><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin, (float *)Qout,
+                                                        (float *)res, (float)tp, (float)tu, (float)a, (float)b,
+                                                        (float)dt, b0);
+    return check_launch("wadg_stage_fused(umma)");
+}
+
 template <typename T, int N>
 static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
                         double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
+    if constexpr (umma_available<T, N>()) {
+        if (use_umma<T, N>()) return fused_launch_umma<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+    }
     if constexpr (tc_available<T, N>()) {
         if (use_tc<T, N>()) return fused_launch_tc<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
     }
@@ -855,7 +905,7 @@ int wadg_debug_set_phase_clock_buffer(void *buf) {
 }
 
 int wadg_debug_set_fused_variant(int variant) {
-    if (variant < -1 || variant > 1) return fail("variant must be -1, 0 or 1");
+    if (variant < -1 || variant > 2) return fail("variant must be -1, 0, 1 or 2");
     g_fused_variant = variant;
     return 0;
 }
@@ -972,4 +1022,99 @@ __global__ void k_mma_test(const float *A, const float *B, float *C, int K) {
 extern "C" int wadg_debug_mma_test(const void *A, const void *B, void *C, int K, void *stream) {
     wadg::k_mma_test<<<1, 32, 0, (cudaStream_t)stream>>>((const float *)A, (const float *)B, (float *)C, K);
     return check_launch("wadg_debug_mma_test");
+}
+
+// Debug / validation of the tcgen05 primitives (wadg_umma.cuh): one CTA of 128
+// threads computes C (128 x N) = A (128 x K) B^T, A row-major (128 x K), B
+// row-major (N x K), with split-TF32 tcgen05.mma (A_lo B_hi + A_hi B_lo +
+// A_hi B_hi).  mode bit 0: hi operands are the raw fp32 values (the tensor core
+// ignores the low mantissa bits) instead of masked copies; bit 1: A_lo comes
+// from TMEM (TS form) instead of shared memory; bit 2: plain TF32 (one MMA).
+namespace wadg {
+__global__ void __launch_bounds__(128) k_umma_test(const float *A, const float *B, float *C, int N, int K, int mode) {
+    using namespace umma;
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(sm + 8);
+    float *sA = reinterpret_cast<float *>(sm + 128);
+    float *sAlo = sA + 128 * K;
+    float *sB = sAlo + 128 * K;
+    float *sBlo = sB + 256 * K;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t SBO = (uint32_t)(K / 4) * 128u;
+    auto off = [&](int r, int k) { return (int)(((r >> 3) * SBO + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4) / 4); };
+    for (int i = tid; i < 128 * K; i += 128) {
+        const int r = i / K, k = i % K;
+        const float x = A[i];
+        sA[off(r, k)] = (mode & 1) ? x : tf32_hi(x);
+        sAlo[off(r, k)] = tf32_lo(x);
+    }
+    for (int i = tid; i < N * K; i += 128) {
+        const int r = i / K, k = i % K;
+        const float x = B[i];
+        sB[off(r, k)] = (mode & 1) ? x : tf32_hi(x);
+        sBlo[off(r, k)] = tf32_lo(x);
+    }
+    if (tid == 0) {
+        fused::mbar_init(bar, 1);
+    }
+    if (warp == 0) tmem_alloc<512>(slot);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tm = *slot;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    if (mode & 2) {   // A_lo into TMEM columns 256 + k
+        for (int k0 = 0; k0 < K; k0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = tf32_lo(A[tid * K + k0 + i]);
+            st8(tm + lane_base + 256 + k0, v);
+        }
+        wait_st();
+        fence_before();
+        __syncthreads();
+        fence_after();
+    }
+    if (tid == 0) {
+        const uint32_t id = idesc_tf32(128, N);
+        for (int ks = 0; ks < K / 8; ++ks) {
+            const uint64_t ah = desc_k(su32(sA) + ks * 256, 128, SBO), al = desc_k(su32(sAlo) + ks * 256, 128, SBO);
+            const uint64_t bh = desc_k(su32(sB) + ks * 256, 128, SBO), bl = desc_k(su32(sBlo) + ks * 256, 128, SBO);
+            if (mode & 4) {
+                mma_ss(tm, ah, bh, id, ks > 0);
+            } else {
+                if (mode & 2)
+                    mma_ts(tm, tm + 256 + ks * 8, bh, id, ks > 0);
+                else
+                    mma_ss(tm, al, bh, id, ks > 0);
+                mma_ss(tm, ah, bl, id, 1);
+                mma_ss(tm, ah, bh, id, 1);
+            }
+        }
+        commit(bar);
+    }
+    fused::mbar_wait(bar, 0);
+    fence_after();
+    for (int c0 = 0; c0 < N; c0 += 8) {
+        float v[8];
+        ld8(tm + lane_base + c0, v);
+        wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) C[tid * N + c0 + i] = v[i];
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tm);
+}
+}  // namespace wadg
+
+extern "C" int wadg_debug_umma_test(const void *A, const void *B, void *C, int N, int K, int mode, void *stream) {
+    if (N % 8 || N < 8 || N > 256 || K % 8 || K < 8 || K > 64) return fail("umma test: bad N / K");
+    const size_t smem = 128 + (size_t)(2 * 128 * K + 2 * 256 * K) * 4;
+    cudaFuncSetAttribute(wadg::k_umma_test, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    wadg::k_umma_test<<<1, 128, smem, (cudaStream_t)stream>>>((const float *)A, (const float *)B, (float *)C, N, K,
+                                                              mode);
+    return check_launch("wadg_debug_umma_test");
 }

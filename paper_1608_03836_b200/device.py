@@ -69,6 +69,72 @@ def neighbour_tables(mesh, n_orient, k0=0, k1=None, halo=None):
     return nbr.T.astype(np.int32), ncode.T.astype(np.int32)
 
 
+def tf32_split(a):
+    """fp32 x = hi + lo exactly, hi = x with the low 13 mantissa bits cleared
+    (the tensor core's TF32 view of x)."""
+    x = np.ascontiguousarray(a, dtype=np.float32)
+    hi = (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    return hi, (x - hi).astype(np.float32)
+
+
+def kmajor_image(B):
+    """Canonical K-major no-swizzle UMMA image of B (rows x K), rows % 8 == 0,
+    K % 4 == 0: 8-row x 4-value core matrices of 128 contiguous bytes, core
+    matrices adjacent along K contiguous (LBO = 128 B), 8-row groups
+    (K/4)*128 B apart (csrc/wadg_umma.cuh)."""
+    R, KT = B.shape
+    assert R % 8 == 0 and KT % 4 == 0
+    return B.reshape(R // 8, 8, KT // 4, 4).transpose(0, 2, 1, 3).ravel()
+
+
+def split_images(*blocks):
+    """hi images of all blocks, then lo images (one operator tile)."""
+    his, los = zip(*(tf32_split(b) for b in blocks))
+    return np.concatenate([kmajor_image(h) for h in his] + [kmajor_image(lo) for lo in los])
+
+
+def umma_operator_images(ref, ru, cfg):
+    """All reference operators of the tcgen05 fused stage (csrc/wadg_fused_umma.cuh,
+    CfgU offsets): volume chunks {D_a; Vq}, {DTW_a, -Pq}; per face and 16-point
+    half {Vf, Vfi, -Pf}; update chunks Vu, Pu."""
+    NP, NQ = ref.Np, ref.Nq
+    QC, NCH, NPK, NPN, NFPK, NFH = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"], cfg["nfq8"]
+    QU = 32
+    NCHU = -(-NQ // QU)
+    nf, nfq, nfp = ref.n_faces, ref.nfq, ref.nfp
+    DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
+
+    def rows(M, r0, n, kt):                 # rows r0.. r0+n of M (zero past the end), K padded to kt
+        out = np.zeros((n, kt))
+        r1 = min(M.shape[0], r0 + n)
+        if r1 > r0:
+            out[:r1 - r0, :M.shape[1]] = M[r0:r1]
+        return out
+
+    parts = []
+    for ch in range(NCH):                   # V1: rows a*16 + qq -> D_a, 48 + qq -> Vq
+        parts.append(split_images(np.vstack([rows(D, ch * QC, QC, NPK) for D in ref.Dq]
+                                            + [rows(ref.Vq, ch * QC, QC, NPK)])))
+    for ch in range(NCH):                   # V2: blocks (NPN rows j) x (QC columns q)
+        blocks = [rows(M.T, ch * QC, QC, NPN).T for M in DTW + [-ref.Pq]]
+        parts.append(split_images(*blocks))
+    for f in range(nf):
+        for hh in range(NFH):
+            Vf = rows(ref.Vfq[f * nfq:(f + 1) * nfq], hh * 16, 16, NPK)
+            Vfi = rows(ref.face_interp, hh * 16, 16, NFPK)
+            Pf = rows((-ref.Pfq[:, f * nfq:(f + 1) * nfq]).T, hh * 16, 16, NPN).T
+            parts.append(split_images(Vf))
+            parts.append(split_images(Vfi))
+            parts.append(split_images(Pf))
+    for u in range(NCHU):
+        parts.append(split_images(rows(ru.Vq, u * QU, QU, NPK)))
+    for u in range(NCHU):
+        parts.append(split_images(rows(ru.Pq.T, u * QU, QU, NPN).T))
+    out = np.concatenate(parts).astype(np.float32)
+    assert nfp <= NFPK
+    return out
+
+
 class DeviceProblem:
     """All device arrays of one (mesh range, reference elements, medium) and
     the C struct pointing at them."""
@@ -186,6 +252,14 @@ class DeviceProblem:
         NP, NQ = ref.Np, ref.Nq
         nf, nfq = ref.n_faces, ref.nfq
         DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
+        if cfg["kind"] == 2:                    # tcgen05 kernel: one buffer of K-major tile images
+            packed = umma_operator_images(ref, ru, cfg)
+            self.ops["umma"] = self._t(packed, torch.float32)
+            for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
+                setattr(self.struct, name, self.ops["umma"].data_ptr())
+            self.fused_kind = 2
+            self.struct.order = N
+            return kb if self.Kpad % kb == 0 else None
         if cfg["kind"] == 0:                    # CUDA-core kernel layouts
             NPP = roundup(NP, 4)
             NQP = nch * qc

@@ -248,15 +248,15 @@ def test_two_slab_halo_path_is_bitwise_single_domain(dtype, fused, rng):
 
 @pytest.mark.parametrize("N", [2, 3, 4])
 def test_tensor_core_and_cuda_core_fused_kernels_agree(N, rng):
-    """fp32: the split-TF32 tensor-core fused stage and the CUDA-core FMA one
-    give the same 2 steps to fp32 rounding, and both match the oracle."""
+    """fp32: the split-TF32 tcgen05 and mma.sync fused stages and the CUDA-core
+    FMA one give the same 2 steps to fp32 rounding, and all match the oracle."""
     from paper_1608_03836_b200 import _native
     mesh = meshgen.warped_cube_tet_mesh(3, N)
     cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype="float32")
     fl = _state3(mesh.K, refelem_np(N), rng)
     outs = {}
     try:
-        for v in (0, 1):
+        for v in (0, 1, 2):
             _native.call("wadg_debug_set_fused_variant", v)
             disc = solver.Discretization(mesh, cfg)
             assert disc.dev.fused_kind == v
@@ -267,11 +267,13 @@ def test_tensor_core_and_cuda_core_fused_kernels_agree(N, rng):
     finally:
         _native.call("wadg_debug_set_fused_variant", -1)
     assert rel(outs[0], outs[1]) < 2e-6
+    assert rel(outs[0], outs[2]) < 2e-6
     od = O.OracleDiscretization(mesh, N, True)
     ost = O.State(fl[0], fl[1:])
     for _ in range(2):
         ost = O.lsrk_step(ost, 2e-3, lambda y: O.rhs_full(y, od))
     assert rel(outs[1], ost.fields()) < 1e-5
+    assert rel(outs[2], ost.fields()) < 1e-5
 
 
 def refelem_np(N):

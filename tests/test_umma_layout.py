@@ -1,0 +1,45 @@
+"""Host side of the tcgen05 fused stage (no GPU): the TF32 hi/lo split is exact
+and the K-major no-swizzle tile image puts B[r, k] at the byte offset the
+kernel's descriptors address (csrc/wadg_umma.cuh kmaj_off), and the packed
+operator buffer has exactly the CfgU size."""
+
+import numpy as np
+import pytest
+
+from paper_1608_03836_b200 import device, refelem
+
+
+def test_tf32_split_is_exact_and_hi_is_tf32():
+    x = np.random.default_rng(0).standard_normal(10000).astype(np.float32) * 1e3
+    hi, lo = device.tf32_split(x)
+    assert np.array_equal((hi.astype(np.float64) + lo.astype(np.float64)).astype(np.float32), x)
+    assert np.all(hi.view(np.uint32) & np.uint32(0x1FFF) == 0)
+    assert np.all(np.abs(lo) <= np.abs(x) * 2.0 ** -10)
+
+
+@pytest.mark.parametrize("R,KT", [(16, 40), (48, 16), (64, 24), (32, 8)])
+def test_kmajor_image_offsets(R, KT):
+    B = np.arange(R * KT, dtype=np.float64).reshape(R, KT)
+    img = device.kmajor_image(B)
+    for r in range(R):
+        for k in range(KT):
+            off = (r // 8) * (KT // 4) * 128 + (k // 4) * 128 + (r % 8) * 16 + (k % 4) * 4
+            assert img[off // 4] == B[r, k]
+
+
+@pytest.mark.parametrize("N", [2, 3, 4])
+def test_operator_image_size(N):
+    ref = refelem.build_reference_element(N, refelem.ElementShape.Tetrahedron)
+    rup = lambda a, b: -(-a // b) * b
+    NP, NQ = ref.Np, ref.Nq
+    NPK, NPN, NFPK = rup(NP, 8), rup(NP, 16), rup(ref.nfp, 8)
+    NFH, NCH, NCHU = -(-ref.nfq // 16), -(-NQ // 16), -(-NQ // 32)
+    cfg = dict(qc=16, nch=NCH, npp=NPK, qcs=NPN, njs=NFPK, nfq8=NFH)
+    img = device.umma_operator_images(ref, ref, cfg)
+    expect = (NCH * 2 * 64 * NPK + NCH * 2 * 4 * NPN * 16
+              + 4 * NFH * (2 * 16 * NPK + 2 * 16 * NFPK + 2 * NPN * 16) + NCHU * (2 * 32 * NPK + 2 * NPN * 32))
+    assert img.size == expect and img.dtype == np.float32
+    # first tile: D_r rows (quadrature points 0..15), hi + lo reproduce fp32(D_r)
+    half = 64 * NPK
+    t = (img[:half] + img[half:2 * half]).reshape(8, NPK // 4, 8, 4).transpose(0, 2, 1, 3).reshape(64, NPK)
+    assert np.array_equal(t[:16, :NP], ref.Dq[0][:16].astype(np.float32))
