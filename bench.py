@@ -248,6 +248,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--split", action="store_true", help="three kernels per stage instead of the fused one")
+    ap.add_argument("--variant", type=int, default=-1,
+                    help="fused kernel: 0 CUDA-core, 1 mma.sync, 2 tcgen05 (default: per-order choice)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -265,6 +267,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    if args.variant >= 0:
+        _native.call("wadg_debug_set_fused_variant", args.variant)
     t_setup = time.perf_counter()
     mesh, cfg, medium, disc, desc = build_problem(args.config, args.order, args.dtype, rank, world)
     d = disc.dev
@@ -445,6 +449,9 @@ def main():
             "e2e": e2e,
             "gpu_launches": (5 if fused else 15) * args.steps,
             "stage_kernel": "wadg_stage_fused" if fused else "wadg_volume+wadg_surface+wadg_update_lsrk",
+            "fused_kernel": ({0: "k_stage_fused (CUDA-core FMA)", 1: "k_stage_fused_tc (mma.sync split-TF32)",
+                              2: "k_stage_umma (tcgen05 split-TF32, TMEM)"}.get(getattr(d, "fused_kind", -1))
+                             if fused else None),
             "clocks": clk,
             "storage_words_per_element": {"wadg_weights": 2 * Nqu, "dense_inverse": 2 * Np2,
                                           "ratio": Np2 / Nqu},

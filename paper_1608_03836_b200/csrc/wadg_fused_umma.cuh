@@ -19,7 +19,7 @@
 // TMEM with tcgen05.st (quadrature values, flux), which is where the
 // epilogue thread of an element already holds them.
 //
-// Phases per CTA (one CTA of 256 threads per SM, TMEM 512 columns):
+// Phases per CTA (one CTA of 512 threads per SM, TMEM 512 columns):
 //   load    Q -> sQ (raw fp32 = tf32 hi operand) and sQlo
 //   volume  per 16-point quadrature chunk:
 //           V1: dp_a = D_a p (N = 48), U_i = Vq u_i (N = 16 each)        -> TMEM
@@ -52,7 +52,7 @@ struct CfgU {
     static constexpr int NFPK = rup(NFP, 8);
     static constexpr int NFQ = (N + 1) * (N + 1);
     static constexpr int NFH = cdiv(NFQ, 16);               // 16-point halves of a face rule
-    static constexpr int NF = 4, FLD = 4, ME = 128, NTH = 256;
+    static constexpr int NF = 4, FLD = 4, ME = 128, NTH = 512;
     static_assert(NFPK <= 16, "exterior-trace K extent must fit 16 TMEM columns per field");
     // operator tile images (floats, hi image then lo image)
     static constexpr int OPV1 = 2 * 64 * NPK;               // rows: D_a (3 x 16 q), Vq (16 q)
@@ -85,26 +85,45 @@ struct CfgU {
     static_assert(SCR + 288 <= 512, "TMEM budget");
 };
 
-// issue the three split-TF32 MMAs of one K step; A from shared memory (hi, lo)
-__device__ __forceinline__ void mma3_ss(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
-                                        uint32_t id, uint32_t acc) {
-    umma::mma_ss(d, al, bh, id, acc);
-    umma::mma_ss(d, ah, bl, id, 1u);
-    umma::mma_ss(d, ah, bh, id, 1u);
+// Split-TF32 K loops, issued by one whole warp (one elected lane issues):
+// D (+)= A B^T over nks K steps of 8, three MMAs per step
+// (A_lo B_hi, A_hi B_lo, A_hi B_hi).  Operand addresses advance 256 B per K
+// step in shared memory (two core matrices, LBO = 128) and 8 columns in TMEM.
+// A from shared memory (hi, lo)
+__device__ __forceinline__ void kloop_ss(uint32_t d, uint32_t ah, uint32_t al, uint32_t sboA, uint32_t bh, uint32_t bl,
+                                         uint32_t sboB, int nks, uint32_t id, uint32_t acc0) {
+#pragma unroll 1
+    for (int ks = 0; ks < nks; ++ks) {
+        const uint32_t o = ks * 256;
+        const uint64_t dbh = umma::desc_k(bh + o, 128, sboB), dah = umma::desc_k(ah + o, 128, sboA);
+        umma::mma_ss_w(d, umma::desc_k(al + o, 128, sboA), dbh, id, (ks > 0) | acc0);
+        umma::mma_ss_w(d, dah, umma::desc_k(bl + o, 128, sboB), id, 1u);
+        umma::mma_ss_w(d, dah, dbh, id, 1u);
+    }
 }
 // A_hi from shared memory, A_lo from TMEM
-__device__ __forceinline__ void mma3_st(uint32_t d, uint64_t ah, uint32_t al_t, uint64_t bh, uint64_t bl,
-                                        uint32_t id, uint32_t acc) {
-    umma::mma_ts(d, al_t, bh, id, acc);
-    umma::mma_ss(d, ah, bl, id, 1u);
-    umma::mma_ss(d, ah, bh, id, 1u);
+__device__ __forceinline__ void kloop_st(uint32_t d, uint32_t ah, uint32_t al_t, uint32_t sboA, uint32_t bh, uint32_t bl,
+                                         uint32_t sboB, int nks, uint32_t id, uint32_t acc0) {
+#pragma unroll 1
+    for (int ks = 0; ks < nks; ++ks) {
+        const uint32_t o = ks * 256;
+        const uint64_t dbh = umma::desc_k(bh + o, 128, sboB), dah = umma::desc_k(ah + o, 128, sboA);
+        umma::mma_ts_w(d, al_t + 8 * ks, dbh, id, (ks > 0) | acc0);
+        umma::mma_ss_w(d, dah, umma::desc_k(bl + o, 128, sboB), id, 1u);
+        umma::mma_ss_w(d, dah, dbh, id, 1u);
+    }
 }
 // A (hi, lo) from TMEM
-__device__ __forceinline__ void mma3_tt(uint32_t d, uint32_t ah_t, uint32_t al_t, uint64_t bh, uint64_t bl,
-                                        uint32_t id, uint32_t acc) {
-    umma::mma_ts(d, al_t, bh, id, acc);
-    umma::mma_ts(d, ah_t, bl, id, 1u);
-    umma::mma_ts(d, ah_t, bh, id, 1u);
+__device__ __forceinline__ void kloop_tt(uint32_t d, uint32_t ah_t, uint32_t al_t, uint32_t bh, uint32_t bl,
+                                         uint32_t sboB, int nks, uint32_t id, uint32_t acc0) {
+#pragma unroll 1
+    for (int ks = 0; ks < nks; ++ks) {
+        const uint32_t o = ks * 256;
+        const uint64_t dbh = umma::desc_k(bh + o, 128, sboB);
+        umma::mma_ts_w(d, al_t + 8 * ks, dbh, id, (ks > 0) | acc0);
+        umma::mma_ts_w(d, ah_t + 8 * ks, umma::desc_k(bl + o, 128, sboB), id, 1u);
+        umma::mma_ts_w(d, ah_t + 8 * ks, dbh, id, 1u);
+    }
 }
 
 // split 8 values and store hi / lo to two TMEM column groups of this warp's lanes
@@ -119,8 +138,19 @@ __device__ __forceinline__ void st_split8(uint32_t t_hi, uint32_t t_lo, const fl
     umma::st8(t_lo, lo);
 }
 
+__device__ __forceinline__ void st_split4(uint32_t t_hi, uint32_t t_lo, const float (&v)[4]) {
+    float hi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        hi[i] = umma::tf32_hi(v[i]);
+        lo[i] = v[i] - hi[i];
+    }
+    umma::st4(t_hi, hi);
+    umma::st4(t_lo, lo);
+}
+
 template <int N>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(512, 1)
 k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *__restrict__ Qout,
              float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt, int block0) {
     using C = CfgU<N>;
@@ -132,6 +162,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     constexpr uint32_t SBO_32 = 8 * 128;                // ... of 32-wide tiles
     constexpr uint32_t SBO_FP = (NFPK / 4) * 128;
     constexpr uint32_t RACC = C::RACC, SCR = C::SCR;
+    constexpr uint32_t FQB = ME * NPK * 4;              // bytes of one field in sQ / sQlo
 
     extern __shared__ __align__(1024) unsigned char smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem);            // [0] MMA, [1..3] operator tiles
@@ -145,11 +176,13 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     const float *ops = P.opVA;                                     // packed tile images (CfgU offsets)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int qd = warp & 3, h = warp >> 2;
+    const int qd = warp & 3, sub = warp >> 2;                     // lane quarter, sub-group 0..3
     const int e = 32 * qd + lane;                                  // element row = TMEM lane
+    const bool issuer = warp == 0;                                 // MMA / TMA issuing warp
     const size_t S = P.Kpad;
     const size_t kblk = (size_t)(block0 + blockIdx.x) * ME;
-    uint32_t ph_mma = 0, ph_op[3] = {0, 0, 0};
+    uint32_t ph_mma = 0, ph_op = 0;                                // phase bits: MMA, operator slots
+    WADG_PROF_MARK(0);
 
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) fused::mbar_init(&bar[i], 1);
@@ -158,11 +191,17 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     for (int r = tid; r < NF * 6 * NFP; r += C::NTH) sExt[r] = __ldg(P.ext_node + r);
     for (int r = tid; r < NF * NFP; r += C::NTH) sFmask[r] = __ldg(P.fmask + r);
     for (int r = tid; r < 6 * NFP; r += C::NTH) sPerm[r] = __ldg(P.fperm + r);
+    // neighbour tables of all faces (consumed in the surface phase)
+    int nbr[NF], ncode[NF];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+        nbr[f] = __ldg(P.nbr + (size_t)f * S + kblk + e);
+        ncode[f] = __ldg(P.ncode + (size_t)f * S + kblk + e);
+    }
 
     // ---- fields -> sQ (raw fp32, the tf32 hi operand) and sQlo ------------
-#pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-        const int c = 2 * h + cc;
+    {
+        const int c = sub;
 #pragma unroll
         for (int j0 = 0; j0 < NPK; j0 += 4) {
             float4 v;
@@ -187,19 +226,26 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     fence_after();
     const uint32_t tm = *tslot;
     const uint32_t tl = tm + ((uint32_t)(32 * qd) << 16);         // this warp's lane quarter
+    const uint32_t aQ = su32(sQ), aQlo = su32(sQlo);
+    WADG_PROF_MARK(1);
 
     auto mma_wait = [&]() {
-        fused::mbar_wait(&bar[0], ph_mma);
+        mbar_wait_bounded(&bar[0], ph_mma);
         ph_mma ^= 1u;
         fence_after();
     };
-    auto op_load = [&](int slot, float *dst, const float *src, uint32_t bytes) {   // thread 0
+    auto op_load = [&](int slot, float *dst, const float *src, uint32_t bytes) {   // one lane of the issuer
         fused::mbar_expect_tx(&bar[1 + slot], bytes);
         fused::bulk_g2s(dst, src, bytes, &bar[1 + slot]);
     };
-    auto op_wait = [&](int slot) {   // thread 0
-        fused::mbar_wait(&bar[1 + slot], ph_op[slot]);
-        ph_op[slot] ^= 1u;
+    auto op_load2 = [&](int slot, float *d0, const float *s0, uint32_t b0, float *d1, const float *s1, uint32_t b1) {
+        fused::mbar_expect_tx(&bar[1 + slot], b0 + b1);
+        fused::bulk_g2s(d0, s0, b0, &bar[1 + slot]);
+        fused::bulk_g2s(d1, s1, b1, &bar[1 + slot]);
+    };
+    auto op_wait = [&](int slot) {   // the issuing warp
+        mbar_wait_bounded(&bar[1 + slot], (ph_op >> slot) & 1u);
+        ph_op ^= 1u << slot;
     };
     auto sync_to_mma = [&]() {   // all threads: make smem / TMEM writes visible to the MMA issuer
         fused::fence_proxy_async();
@@ -208,88 +254,72 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     };
 
     // ======================= volume =======================================
-    float *sV1[2] = {sOp, sOp + C::OPV1};
+    auto sV1 = [&](int ch) { return sOp + (ch & 1) * C::OPV1; };
     float *sV2 = sOp + 2 * C::OPV1;
     const uint32_t V1OUT = SCR, V2AH = SCR + 96, V2AL = SCR + 192;
     auto issue_v1 = [&](int ch) {
-        const float *b = sV1[ch & 1];
-        const uint32_t bh0 = su32(b), bl0 = su32(b + C::OPV1 / 2);
-        const uint32_t idD = idesc_tf32(128, 48), idU = idesc_tf32(128, 16);
-#pragma unroll
-        for (int ks = 0; ks < NPK / 8; ++ks) {
-            const uint32_t koff = ks * 256;
-            // dp_a = D_a p: rows 0..47 of the tile
-            mma3_ss(tm + V1OUT, desc_k(su32(sQ) + koff, 128, SBO_Q), desc_k(su32(sQlo) + koff, 128, SBO_Q),
-                    desc_k(bh0 + koff, 128, SBO_Q), desc_k(bl0 + koff, 128, SBO_Q), idD, ks > 0);
-            // U_i = Vq u_i: rows 48..63 (8-row groups 6, 7)
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const uint32_t qa = su32(sQ + (1 + i) * ME * NPK) + koff;
-                const uint32_t ql = su32(sQlo + (1 + i) * ME * NPK) + koff;
-                mma3_ss(tm + V1OUT + 48 + 16 * i, desc_k(qa, 128, SBO_Q), desc_k(ql, 128, SBO_Q),
-                        desc_k(bh0 + 6 * SBO_Q + koff, 128, SBO_Q), desc_k(bl0 + 6 * SBO_Q + koff, 128, SBO_Q),
-                        idU, ks > 0);
-            }
-        }
+        const uint32_t bh = su32(sV1(ch)), bl = bh + C::OPV1 * 2;
+        // dp_a = D_a p (tile rows 0..47), U_i = Vq u_i (rows 48..63 = 8-row groups 6, 7)
+        kloop_ss(tm + V1OUT, aQ, aQlo, SBO_Q, bh, bl, SBO_Q, NPK / 8, idesc_tf32(128, 48), 0u);
+#pragma unroll 1
+        for (int i = 0; i < 3; ++i)
+            kloop_ss(tm + V1OUT + 48 + 16 * i, aQ + (1 + i) * FQB, aQlo + (1 + i) * FQB, SBO_Q, bh + 6 * SBO_Q,
+                     bl + 6 * SBO_Q, SBO_Q, NPK / 8, idesc_tf32(128, 16), 0u);
     };
     auto issue_v2 = [&](int ch) {
-        const uint32_t bh0 = su32(sV2), bl0 = su32(sV2 + C::OPV2 / 2);
-        const uint32_t id = idesc_tf32(128, NPN);
+        const uint32_t bh = su32(sV2), bl = bh + C::OPV2 * 2;
         constexpr uint32_t BLK = NPN * QC * 4;   // bytes of one operator block
-#pragma unroll
-        for (int ks = 0; ks < QC / 8; ++ks) {
-            const uint32_t koff = ks * 256;
-            // R_p += sum_a DTW_a F_a  (F_a = quantity 3 + a)
-#pragma unroll
-            for (int a = 0; a < 3; ++a)
-                mma3_tt(tm + RACC, tm + V2AH + 16 * (3 + a) + 8 * ks, tm + V2AL + 16 * (3 + a) + 8 * ks,
-                        desc_k(bh0 + a * BLK + koff, 128, SBO_16), desc_k(bl0 + a * BLK + koff, 128, SBO_16), id,
-                        (ch > 0 || ks > 0 || a > 0) ? 1u : 0u);
-            // R_u_i += (-Pq) gp_i
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-                mma3_tt(tm + RACC + NPN * (1 + i), tm + V2AH + 16 * i + 8 * ks, tm + V2AL + 16 * i + 8 * ks,
-                        desc_k(bh0 + 3 * BLK + koff, 128, SBO_16), desc_k(bl0 + 3 * BLK + koff, 128, SBO_16), id,
-                        (ch > 0 || ks > 0) ? 1u : 0u);
-        }
+        const uint32_t id = idesc_tf32(128, NPN);
+        // R_p += sum_a DTW_a F_a  (F_a = quantity 3 + a), R_u_i += (-Pq) gp_i
+#pragma unroll 1
+        for (int a = 0; a < 3; ++a)
+            kloop_tt(tm + RACC, tm + V2AH + 16 * (3 + a), tm + V2AL + 16 * (3 + a), bh + a * BLK, bl + a * BLK, SBO_16,
+                     QC / 8, id, (ch > 0 || a > 0) ? 1u : 0u);
+#pragma unroll 1
+        for (int i = 0; i < 3; ++i)
+            kloop_tt(tm + RACC + NPN * (1 + i), tm + V2AH + 16 * i, tm + V2AL + 16 * i, bh + 3 * BLK, bl + 3 * BLK,
+                     SBO_16, QC / 8, id, ch > 0 ? 1u : 0u);
     };
 
     // geometric factors of this thread's 8 points of a chunk, prefetched one chunk ahead
-    float G[9][8];
+    float G[9][4];
     auto load_G = [&](int ch) {
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-            const int q = ch * QC + 8 * h + p;
+        for (int p = 0; p < 4; ++p) {
+            const int q = ch * QC + 4 * sub + p;
 #pragma unroll
             for (int r = 0; r < 9; ++r) G[r][p] = q < NQ ? __ldg(P.geo + (size_t)(r * NQ + q) * S + kblk + e) : 0.f;
         }
     };
     load_G(0);
-    if (tid == 0) {
-        op_load(0, sV1[0], ops + C::O_V1, C::OPV1 * 4);
-        op_load(2, sV2, ops + C::O_V2, C::OPV2 * 4);
-        if (C::NCH > 1) op_load(1, sV1[1], ops + C::O_V1 + C::OPV1, C::OPV1 * 4);
+    if (issuer) {
+        if (lane == 0) {
+            op_load(0, sV1(0), ops + C::O_V1, C::OPV1 * 4);
+            op_load(2, sV2, ops + C::O_V2, C::OPV2 * 4);
+            if (C::NCH > 1) op_load(1, sV1(1), ops + C::O_V1 + C::OPV1, C::OPV1 * 4);
+        }
+        __syncwarp();
         op_wait(0);
         issue_v1(0);
-        commit(&bar[0]);
+        commit_w(&bar[0]);
     }
     for (int ch = 0; ch < C::NCH; ++ch) {
         mma_wait();                     // V1(ch) and V2(ch-1) complete
-        if (tid == 0 && ch > 0) {       // their operator tiles are free: refill for V2(ch), V1(ch+1)
+        if (issuer && lane == 0 && ch > 0) {   // their operator tiles are free: refill for V2(ch), V1(ch+1)
             op_load(2, sV2, ops + C::O_V2 + (size_t)ch * C::OPV2, C::OPV2 * 4);
             if (ch + 1 < C::NCH)
-                op_load((ch + 1) & 1, sV1[(ch + 1) & 1], ops + C::O_V1 + (size_t)(ch + 1) * C::OPV1, C::OPV1 * 4);
+                op_load((ch + 1) & 1, sV1(ch + 1), ops + C::O_V1 + (size_t)(ch + 1) * C::OPV1, C::OPV1 * 4);
         }
         {
-            float dp[3][8], U[3][8];
+            float dp[3][4], U[3][4];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) ld8(tl + V1OUT + 16 * a + 8 * h, dp[a]);
+            for (int a = 0; a < 3; ++a) ld4(tl + V1OUT + 16 * a + 4 * sub, dp[a]);
 #pragma unroll
-            for (int i = 0; i < 3; ++i) ld8(tl + V1OUT + 48 + 16 * i + 8 * h, U[i]);
+            for (int i = 0; i < 3; ++i) ld4(tl + V1OUT + 48 + 16 * i + 4 * sub, U[i]);
             wait_ld();
-            float gp[3][8], F[3][8];
+            float gp[3][4], F[3][4];
 #pragma unroll
-            for (int p = 0; p < 8; ++p) {
+            for (int p = 0; p < 4; ++p) {
 #pragma unroll
                 for (int m = 0; m < 3; ++m) {
                     gp[m][p] = G[0 * 3 + m][p] * dp[0][p] + G[1 * 3 + m][p] * dp[1][p] + G[2 * 3 + m][p] * dp[2][p];
@@ -299,13 +329,13 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             if (ch + 1 < C::NCH) load_G(ch + 1);
 #pragma unroll
             for (int m = 0; m < 3; ++m) {
-                st_split8(tl + V2AH + 16 * m + 8 * h, tl + V2AL + 16 * m + 8 * h, gp[m]);
-                st_split8(tl + V2AH + 16 * (3 + m) + 8 * h, tl + V2AL + 16 * (3 + m) + 8 * h, F[m]);
+                st_split4(tl + V2AH + 16 * m + 4 * sub, tl + V2AL + 16 * m + 4 * sub, gp[m]);
+                st_split4(tl + V2AH + 16 * (3 + m) + 4 * sub, tl + V2AL + 16 * (3 + m) + 4 * sub, F[m]);
             }
             wait_st();
         }
         sync_to_mma();
-        if (tid == 0) {
+        if (issuer) {
             fence_after();
             op_wait(2);
             issue_v2(ch);
@@ -313,24 +343,23 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 op_wait((ch + 1) & 1);
                 issue_v1(ch + 1);
             }
-            commit(&bar[0]);
+            commit_w(&bar[0]);
         }
     }
-    mma_wait();                         // V2 of the last chunk
 
     // ======================= surface ======================================
     float *sExtHi = sOp;                                       // [c][K-major 128 x NFPK]
-    float *sFace[2] = {sOp + C::S_EXT / 4, sOp + C::S_EXT / 4 + C::OPS_FACE};
+    auto sFace = [&](int b) { return sOp + C::S_EXT / 4 + b * C::OPS_FACE; };
     const uint32_t OWN = SCR, EXT = SCR + 64, EXTLO = SCR + 128;
     const int NFQT = NF * NFQ;
-    // neighbour face nodes of face f for this thread's fields {2h, 2h+1}
-    float xn[2][NFP];
+    // neighbour face nodes of face f for this thread's field c = sub
+    float xn[NFP];
     auto gather = [&](int f) {
-        const int nb = P.nbr[(size_t)f * S + kblk + e];
-        const int code = P.ncode[(size_t)f * S + kblk + e];
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-            const int c = 2 * h + cc;
+        // select without dynamic indexing (keeps the tables in registers)
+        const int nb = f == 0 ? nbr[0] : f == 1 ? nbr[1] : f == 2 ? nbr[2] : nbr[3];
+        const int code = f == 0 ? ncode[0] : f == 1 ? ncode[1] : f == 2 ? ncode[2] : ncode[3];
+        {
+            const int c = sub;
 #pragma unroll
             for (int i = 0; i < NFP; ++i) {
                 float v;
@@ -342,18 +371,31 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 } else {
                     v = P.halo[((size_t)(-nb - 2) * 4 + c) * NFP + sPerm[(code % P.nor) * NFP + i]];
                 }
-                xn[cc][i] = v;
+                xn[i] = v;
             }
         }
     };
+    // face factors n_0, n_1, n_2, sJ/2 of this thread's 8 points of a (face, half) step
+    float fg[4][4];
+    auto load_fg = [&](int step) {
+        const int f = step / NFH, hh = step % NFH;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            const int fq = 16 * hh + 4 * sub + p;
+#pragma unroll
+            for (int d = 0; d < 4; ++d)
+                fg[d][p] = fq < NFQ ? __ldg(P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + kblk + e) : 0.f;
+        }
+    };
     gather(0);
-    int hstep = 0;   // running index of (face, half) steps: operator buffer = hstep & 1
-    if (tid == 0) op_load(0, sFace[0], ops + C::O_FACE, C::OPS_FACE * 4);
+    load_fg(0);
+    mma_wait();                         // V2 of the last chunk
+    WADG_PROF_MARK(2);
+    if (issuer && lane == 0) op_load(0, sFace(0), ops + C::O_FACE, C::OPS_FACE * 4);
     for (int f = 0; f < NF; ++f) {
         // exterior nodes -> shared (hi) and TMEM (lo), zero K padding
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-            const int c = 2 * h + cc;
+        {
+            const int c = sub;
             float lo[16];
 #pragma unroll
             for (int i0 = 0; i0 < NFPK; i0 += 4) {
@@ -361,7 +403,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 float *pv = reinterpret_cast<float *>(&v);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const float x = (i0 + i < NFP) ? xn[cc][i0 + i] : 0.f;
+                    const float x = (i0 + i < NFP) ? xn[i0 + i] : 0.f;
                     pv[i] = tf32_hi(x);
                     lo[i0 + i] = x - pv[i];
                 }
@@ -381,59 +423,40 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         wait_st();
         if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
         sync_to_mma();
-        for (int hh = 0; hh < NFH; ++hh, ++hstep) {
-            const int buf = hstep & 1;
-            const float *fo = sFace[buf];
-            if (tid == 0) {
+        for (int hh = 0; hh < NFH; ++hh) {
+            const int step = f * NFH + hh;
+            const int buf = step & 1;
+            const float *fo = sFace(buf);
+            if (issuer) {
                 fence_after();
                 op_wait(buf);
                 // next (face, half) operators into the other buffer (its last readers finished)
-                if (f * NFH + hh + 1 < NF * NFH)
-                    op_load(buf ^ 1, sFace[buf ^ 1], ops + C::O_FACE + (size_t)(f * NFH + hh + 1) * C::OPS_FACE,
+                if (lane == 0 && step + 1 < NF * NFH)
+                    op_load(buf ^ 1, sFace(buf ^ 1), ops + C::O_FACE + (size_t)(step + 1) * C::OPS_FACE,
                             C::OPS_FACE * 4);
-                const uint32_t vfh = su32(fo), vfl = su32(fo + C::OPVF / 2);
-                const uint32_t vih = su32(fo + C::OPVF), vil = su32(fo + C::OPVF + C::OPVFI / 2);
+                const uint32_t vfh = su32(fo), vfl = vfh + C::OPVF * 2;
+                const uint32_t vih = vfh + C::OPVF * 4, vil = vih + C::OPVFI * 2;
                 const uint32_t id = idesc_tf32(128, 16);
-#pragma unroll
+#pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
-#pragma unroll
-                    for (int ks = 0; ks < NPK / 8; ++ks) {   // own traces
-                        const uint32_t koff = ks * 256;
-                        mma3_ss(tm + OWN + 16 * c, desc_k(su32(sQ + c * ME * NPK) + koff, 128, SBO_Q),
-                                desc_k(su32(sQlo + c * ME * NPK) + koff, 128, SBO_Q), desc_k(vfh + koff, 128, SBO_Q),
-                                desc_k(vfl + koff, 128, SBO_Q), id, ks > 0);
-                    }
-#pragma unroll
-                    for (int ks = 0; ks < NFPK / 8; ++ks) {  // exterior traces
-                        const uint32_t koff = ks * 256;
-                        mma3_st(tm + EXT + 16 * c, desc_k(su32(sExtHi + c * ME * NFPK) + koff, 128, SBO_FP),
-                                tm + EXTLO + 16 * c + 8 * ks, desc_k(vih + koff, 128, SBO_FP),
-                                desc_k(vil + koff, 128, SBO_FP), id, ks > 0);
-                    }
+                    kloop_ss(tm + OWN + 16 * c, aQ + c * FQB, aQlo + c * FQB, SBO_Q, vfh, vfl, SBO_Q, NPK / 8, id, 0u);
+                    kloop_st(tm + EXT + 16 * c, su32(sExtHi) + c * ME * NFPK * 4, tm + EXTLO + 16 * c, SBO_FP, vih,
+                             vil, SBO_FP, NFPK / 8, id, 0u);
                 }
-                commit(&bar[0]);
-            }
-            // face factors of this thread's 8 points: n_0, n_1, n_2, sJ/2
-            float fg[4][8];
-#pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                const int fq = 16 * hh + 8 * h + p;
-#pragma unroll
-                for (int d = 0; d < 4; ++d)
-                    fg[d][p] = fq < NFQ ? __ldg(P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + kblk + e) : 0.f;
+                commit_w(&bar[0]);
             }
             mma_wait();
             {
-                float mM[4][8], mP[4][8];
+                float mM[4][4], mP[4][4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    ld8(tl + OWN + 16 * c + 8 * h, mM[c]);
-                    ld8(tl + EXT + 16 * c + 8 * h, mP[c]);
+                    ld4(tl + OWN + 16 * c + 4 * sub, mM[c]);
+                    ld4(tl + EXT + 16 * c + 4 * sub, mP[c]);
                 }
                 wait_ld();
-                float g[4][8];
+                float g[4][4];
 #pragma unroll
-                for (int p = 0; p < 8; ++p) {
+                for (int p = 0; p < 4; ++p) {
                     const float n0 = fg[0][p], n1 = fg[1][p], n2 = fg[2][p], sJh = fg[3][p];
                     const float dpj = mP[0][p] - mM[0][p];
                     const float dUn = (mP[1][p] - mM[1][p]) * n0 + (mP[2][p] - mM[2][p]) * n1 + (mP[3][p] - mM[3][p]) * n2;
@@ -445,44 +468,54 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     g[2][p] = fuu * (sJh * n1);
                     g[3][p] = fuu * (sJh * n2);
                 }
+                if (step + 1 < NF * NFH) load_fg(step + 1);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) st_split8(tl + OWN + 16 * c + 8 * h, tl + EXT + 16 * c + 8 * h, g[c]);
+                for (int c = 0; c < 4; ++c) st_split4(tl + OWN + 16 * c + 4 * sub, tl + EXT + 16 * c + 4 * sub, g[c]);
                 wait_st();
             }
             fence_before();
             __syncthreads();
-            if (tid == 0) {
+            if (issuer) {
                 fence_after();
-                const uint32_t pfh = su32(fo + C::OPVF + C::OPVFI), pfl = su32(fo + C::OPVF + C::OPVFI + C::OPPF / 2);
+                const uint32_t pfh = su32(fo) + (C::OPVF + C::OPVFI) * 4, pfl = pfh + C::OPPF * 2;
                 const uint32_t id = idesc_tf32(128, NPN);
-#pragma unroll
+#pragma unroll 1
                 for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int ks = 0; ks < 2; ++ks)
-                        mma3_tt(tm + RACC + NPN * c, tm + OWN + 16 * c + 8 * ks, tm + EXT + 16 * c + 8 * ks,
-                                desc_k(pfh + ks * 256, 128, SBO_16), desc_k(pfl + ks * 256, 128, SBO_16), id, 1u);
-                commit(&bar[0]);
+                    kloop_tt(tm + RACC + NPN * c, tm + OWN + 16 * c, tm + EXT + 16 * c, pfh, pfl, SBO_16, 2, id, 1u);
+                commit_w(&bar[0]);
             }
             mma_wait();
         }
     }
 
+    WADG_PROF_MARK(3);
     // ======================= WADG update + LSRK ===========================
     // the surface left no TMA in flight; sQlo now holds the update A operand
     float *sA = sQlo;                                          // [hi f0, hi f1, lo f0, lo f1] x (128 x NPK)
-    float *sU[2] = {sOp, sOp + C::OPU1 + C::OPU2};
+    auto sU = [&](int b) { return sOp + b * (C::OPU1 + C::OPU2); };
     const uint32_t ZC = SCR, UAH = SCR + 64, UAL = SCR + 128;
-    int ustep = 0;
-    if (tid == 0) {
-        fused::mbar_expect_tx(&bar[1], (C::OPU1 + C::OPU2) * 4);
-        fused::bulk_g2s(sU[0], ops + C::O_U1, C::OPU1 * 4, &bar[1]);
-        fused::bulk_g2s(sU[0] + C::OPU1, ops + C::O_U2, C::OPU2 * 4, &bar[1]);
-    }
-    for (int pr = 0; pr < 2; ++pr) {
-        {   // R_c (c = 2 pr + h) -> shared hi / lo
-            const int lf = h, c = 2 * pr + h;
+    // WADG weight of this thread's field (lf = sub & 1 of the pair) at its 16 of the
+    // 32 points of an update chunk
+    float w[16];
+    auto load_w = [&](int pr, int u) {
+        const int c = 2 * pr + (sub & 1);
+        const float *src = (c > 0 || !P.wp) ? P.wu : P.wp;
+        const float sc = (c > 0 || P.wp) ? 1.f : P.c2;
 #pragma unroll
-            for (int j0 = 0; j0 < NPK; j0 += 8) {
+        for (int p = 0; p < 16; ++p) {
+            const int q = u * QU + 16 * (sub >> 1) + p;
+            w[p] = q < NQ ? sc * __ldg(src + (size_t)q * S + kblk + e) : 0.f;
+        }
+    };
+    load_w(0, 0);
+    if (issuer && lane == 0)
+        op_load2(0, sU(0), ops + C::O_U1, C::OPU1 * 4, sU(0) + C::OPU1, ops + C::O_U2, C::OPU2 * 4);
+    int ustep = 0;
+    for (int pr = 0; pr < 2; ++pr) {
+        {   // R_c (c = 2 pr + lf) -> shared hi / lo, node groups of 8 split between sub >> 1
+            const int lf = sub & 1, c = 2 * pr + lf;
+#pragma unroll
+            for (int j0 = 8 * (sub >> 1); j0 < NPK; j0 += 16) {
                 float v[8];
                 ld8(tl + RACC + NPN * c + j0, v);
                 wait_ld();
@@ -504,79 +537,62 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         sync_to_mma();
         for (int u = 0; u < C::NCHU; ++u, ++ustep) {
             const int buf = ustep & 1;
-            const float *uo = sU[buf];
-            if (tid == 0) {
+            const uint32_t uo = su32(sU(buf));
+            if (issuer) {
                 fence_after();
                 op_wait(buf);
                 const int nx = ustep + 1;   // prefetch the next chunk's tiles
-                if (nx < 2 * C::NCHU) {
+                if (lane == 0 && nx < 2 * C::NCHU) {
                     const int un = nx % C::NCHU;
-                    float *d = sU[nx & 1];
-                    fused::mbar_expect_tx(&bar[1 + (nx & 1)], (C::OPU1 + C::OPU2) * 4);
-                    fused::bulk_g2s(d, ops + C::O_U1 + (size_t)un * C::OPU1, C::OPU1 * 4, &bar[1 + (nx & 1)]);
-                    fused::bulk_g2s(d + C::OPU1, ops + C::O_U2 + (size_t)un * C::OPU2, C::OPU2 * 4, &bar[1 + (nx & 1)]);
+                    float *d = sU(nx & 1);
+                    op_load2(nx & 1, d, ops + C::O_U1 + (size_t)un * C::OPU1, C::OPU1 * 4, d + C::OPU1,
+                             ops + C::O_U2 + (size_t)un * C::OPU2, C::OPU2 * 4);
                 }
-                const uint32_t bh = su32(uo), bl = su32(uo + C::OPU1 / 2);
-                const uint32_t id = idesc_tf32(128, QU);
-#pragma unroll
+                const uint32_t sA0 = su32(sA);
+#pragma unroll 1
                 for (int lf = 0; lf < 2; ++lf)
-#pragma unroll
-                    for (int ks = 0; ks < NPK / 8; ++ks) {
-                        const uint32_t koff = ks * 256;
-                        mma3_ss(tm + ZC + 32 * lf, desc_k(su32(sA + lf * ME * NPK) + koff, 128, SBO_Q),
-                                desc_k(su32(sA + (2 + lf) * ME * NPK) + koff, 128, SBO_Q), desc_k(bh + koff, 128, SBO_Q),
-                                desc_k(bl + koff, 128, SBO_Q), id, ks > 0);
-                    }
-                commit(&bar[0]);
+                    kloop_ss(tm + ZC + 32 * lf, sA0 + lf * FQB, sA0 + (2 + lf) * FQB, SBO_Q, uo, uo + C::OPU1 * 2,
+                             SBO_Q, NPK / 8, idesc_tf32(128, QU), 0u);
+                commit_w(&bar[0]);
             }
-            {   // omega z for this thread's field (lf = h), all 32 points
-                const int c = 2 * pr + h;
-                float w[32];
+            mma_wait();
+            {   // omega z for this thread's field (lf = sub & 1) and 16 of the 32 points
+                const int lf = sub & 1, pb = 16 * (sub >> 1);
+                float wz[16];
 #pragma unroll
-                for (int p = 0; p < 32; ++p) {
-                    const int q = u * QU + p;
-                    float wv = 0.f;
-                    if (q < NQ) {
-                        const float wu = __ldg(P.wu + (size_t)q * S + kblk + e);
-                        wv = c > 0 ? wu : (P.wp ? __ldg(P.wp + (size_t)q * S + kblk + e) : P.c2 * wu);
-                    }
-                    w[p] = wv;
-                }
-                mma_wait();
+                for (int p = 0; p < 16; ++p) wz[p] = w[p];
+                const int nx = ustep + 1;
+                if (nx < 2 * C::NCHU) load_w(nx / C::NCHU, nx % C::NCHU);
 #pragma unroll
-                for (int p0 = 0; p0 < 32; p0 += 8) {
+                for (int p0 = 0; p0 < 16; p0 += 8) {
                     float z[8];
-                    ld8(tl + ZC + 32 * h + p0, z);
+                    ld8(tl + ZC + 32 * lf + pb + p0, z);
                     wait_ld();
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) z[i] *= w[p0 + i];
-                    st_split8(tl + UAH + 32 * h + p0, tl + UAL + 32 * h + p0, z);
+                    for (int i = 0; i < 8; ++i) z[i] *= wz[p0 + i];
+                    st_split8(tl + UAH + 32 * lf + pb + p0, tl + UAL + 32 * lf + pb + p0, z);
                 }
                 wait_st();
             }
             fence_before();
             __syncthreads();
-            if (tid == 0) {
+            if (issuer) {
                 fence_after();
-                const uint32_t bh = su32(uo + C::OPU1), bl = su32(uo + C::OPU1 + C::OPU2 / 2);
-                const uint32_t id = idesc_tf32(128, NPN);
-#pragma unroll
+                const uint32_t bh = uo + C::OPU1 * 4, bl = bh + C::OPU2 * 2;
+#pragma unroll 1
                 for (int lf = 0; lf < 2; ++lf)
-#pragma unroll
-                    for (int ks = 0; ks < QU / 8; ++ks)
-                        mma3_tt(tm + RACC + NPN * (2 * pr + lf), tm + UAH + 32 * lf + 8 * ks, tm + UAL + 32 * lf + 8 * ks,
-                                desc_k(bh + ks * 256, 128, SBO_32), desc_k(bl + ks * 256, 128, SBO_32), id,
-                                (u > 0 || ks > 0) ? 1u : 0u);
-                commit(&bar[0]);
+                    kloop_tt(tm + RACC + NPN * (2 * pr + lf), tm + UAH + 32 * lf, tm + UAL + 32 * lf, bh, bl, SBO_32,
+                             QU / 8, idesc_tf32(128, NPN), u > 0 ? 1u : 0u);
+                commit_w(&bar[0]);
             }
             mma_wait();
         }
     }
 
-    // res = a res + dt Minv(rhs); Q_out = Q_in + b res   (fields 2h, 2h+1)
-#pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-        const int c = 2 * h + cc;
+    WADG_PROF_MARK(4);
+    // res = a res + dt Minv(rhs); Q_out = Q_in + b res   (field c = sub)
+    {
+        const int c = sub;
 #pragma unroll
         for (int j0 = 0; j0 < NPK; j0 += 8) {
             float v[8];
@@ -596,6 +612,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     }
     fence_before();
     __syncthreads();
+    WADG_PROF_MARK(5);
     if (warp == 0) tmem_dealloc<512>(tm);
 }
 

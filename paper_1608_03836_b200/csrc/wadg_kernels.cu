@@ -1095,7 +1095,7 @@ __global__ void __launch_bounds__(128) k_umma_test(const float *A, const float *
         }
         commit(bar);
     }
-    fused::mbar_wait(bar, 0);
+    mbar_wait_bounded(bar, 0);
     fence_after();
     for (int c0 = 0; c0 < N; c0 += 8) {
         float v[8];

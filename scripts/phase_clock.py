@@ -28,7 +28,10 @@ def main():
     ap.add_argument("--n", type=int, default=32)
     ap.add_argument("--order", type=int, default=4)
     ap.add_argument("--dtype", default="float32")
+    ap.add_argument("--variant", type=int, default=-1)
     args = ap.parse_args()
+    if args.variant >= 0:
+        _native.call("wadg_debug_set_fused_variant", args.variant)
     mesh = meshgen.warped_cube_tet_mesh(args.n, args.order)
     cfg = solver.SolverConfig(N=args.order, formulation=solver.Formulation.StrongWeak, dtype=args.dtype)
     disc = solver.Discretization(mesh, cfg)
