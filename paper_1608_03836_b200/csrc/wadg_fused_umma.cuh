@@ -37,6 +37,14 @@
 namespace wadg {
 namespace uk {
 
+// debug: fine-grained clocks of the tcgen05 stage (slots 8..31 of a 32-slot
+// per-CTA record in P.prof; phase marks use WADG_PROF_MARK as elsewhere)
+#define UMMA_MARK0(slot) UMMA_MARK(slot, threadIdx.x == 0)
+#define UMMA_MARK(slot, cond)                                                                  \
+    do {                                                                                       \
+        if (P.prof && (cond)) P.prof[(size_t)blockIdx.x * 32 + (slot)] = clock64();            \
+    } while (0)
+
 using fused::cdiv;
 using fused::rup;
 
@@ -175,14 +183,16 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     float *sOp = sQlo + C::SQF;
     const float *ops = P.opVA;                                     // packed tile images (CfgU offsets)
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // warp index through a shuffle: provably warp-uniform, so the issuer branch
+    // and its descriptor arithmetic stay on the uniform datapath
+    const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
     const int qd = warp & 3, sub = warp >> 2;                     // lane quarter, sub-group 0..3
     const int e = 32 * qd + lane;                                  // element row = TMEM lane
     const bool issuer = warp == 0;                                 // MMA / TMA issuing warp
     const size_t S = P.Kpad;
     const size_t kblk = (size_t)(block0 + blockIdx.x) * ME;
     uint32_t ph_mma = 0, ph_op = 0;                                // phase bits: MMA, operator slots
-    WADG_PROF_MARK(0);
+    UMMA_MARK0(0);
 
     if (tid == 0) {
         for (int i = 0; i < 4; ++i) fused::mbar_init(&bar[i], 1);
@@ -227,7 +237,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     const uint32_t tm = *tslot;
     const uint32_t tl = tm + ((uint32_t)(32 * qd) << 16);         // this warp's lane quarter
     const uint32_t aQ = su32(sQ), aQlo = su32(sQlo);
-    WADG_PROF_MARK(1);
+    UMMA_MARK0(1);
 
     auto mma_wait = [&]() {
         mbar_wait_bounded(&bar[0], ph_mma);
@@ -257,28 +267,47 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     auto sV1 = [&](int ch) { return sOp + (ch & 1) * C::OPV1; };
     float *sV2 = sOp + 2 * C::OPV1;
     const uint32_t V1OUT = SCR, V2AH = SCR + 96, V2AL = SCR + 192;
+    // MMA issue order: K step, split term, then accumulator region, so that
+    // consecutive MMAs never accumulate into the same TMEM columns (a small-N
+    // MMA is otherwise serialised behind its predecessor's accumulate)
     auto issue_v1 = [&](int ch) {
         const uint32_t bh = su32(sV1(ch)), bl = bh + C::OPV1 * 2;
-        // dp_a = D_a p (tile rows 0..47), U_i = Vq u_i (rows 48..63 = 8-row groups 6, 7)
-        kloop_ss(tm + V1OUT, aQ, aQlo, SBO_Q, bh, bl, SBO_Q, NPK / 8, idesc_tf32(128, 48), 0u);
+        const uint32_t idD = idesc_tf32(128, 48), idU = idesc_tf32(128, 16);
+        // region 0: dp_a = D_a p (tile rows 0..47); regions 1..3: U_i = Vq u_i (rows 48..63)
 #pragma unroll 1
-        for (int i = 0; i < 3; ++i)
-            kloop_ss(tm + V1OUT + 48 + 16 * i, aQ + (1 + i) * FQB, aQlo + (1 + i) * FQB, SBO_Q, bh + 6 * SBO_Q,
-                     bl + 6 * SBO_Q, SBO_Q, NPK / 8, idesc_tf32(128, 16), 0u);
+        for (int ks = 0; ks < NPK / 8; ++ks) {
+            const uint32_t o = ks * 256;
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint32_t a = (t == 0 ? aQlo : aQ) + r * FQB + o;
+                    const uint32_t b = (t == 1 ? bl : bh) + (r ? 6 * SBO_Q : 0) + o;
+                    mma_ss_w(tm + V1OUT + (r ? 32 + 16 * r : 0), desc_k(a, 128, SBO_Q), desc_k(b, 128, SBO_Q),
+                             r ? idU : idD, (ks > 0 || t > 0) ? 1u : 0u);
+                }
+        }
     };
     auto issue_v2 = [&](int ch) {
         const uint32_t bh = su32(sV2), bl = bh + C::OPV2 * 2;
         constexpr uint32_t BLK = NPN * QC * 4;   // bytes of one operator block
         const uint32_t id = idesc_tf32(128, NPN);
-        // R_p += sum_a DTW_a F_a  (F_a = quantity 3 + a), R_u_i += (-Pq) gp_i
+        // R_p += sum_a DTW_a F_a  (F_a = quantity 3 + a), R_u_a += (-Pq) gp_a, interleaved
 #pragma unroll 1
-        for (int a = 0; a < 3; ++a)
-            kloop_tt(tm + RACC, tm + V2AH + 16 * (3 + a), tm + V2AL + 16 * (3 + a), bh + a * BLK, bl + a * BLK, SBO_16,
-                     QC / 8, id, (ch > 0 || a > 0) ? 1u : 0u);
-#pragma unroll 1
-        for (int i = 0; i < 3; ++i)
-            kloop_tt(tm + RACC + NPN * (1 + i), tm + V2AH + 16 * i, tm + V2AL + 16 * i, bh + 3 * BLK, bl + 3 * BLK,
-                     SBO_16, QC / 8, id, ch > 0 ? 1u : 0u);
+        for (int ks = 0; ks < QC / 8; ++ks) {
+            const uint32_t o = ks * 256;
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const uint32_t ab = (t == 0 ? V2AL : V2AH) + 8 * ks;
+                    const uint32_t bb = (t == 1 ? bl : bh) + o;
+                    mma_ts_w(tm + RACC, tm + ab + 16 * (3 + a), desc_k(bb + a * BLK, 128, SBO_16), id,
+                             (ch > 0 || ks > 0 || t > 0 || a > 0) ? 1u : 0u);
+                    mma_ts_w(tm + RACC + NPN * (1 + a), tm + ab + 16 * a, desc_k(bb + 3 * BLK, 128, SBO_16), id,
+                             (ch > 0 || ks > 0 || t > 0) ? 1u : 0u);
+                }
+        }
     };
 
     // geometric factors of this thread's 8 points of a chunk, prefetched one chunk ahead
@@ -304,7 +333,11 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         commit_w(&bar[0]);
     }
     for (int ch = 0; ch < C::NCH; ++ch) {
+        UMMA_MARK(8, ch == 3 && tid == 0);
+        UMMA_MARK(16, ch == 3 && tid == 511);
         mma_wait();                     // V1(ch) and V2(ch-1) complete
+        UMMA_MARK(9, ch == 3 && tid == 0);
+        UMMA_MARK(17, ch == 3 && tid == 511);
         if (issuer && lane == 0 && ch > 0) {   // their operator tiles are free: refill for V2(ch), V1(ch+1)
             op_load(2, sV2, ops + C::O_V2 + (size_t)ch * C::OPV2, C::OPV2 * 4);
             if (ch + 1 < C::NCH)
@@ -317,6 +350,8 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 #pragma unroll
             for (int i = 0; i < 3; ++i) ld4(tl + V1OUT + 48 + 16 * i + 4 * sub, U[i]);
             wait_ld();
+            UMMA_MARK(10, ch == 3 && tid == 0);
+            UMMA_MARK(18, ch == 3 && tid == 511);
             float gp[3][4], F[3][4];
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
@@ -333,17 +368,24 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 st_split4(tl + V2AH + 16 * (3 + m) + 4 * sub, tl + V2AL + 16 * (3 + m) + 4 * sub, F[m]);
             }
             wait_st();
+            UMMA_MARK(11, ch == 3 && tid == 0);
+            UMMA_MARK(19, ch == 3 && tid == 511);
         }
         sync_to_mma();
+        UMMA_MARK(12, ch == 3 && tid == 0);
+        UMMA_MARK(20, ch == 3 && tid == 511);
         if (issuer) {
             fence_after();
             op_wait(2);
+            UMMA_MARK(13, ch == 3 && tid == 0);
             issue_v2(ch);
+            UMMA_MARK(14, ch == 3 && tid == 0);
             if (ch + 1 < C::NCH) {
                 op_wait((ch + 1) & 1);
                 issue_v1(ch + 1);
             }
             commit_w(&bar[0]);
+            UMMA_MARK(15, ch == 3 && tid == 0);
         }
     }
 
@@ -390,7 +432,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     gather(0);
     load_fg(0);
     mma_wait();                         // V2 of the last chunk
-    WADG_PROF_MARK(2);
+    UMMA_MARK0(2);
     if (issuer && lane == 0) op_load(0, sFace(0), ops + C::O_FACE, C::OPS_FACE * 4);
     for (int f = 0; f < NF; ++f) {
         // exterior nodes -> shared (hi) and TMEM (lo), zero K padding
@@ -436,12 +478,32 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                             C::OPS_FACE * 4);
                 const uint32_t vfh = su32(fo), vfl = vfh + C::OPVF * 2;
                 const uint32_t vih = vfh + C::OPVF * 4, vil = vih + C::OPVFI * 2;
+                const uint32_t aE = su32(sExtHi);
                 const uint32_t id = idesc_tf32(128, 16);
 #pragma unroll 1
-                for (int c = 0; c < 4; ++c) {
-                    kloop_ss(tm + OWN + 16 * c, aQ + c * FQB, aQlo + c * FQB, SBO_Q, vfh, vfl, SBO_Q, NPK / 8, id, 0u);
-                    kloop_st(tm + EXT + 16 * c, su32(sExtHi) + c * ME * NFPK * 4, tm + EXTLO + 16 * c, SBO_FP, vih,
-                             vil, SBO_FP, NFPK / 8, id, 0u);
+                for (int ks = 0; ks < NPK / 8; ++ks) {    // own traces, 4 field accumulators
+                    const uint32_t o = ks * 256;
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            mma_ss_w(tm + OWN + 16 * c, desc_k((t == 0 ? aQlo : aQ) + c * FQB + o, 128, SBO_Q),
+                                     desc_k((t == 1 ? vfl : vfh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
+                }
+#pragma unroll 1
+                for (int ks = 0; ks < NFPK / 8; ++ks) {   // exterior traces (A_lo in TMEM)
+                    const uint32_t o = ks * 256;
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint64_t db = desc_k((t == 1 ? vil : vih) + o, 128, SBO_FP);
+                            const uint32_t acc = (ks > 0 || t > 0) ? 1u : 0u;
+                            if (t == 0)
+                                mma_ts_w(tm + EXT + 16 * c, tm + EXTLO + 16 * c + 8 * ks, db, id, acc);
+                            else
+                                mma_ss_w(tm + EXT + 16 * c, desc_k(aE + c * ME * NFPK * 4 + o, 128, SBO_FP), db, id, acc);
+                        }
                 }
                 commit_w(&bar[0]);
             }
@@ -480,15 +542,20 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 const uint32_t pfh = su32(fo) + (C::OPVF + C::OPVFI) * 4, pfl = pfh + C::OPPF * 2;
                 const uint32_t id = idesc_tf32(128, NPN);
 #pragma unroll 1
-                for (int c = 0; c < 4; ++c)
-                    kloop_tt(tm + RACC + NPN * c, tm + OWN + 16 * c, tm + EXT + 16 * c, pfh, pfl, SBO_16, 2, id, 1u);
+                for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            mma_ts_w(tm + RACC + NPN * c, tm + (t == 0 ? EXT : OWN) + 16 * c + 8 * ks,
+                                     desc_k((t == 1 ? pfl : pfh) + ks * 256, 128, SBO_16), id, 1u);
                 commit_w(&bar[0]);
             }
             mma_wait();
         }
     }
 
-    WADG_PROF_MARK(3);
+    UMMA_MARK0(3);
     // ======================= WADG update + LSRK ===========================
     // the surface left no TMA in flight; sQlo now holds the update A operand
     float *sA = sQlo;                                          // [hi f0, hi f1, lo f0, lo f1] x (128 x NPK)
@@ -548,11 +615,18 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     op_load2(nx & 1, d, ops + C::O_U1 + (size_t)un * C::OPU1, C::OPU1 * 4, d + C::OPU1,
                              ops + C::O_U2 + (size_t)un * C::OPU2, C::OPU2 * 4);
                 }
-                const uint32_t sA0 = su32(sA);
+                const uint32_t sA0 = su32(sA), id = idesc_tf32(128, QU);
 #pragma unroll 1
-                for (int lf = 0; lf < 2; ++lf)
-                    kloop_ss(tm + ZC + 32 * lf, sA0 + lf * FQB, sA0 + (2 + lf) * FQB, SBO_Q, uo, uo + C::OPU1 * 2,
-                             SBO_Q, NPK / 8, idesc_tf32(128, QU), 0u);
+                for (int ks = 0; ks < NPK / 8; ++ks) {
+                    const uint32_t o = ks * 256;
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+#pragma unroll
+                        for (int lf = 0; lf < 2; ++lf)
+                            mma_ss_w(tm + ZC + 32 * lf, desc_k(sA0 + (t == 0 ? 2 + lf : lf) * FQB + o, 128, SBO_Q),
+                                     desc_k(uo + (t == 1 ? C::OPU1 * 2 : 0) + o, 128, SBO_Q), id,
+                                     (ks > 0 || t > 0) ? 1u : 0u);
+                }
                 commit_w(&bar[0]);
             }
             mma_wait();
@@ -578,18 +652,23 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             __syncthreads();
             if (issuer) {
                 fence_after();
-                const uint32_t bh = uo + C::OPU1 * 4, bl = bh + C::OPU2 * 2;
+                const uint32_t bh = uo + C::OPU1 * 4, bl = bh + C::OPU2 * 2, id = idesc_tf32(128, NPN);
 #pragma unroll 1
-                for (int lf = 0; lf < 2; ++lf)
-                    kloop_tt(tm + RACC + NPN * (2 * pr + lf), tm + UAH + 32 * lf, tm + UAL + 32 * lf, bh, bl, SBO_32,
-                             QU / 8, idesc_tf32(128, NPN), u > 0 ? 1u : 0u);
+                for (int ks = 0; ks < QU / 8; ++ks)
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+#pragma unroll
+                        for (int lf = 0; lf < 2; ++lf)
+                            mma_ts_w(tm + RACC + NPN * (2 * pr + lf), tm + (t == 0 ? UAL : UAH) + 32 * lf + 8 * ks,
+                                     desc_k((t == 1 ? bl : bh) + ks * 256, 128, SBO_32), id,
+                                     (u > 0 || ks > 0 || t > 0) ? 1u : 0u);
                 commit_w(&bar[0]);
             }
             mma_wait();
         }
     }
 
-    WADG_PROF_MARK(4);
+    UMMA_MARK0(4);
     // res = a res + dt Minv(rhs); Q_out = Q_in + b res   (field c = sub)
     {
         const int c = sub;
@@ -612,7 +691,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     }
     fence_before();
     __syncthreads();
-    WADG_PROF_MARK(5);
+    UMMA_MARK0(5);
     if (warp == 0) tmem_dealloc<512>(tm);
 }
 

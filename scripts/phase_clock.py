@@ -38,7 +38,8 @@ def main():
     d = disc.dev
     kb = d.fused
     nblk = d.Kpad // kb
-    buf = torch.zeros(nblk * 8, dtype=torch.int64, device="cuda")
+    stride = 32 if d.fused_kind == 2 else 8      # the tcgen05 kernel keeps 32 slots per CTA
+    buf = torch.zeros(nblk * stride, dtype=torch.int64, device="cuda")
     Q = d.empty_fields().normal_()
     Q2, res = d.empty_fields(), d.empty_fields()
     sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -50,7 +51,7 @@ def main():
                      0.0, 0.1, 1e-3, 0, -1, sp)
     _native.call("wadg_debug_set_phase_clock_buffer", ctypes.c_void_p(0))
     torch.cuda.synchronize()
-    t = buf.view(nblk, 8).cpu().numpy().astype(np.float64)
+    t = buf.view(nblk, stride).cpu().numpy().astype(np.float64)[:, :8]
     nm = int(np.max(np.nonzero(t[0])[0])) + 1          # marks written by this kernel
     t = t[:, :nm]
     dur = np.diff(t, axis=1)
