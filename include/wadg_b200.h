@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define WADG_ABI_VERSION 3
+#define WADG_ABI_VERSION 4
 #define WADG_ELEMS_PER_BLOCK 32
 
 enum { WADG_F64 = 0, WADG_F32 = 1 };
@@ -91,6 +91,16 @@ typedef struct wadg_problem {
     const void *opU1;     /* Vu                                                        */
     const void *opU2;     /* Pu                                                        */
     const void *liftT;    /* Pf transposed                                             */
+    /* tcgen05 stage (kind 2): per-element data interleaved by 128-element
+     * blocks with 4 consecutive points per element, so that a thread loads 4
+     * points of its element with one 16-byte load and a warp reads 512
+     * contiguous bytes:  X_il[blk][row][point/4][128][4], points zero padded
+     * (geo: rows = dim*dim, points = Nq padded to 16; fgeo: rows = (dim+1)*Nf,
+     * points per face padded to 16; wu/wp: one row, points padded to 32).   */
+    const void *geo_il;
+    const void *fgeo_il;
+    const void *wu_il;
+    const void *wp_il;    /* NULL when wp is NULL */
 } wadg_problem;
 
 int wadg_abi_version(void);

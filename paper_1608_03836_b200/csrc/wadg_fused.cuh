@@ -229,6 +229,7 @@ struct FProb {
     const T *halo;
     int nor;
     long long *prof;   // optional: per-CTA clock64 at phase boundaries (debug)
+    const T *geo_il, *fgeo_il, *wu_il, *wp_il;   // block-interleaved copies (tcgen05 stage)
 };
 
 #define WADG_PROF_MARK(slot)                                                          \

@@ -312,12 +312,14 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 
     // geometric factors of this thread's 8 points of a chunk, prefetched one chunk ahead
     float G[9][4];
+    const size_t blk = (size_t)(block0 + blockIdx.x);
+    constexpr int GQ4 = C::NCH * 4;                 // float4 rows per geometric factor (Nq padded to 16)
     auto load_G = [&](int ch) {
+        const float4 *src = reinterpret_cast<const float4 *>(P.geo_il) + (blk * 9 * GQ4 + ch * 4 + sub) * ME + e;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const int q = ch * QC + 4 * sub + p;
-#pragma unroll
-            for (int r = 0; r < 9; ++r) G[r][p] = q < NQ ? __ldg(P.geo + (size_t)(r * NQ + q) * S + kblk + e) : 0.f;
+        for (int r = 0; r < 9; ++r) {
+            const float4 v = __ldg(src + (size_t)r * GQ4 * ME);
+            G[r][0] = v.x; G[r][1] = v.y; G[r][2] = v.z; G[r][3] = v.w;
         }
     };
     load_G(0);
@@ -419,14 +421,15 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     };
     // face factors n_0, n_1, n_2, sJ/2 of this thread's 8 points of a (face, half) step
     float fg[4][4];
+    constexpr int FQ4 = NFH * 4;                    // float4 rows per face (face rule padded to 16)
     auto load_fg = [&](int step) {
         const int f = step / NFH, hh = step % NFH;
+        const int fq4 = 4 * hh + sub;
+        const float4 *src = reinterpret_cast<const float4 *>(P.fgeo_il) + (blk * 4 * NF * FQ4 + f * FQ4 + fq4) * ME + e;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const int fq = 16 * hh + 4 * sub + p;
-#pragma unroll
-            for (int d = 0; d < 4; ++d)
-                fg[d][p] = fq < NFQ ? __ldg(P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + kblk + e) : 0.f;
+        for (int d = 0; d < 4; ++d) {
+            const float4 v = 4 * fq4 < NFQ ? __ldg(src + (size_t)d * NF * FQ4 * ME) : make_float4(0.f, 0.f, 0.f, 0.f);
+            fg[d][0] = v.x; fg[d][1] = v.y; fg[d][2] = v.z; fg[d][3] = v.w;
         }
     };
     gather(0);
@@ -564,14 +567,16 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     // WADG weight of this thread's field (lf = sub & 1 of the pair) at its 16 of the
     // 32 points of an update chunk
     float w[16];
+    constexpr int WQ4 = C::NCHU * 8;                // float4 rows of the weights (Nq padded to 32)
     auto load_w = [&](int pr, int u) {
         const int c = 2 * pr + (sub & 1);
-        const float *src = (c > 0 || !P.wp) ? P.wu : P.wp;
+        const float *base = (c > 0 || !P.wp) ? P.wu_il : P.wp_il;
         const float sc = (c > 0 || P.wp) ? 1.f : P.c2;
+        const float4 *src = reinterpret_cast<const float4 *>(base) + (blk * WQ4 + u * 8 + 4 * (sub >> 1)) * ME + e;
 #pragma unroll
-        for (int p = 0; p < 16; ++p) {
-            const int q = u * QU + 16 * (sub >> 1) + p;
-            w[p] = q < NQ ? sc * __ldg(src + (size_t)q * S + kblk + e) : 0.f;
+        for (int k = 0; k < 4; ++k) {
+            const float4 v = __ldg(src + (size_t)k * ME);
+            w[4 * k + 0] = sc * v.x; w[4 * k + 1] = sc * v.y; w[4 * k + 2] = sc * v.z; w[4 * k + 3] = sc * v.w;
         }
     };
     load_w(0, 0);

@@ -653,6 +653,8 @@ static fused::FProb<T> make_fprob(const wadg_problem &p) {
     q.wp = (const T *)p.wp; q.c2 = (T)p.c2; q.nbr = p.nbr; q.ncode = p.ncode;
     q.halo = (const T *)p.halo; q.nor = p.n_orient;
     q.prof = g_prof;
+    q.geo_il = (const T *)p.geo_il; q.fgeo_il = (const T *)p.fgeo_il;
+    q.wu_il = (const T *)p.wu_il; q.wp_il = (const T *)p.wp_il;
     return q;
 }
 
@@ -753,6 +755,8 @@ static int fused_launch_umma(const wadg_problem *Pc, const void *Qin, void *Qout
                              double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
     using C = uk::CfgU<N>;
     if (Pc->Kpad % C::ME) return fail("Kpad must be a multiple of the fused block size");
+    if (!Pc->geo_il || !Pc->fgeo_il || !Pc->wu_il || (Pc->wp && !Pc->wp_il))
+        return fail("tcgen05 stage needs the block-interleaved geo_il / fgeo_il / wu_il / wp_il");
     const int nblk = Pc->Kpad / C::ME;
     if (b1 < 0 || b1 > nblk) b1 = nblk;
     if (b0 < 0) b0 = 0;

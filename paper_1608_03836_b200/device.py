@@ -69,6 +69,19 @@ def neighbour_tables(mesh, n_orient, k0=0, k1=None, halo=None):
     return nbr.T.astype(np.int32), ncode.T.astype(np.int32)
 
 
+def interleave_blocks(x, npad, blk=128):
+    """(rows, npts, Kpad) element-fastest -> (Kpad/blk, rows, npad/4, blk, 4):
+    per 128-element block, 4 consecutive points of one element are 16
+    contiguous bytes and a warp's 32 elements read 512 contiguous bytes
+    (include/wadg_b200.h, *_il).  Points npts..npad are zero."""
+    rows, npts, Kp = x.shape
+    xp = torch.zeros((rows, npad, Kp), dtype=x.dtype, device=x.device)
+    xp[:, :npts] = x
+    out = xp.view(rows, npad // 4, 4, Kp // blk, blk).permute(3, 0, 1, 4, 2).contiguous()
+    del xp
+    return out
+
+
 def tf32_split(a):
     """fp32 x = hi + lo exactly, hi = x with the low 13 mantissa bits cleared
     (the tensor core's TF32 view of x)."""
@@ -253,13 +266,26 @@ class DeviceProblem:
         nf, nfq = ref.n_faces, ref.nfq
         DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
         if cfg["kind"] == 2:                    # tcgen05 kernel: one buffer of K-major tile images
+            if self.Kpad % kb:
+                return None
             packed = umma_operator_images(ref, ru, cfg)
             self.ops["umma"] = self._t(packed, torch.float32)
             for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
                 setattr(self.struct, name, self.ops["umma"].data_ptr())
+            # block-interleaved per-element data (include/wadg_b200.h, *_il)
+            nch, nchu, nfh = cfg["nch"], -(-ru.Nq // 32), cfg["nfq8"]
+            self.geo_il = interleave_blocks(self.geo, nch * 16, kb)
+            fg = self.fgeo.view(self.dim + 1, ref.n_faces, ref.nfq, self.Kpad)
+            self.fgeo_il = interleave_blocks(fg.reshape((self.dim + 1) * ref.n_faces, ref.nfq, self.Kpad),
+                                             nfh * 16, kb)
+            self.wu_il = interleave_blocks(self.wu.unsqueeze(0), nchu * 32, kb)
+            self.wp_il = interleave_blocks(self.wp.unsqueeze(0), nchu * 32, kb) if self.wp is not None else None
+            s = self.struct
+            s.geo_il, s.fgeo_il, s.wu_il = self.geo_il.data_ptr(), self.fgeo_il.data_ptr(), self.wu_il.data_ptr()
+            s.wp_il = self.wp_il.data_ptr() if self.wp_il is not None else None
             self.fused_kind = 2
             self.struct.order = N
-            return kb if self.Kpad % kb == 0 else None
+            return kb
         if cfg["kind"] == 0:                    # CUDA-core kernel layouts
             NPP = roundup(NP, 4)
             NQP = nch * qc

@@ -43,3 +43,14 @@ def test_operator_image_size(N):
     half = 64 * NPK
     t = (img[:half] + img[half:2 * half]).reshape(8, NPK // 4, 8, 4).transpose(0, 2, 1, 3).reshape(64, NPK)
     assert np.array_equal(t[:16, :NP], ref.Dq[0][:16].astype(np.float32))
+
+
+def test_interleave_blocks_layout():
+    import torch
+    rows, npts, Kp = 3, 13, 256
+    x = torch.arange(rows * npts * Kp, dtype=torch.float32).reshape(rows, npts, Kp)
+    y = device.interleave_blocks(x, 16, 128)
+    assert y.shape == (2, rows, 4, 128, 4)
+    for b, r, q, e in [(0, 0, 0, 0), (1, 2, 12, 127), (0, 1, 7, 33), (1, 0, 5, 64)]:
+        assert y[b, r, q // 4, e, q % 4] == x[r, q, b * 128 + e]
+    assert torch.all(y[:, :, 3, :, 1:] == 0)          # points 13..15 are zero padding
