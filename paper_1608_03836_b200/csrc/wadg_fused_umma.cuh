@@ -52,7 +52,7 @@ template <int N>
 struct CfgU {
     static constexpr int NP = fused::np_tet(N);
     static constexpr int NPK = rup(NP, 8);      // K extent over nodes (MMA K step 8)
-    static constexpr int NPN = rup(NP, 16);     // N extent over nodes (M = 128 needs N % 16 == 0)
+    static constexpr int NPN = NPK;             // N extent over nodes (M = 128 accepts N % 8 == 0 on sm_100a)
     static constexpr int NQ = (N + 1) * (N + 1) * (N + 1);
     static constexpr int QC = 16, NCH = cdiv(NQ, QC);       // volume quadrature chunks
     static constexpr int QU = 32, NCHU = cdiv(NQ, QU);      // update quadrature chunks
@@ -63,8 +63,9 @@ struct CfgU {
     static constexpr int NF = 4, FLD = 4, ME = 128, NTH = 512;
     static_assert(NFPK <= 16, "exterior-trace K extent must fit 16 TMEM columns per field");
     // operator tile images (floats, hi image then lo image)
-    static constexpr int OPV1 = 2 * 64 * NPK;               // rows: D_a (3 x 16 q), Vq (16 q)
-    static constexpr int OPV2 = 2 * 4 * NPN * QC;           // 4 blocks: DTW_a (3), -Pq; rows j, K = q
+    // volume tiles per quadrature chunk: D_a (rows a*16 + q), Vq (rows q), DTW_a (3 blocks of
+    // rows j, K = q), -Pq (rows j, K = q)
+    static constexpr int OPDA = 2 * 48 * NPK, OPVQ = 2 * 16 * NPK, OPDTW = 2 * 3 * NPN * QC, OPPQ = 2 * NPN * QC;
     static constexpr int OPVF = 2 * 16 * NPK;               // rows: face points of one half
     static constexpr int OPVFI = 2 * 16 * NFPK;
     static constexpr int OPPF = 2 * NPN * 16;               // rows j, K = face points
@@ -72,9 +73,11 @@ struct CfgU {
     static constexpr int OPU2 = 2 * NPN * QU;
     static constexpr int OPS_FACE = OPVF + OPVFI + OPPF;
     // offsets (floats) of the packed operator buffer
-    static constexpr size_t O_V1 = 0;
-    static constexpr size_t O_V2 = O_V1 + (size_t)NCH * OPV1;
-    static constexpr size_t O_FACE = O_V2 + (size_t)NCH * OPV2;        // [f][half]{Vf, Vfi, Pf}
+    static constexpr size_t O_DA = 0;
+    static constexpr size_t O_VQ = O_DA + (size_t)NCH * OPDA;
+    static constexpr size_t O_DTW = O_VQ + (size_t)NCH * OPVQ;
+    static constexpr size_t O_PQ = O_DTW + (size_t)NCH * OPDTW;
+    static constexpr size_t O_FACE = O_PQ + (size_t)NCH * OPPQ;        // [f][half]{Vf, Vfi, Pf}
     static constexpr size_t O_U1 = O_FACE + (size_t)NF * NFH * OPS_FACE;
     static constexpr size_t O_U2 = O_U1 + (size_t)NCHU * OPU1;
     static constexpr size_t OP_TOTAL = O_U2 + (size_t)NCHU * OPU2;
@@ -82,7 +85,7 @@ struct CfgU {
     static constexpr size_t MISC = 2304;
     static_assert(128 + 4 * (NF * 6 * NFP + NF * NFP + 6 * NFP) <= MISC, "index tables exceed MISC");
     static constexpr size_t SQF = (size_t)FLD * ME * NPK;              // floats of one field set
-    static constexpr size_t S_VOL = (size_t)(2 * OPV1 + OPV2) * 4;
+    static constexpr size_t S_VOL = (size_t)(2 * OPDA + 2 * OPVQ + OPDTW + OPPQ) * 4;
     static constexpr size_t S_EXT = (size_t)FLD * ME * NFPK * 4;
     static constexpr size_t S_SURF = S_EXT + (size_t)2 * OPS_FACE * 4;
     static constexpr size_t S_UPD = (size_t)2 * (OPU1 + OPU2) * 4;
@@ -91,6 +94,9 @@ struct CfgU {
     // TMEM columns
     static constexpr uint32_t RACC = 0, SCR = 4 * NPN;
     static_assert(SCR + 288 <= 512, "TMEM budget");
+    // op-tile barrier slots (bar[1 + slot]) in the volume phase; the surface and update
+    // phases use slots 0 and 1
+    static constexpr int SL_DA = 0, SL_VQ = 2, SL_PQ = 4, SL_DTW = 5;
 };
 
 // Split-TF32 K loops, issued by one whole warp (one elected lane issues):
@@ -173,7 +179,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     constexpr uint32_t FQB = ME * NPK * 4;              // bytes of one field in sQ / sQlo
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);            // [0] MMA, [1..3] operator tiles
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);            // [0] MMA, [1..6] operator tiles, [7] MMA (u chain)
     uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + 64);
     int32_t *sExt = reinterpret_cast<int32_t *>(smem + 128);       // [f2 * nor + o][i]
     int32_t *sFmask = sExt + NF * 6 * NFP;                         // [f][i]
@@ -195,7 +201,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     UMMA_MARK0(0);
 
     if (tid == 0) {
-        for (int i = 0; i < 4; ++i) fused::mbar_init(&bar[i], 1);
+        for (int i = 0; i < 8; ++i) fused::mbar_init(&bar[i], 1);
     }
     if (warp == 0) tmem_alloc<512>(tslot);
     for (int r = tid; r < NF * 6 * NFP; r += C::NTH) sExt[r] = __ldg(P.ext_node + r);
@@ -240,8 +246,13 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     UMMA_MARK0(1);
 
     auto mma_wait = [&]() {
-        mbar_wait_bounded(&bar[0], ph_mma);
+        mbar_wait_bounded(&bar[0], ph_mma & 1u);
         ph_mma ^= 1u;
+        fence_after();
+    };
+    auto mma_wait_u = [&]() {     // second MMA barrier (volume u chain)
+        mbar_wait_bounded(&bar[7], (ph_mma >> 1) & 1u);
+        ph_mma ^= 2u;
         fence_after();
     };
     auto op_load = [&](int slot, float *dst, const float *src, uint32_t bytes) {   // one lane of the issuer
@@ -264,53 +275,70 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     };
 
     // ======================= volume =======================================
-    auto sV1 = [&](int ch) { return sOp + (ch & 1) * C::OPV1; };
-    float *sV2 = sOp + 2 * C::OPV1;
-    const uint32_t V1OUT = SCR, V2AH = SCR + 96, V2AL = SCR + 192;
-    // MMA issue order: K step, split term, then accumulator region, so that
-    // consecutive MMAs never accumulate into the same TMEM columns (a small-N
-    // MMA is otherwise serialised behind its predecessor's accumulate)
-    auto issue_v1 = [&](int ch) {
-        const uint32_t bh = su32(sV1(ch)), bl = bh + C::OPV1 * 2;
-        const uint32_t idD = idesc_tf32(128, 48), idU = idesc_tf32(128, 16);
-        // region 0: dp_a = D_a p (tile rows 0..47); regions 1..3: U_i = Vq u_i (rows 48..63)
+    // Two independent chains share the geometric factors of a chunk:
+    //   p chain: dp_a = D_a p -> gp_i = sum_a G_ai dp_a -> R_u_i += (-Pq) gp_i
+    //   u chain: U_i = Vq u_i -> F_a = sum_i G_ai U_i   -> R_p   += sum_a DTW_a F_a
+    // They alternate (own TMEM regions, own MMA barriers), so the tensor core
+    // runs one chain's MMAs while the threads do the other chain's epilogue.
+    // MMA issue order: K step, split term, accumulator region, so consecutive
+    // MMAs never accumulate into the same TMEM columns.
+    const uint32_t DPO = SCR, UO = SCR + 48, GPH = SCR + 96, GPL = SCR + 144, FH = SCR + 192, FL = SCR + 240;
+    float *sDa = sOp;                                   // [2][OPDA]
+    float *sVq = sDa + 2 * C::OPDA;                     // [2][OPVQ]
+    float *sPq = sVq + 2 * C::OPVQ;                     // [OPPQ]
+    float *sDTW = sPq + C::OPPQ;                        // [OPDTW]
+    auto issue_v1p = [&](int ch) {                      // dp_a = D_a p
+        const uint32_t bh = su32(sDa + (ch & 1) * C::OPDA), bl = bh + C::OPDA * 2, id = idesc_tf32(128, 48);
+#pragma unroll 1
+        for (int ks = 0; ks < NPK / 8; ++ks) {
+            const uint32_t o = ks * 256;
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+                mma_ss_w(tm + DPO, desc_k((t == 0 ? aQlo : aQ) + o, 128, SBO_Q), desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q),
+                         id, (ks > 0 || t > 0) ? 1u : 0u);
+        }
+    };
+    auto issue_v1u = [&](int ch) {                      // U_i = Vq u_i
+        const uint32_t bh = su32(sVq + (ch & 1) * C::OPVQ), bl = bh + C::OPVQ * 2, id = idesc_tf32(128, 16);
 #pragma unroll 1
         for (int ks = 0; ks < NPK / 8; ++ks) {
             const uint32_t o = ks * 256;
 #pragma unroll
             for (int t = 0; t < 3; ++t)
 #pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const uint32_t a = (t == 0 ? aQlo : aQ) + r * FQB + o;
-                    const uint32_t b = (t == 1 ? bl : bh) + (r ? 6 * SBO_Q : 0) + o;
-                    mma_ss_w(tm + V1OUT + (r ? 32 + 16 * r : 0), desc_k(a, 128, SBO_Q), desc_k(b, 128, SBO_Q),
-                             r ? idU : idD, (ks > 0 || t > 0) ? 1u : 0u);
-                }
+                for (int i = 0; i < 3; ++i)
+                    mma_ss_w(tm + UO + 16 * i, desc_k((t == 0 ? aQlo : aQ) + (1 + i) * FQB + o, 128, SBO_Q),
+                             desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
         }
     };
-    auto issue_v2 = [&](int ch) {
-        const uint32_t bh = su32(sV2), bl = bh + C::OPV2 * 2;
-        constexpr uint32_t BLK = NPN * QC * 4;   // bytes of one operator block
-        const uint32_t id = idesc_tf32(128, NPN);
-        // R_p += sum_a DTW_a F_a  (F_a = quantity 3 + a), R_u_a += (-Pq) gp_a, interleaved
+    auto issue_v2p = [&](int ch) {                      // R_u_i += (-Pq) gp_i
+        const uint32_t bh = su32(sPq), bl = bh + C::OPPQ * 2, id = idesc_tf32(128, NPN);
 #pragma unroll 1
         for (int ks = 0; ks < QC / 8; ++ks) {
-            const uint32_t o = ks * 256;
 #pragma unroll
             for (int t = 0; t < 3; ++t)
 #pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const uint32_t ab = (t == 0 ? V2AL : V2AH) + 8 * ks;
-                    const uint32_t bb = (t == 1 ? bl : bh) + o;
-                    mma_ts_w(tm + RACC, tm + ab + 16 * (3 + a), desc_k(bb + a * BLK, 128, SBO_16), id,
+                for (int i = 0; i < 3; ++i)
+                    mma_ts_w(tm + RACC + NPN * (1 + i), tm + (t == 0 ? GPL : GPH) + 16 * i + 8 * ks,
+                             desc_k((t == 1 ? bl : bh) + ks * 256, 128, SBO_16), id, (ch > 0 || ks > 0 || t > 0) ? 1u : 0u);
+        }
+    };
+    auto issue_v2u = [&](int ch) {                      // R_p += sum_a DTW_a F_a
+        constexpr uint32_t BLK = NPN * QC * 4;
+        const uint32_t bh = su32(sDTW), bl = bh + C::OPDTW * 2, id = idesc_tf32(128, NPN);
+#pragma unroll 1
+        for (int ks = 0; ks < QC / 8; ++ks) {
+#pragma unroll
+            for (int t = 0; t < 3; ++t)
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+                    mma_ts_w(tm + RACC, tm + (t == 0 ? FL : FH) + 16 * a + 8 * ks,
+                             desc_k((t == 1 ? bl : bh) + a * BLK + ks * 256, 128, SBO_16), id,
                              (ch > 0 || ks > 0 || t > 0 || a > 0) ? 1u : 0u);
-                    mma_ts_w(tm + RACC + NPN * (1 + a), tm + ab + 16 * a, desc_k(bb + 3 * BLK, 128, SBO_16), id,
-                             (ch > 0 || ks > 0 || t > 0) ? 1u : 0u);
-                }
         }
     };
 
-    // geometric factors of this thread's 8 points of a chunk, prefetched one chunk ahead
+    // geometric factors of this thread's 4 points of a chunk, prefetched one step ahead
     float G[9][4];
     const size_t blk = (size_t)(block0 + blockIdx.x);
     constexpr int GQ4 = C::NCH * 4;                 // float4 rows per geometric factor (Nq padded to 16)
@@ -325,71 +353,97 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     load_G(0);
     if (issuer) {
         if (lane == 0) {
-            op_load(0, sV1(0), ops + C::O_V1, C::OPV1 * 4);
-            op_load(2, sV2, ops + C::O_V2, C::OPV2 * 4);
-            if (C::NCH > 1) op_load(1, sV1(1), ops + C::O_V1 + C::OPV1, C::OPV1 * 4);
+            op_load(C::SL_DA, sDa, ops + C::O_DA, C::OPDA * 4);
+            op_load(C::SL_VQ, sVq, ops + C::O_VQ, C::OPVQ * 4);
+            op_load(C::SL_PQ, sPq, ops + C::O_PQ, C::OPPQ * 4);
+            op_load(C::SL_DTW, sDTW, ops + C::O_DTW, C::OPDTW * 4);
+            if (C::NCH > 1) {
+                op_load(C::SL_DA + 1, sDa + C::OPDA, ops + C::O_DA + C::OPDA, C::OPDA * 4);
+                op_load(C::SL_VQ + 1, sVq + C::OPVQ, ops + C::O_VQ + C::OPVQ, C::OPVQ * 4);
+            }
         }
         __syncwarp();
-        op_wait(0);
-        issue_v1(0);
+        op_wait(C::SL_DA);
+        issue_v1p(0);
         commit_w(&bar[0]);
+        op_wait(C::SL_VQ);
+        issue_v1u(0);
+        commit_w(&bar[7]);
     }
     for (int ch = 0; ch < C::NCH; ++ch) {
-        UMMA_MARK(8, ch == 3 && tid == 0);
-        UMMA_MARK(16, ch == 3 && tid == 511);
-        mma_wait();                     // V1(ch) and V2(ch-1) complete
-        UMMA_MARK(9, ch == 3 && tid == 0);
-        UMMA_MARK(17, ch == 3 && tid == 511);
-        if (issuer && lane == 0 && ch > 0) {   // their operator tiles are free: refill for V2(ch), V1(ch+1)
-            op_load(2, sV2, ops + C::O_V2 + (size_t)ch * C::OPV2, C::OPV2 * 4);
-            if (ch + 1 < C::NCH)
-                op_load((ch + 1) & 1, sV1(ch + 1), ops + C::O_V1 + (size_t)(ch + 1) * C::OPV1, C::OPV1 * 4);
+        const bool more = ch + 1 < C::NCH;
+        // ---- p chain
+        mma_wait();                     // V1p(ch), V2p(ch-1) complete
+        if (issuer && lane == 0 && ch > 0) {
+            op_load(C::SL_PQ, sPq, ops + C::O_PQ + (size_t)ch * C::OPPQ, C::OPPQ * 4);
+            if (more)
+                op_load(C::SL_DA + ((ch + 1) & 1), sDa + ((ch + 1) & 1) * C::OPDA, ops + C::O_DA + (size_t)(ch + 1) * C::OPDA,
+                        C::OPDA * 4);
         }
         {
-            float dp[3][4], U[3][4];
+            float dp[3][4];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) ld4(tl + V1OUT + 16 * a + 4 * sub, dp[a]);
-#pragma unroll
-            for (int i = 0; i < 3; ++i) ld4(tl + V1OUT + 48 + 16 * i + 4 * sub, U[i]);
+            for (int a = 0; a < 3; ++a) ld4(tl + DPO + 16 * a + 4 * sub, dp[a]);
             wait_ld();
-            UMMA_MARK(10, ch == 3 && tid == 0);
-            UMMA_MARK(18, ch == 3 && tid == 511);
-            float gp[3][4], F[3][4];
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-#pragma unroll
-                for (int m = 0; m < 3; ++m) {
-                    gp[m][p] = G[0 * 3 + m][p] * dp[0][p] + G[1 * 3 + m][p] * dp[1][p] + G[2 * 3 + m][p] * dp[2][p];
-                    F[m][p] = G[m * 3 + 0][p] * U[0][p] + G[m * 3 + 1][p] * U[1][p] + G[m * 3 + 2][p] * U[2][p];
-                }
-            }
-            if (ch + 1 < C::NCH) load_G(ch + 1);
 #pragma unroll
             for (int m = 0; m < 3; ++m) {
-                st_split4(tl + V2AH + 16 * m + 4 * sub, tl + V2AL + 16 * m + 4 * sub, gp[m]);
-                st_split4(tl + V2AH + 16 * (3 + m) + 4 * sub, tl + V2AL + 16 * (3 + m) + 4 * sub, F[m]);
+                float gp[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+                    gp[p] = G[0 * 3 + m][p] * dp[0][p] + G[1 * 3 + m][p] * dp[1][p] + G[2 * 3 + m][p] * dp[2][p];
+                st_split4(tl + GPH + 16 * m + 4 * sub, tl + GPL + 16 * m + 4 * sub, gp);
             }
             wait_st();
-            UMMA_MARK(11, ch == 3 && tid == 0);
-            UMMA_MARK(19, ch == 3 && tid == 511);
         }
         sync_to_mma();
-        UMMA_MARK(12, ch == 3 && tid == 0);
-        UMMA_MARK(20, ch == 3 && tid == 511);
         if (issuer) {
             fence_after();
-            op_wait(2);
-            UMMA_MARK(13, ch == 3 && tid == 0);
-            issue_v2(ch);
-            UMMA_MARK(14, ch == 3 && tid == 0);
-            if (ch + 1 < C::NCH) {
-                op_wait((ch + 1) & 1);
-                issue_v1(ch + 1);
+            op_wait(C::SL_PQ);
+            issue_v2p(ch);
+            if (more) {
+                op_wait(C::SL_DA + ((ch + 1) & 1));
+                issue_v1p(ch + 1);
             }
             commit_w(&bar[0]);
-            UMMA_MARK(15, ch == 3 && tid == 0);
+        }
+        // ---- u chain
+        mma_wait_u();                   // V1u(ch), V2u(ch-1) complete
+        if (issuer && lane == 0 && ch > 0) {
+            op_load(C::SL_DTW, sDTW, ops + C::O_DTW + (size_t)ch * C::OPDTW, C::OPDTW * 4);
+            if (more)
+                op_load(C::SL_VQ + ((ch + 1) & 1), sVq + ((ch + 1) & 1) * C::OPVQ, ops + C::O_VQ + (size_t)(ch + 1) * C::OPVQ,
+                        C::OPVQ * 4);
+        }
+        {
+            float U[3][4];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) ld4(tl + UO + 16 * i + 4 * sub, U[i]);
+            wait_ld();
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+                float F[4];
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+                    F[p] = G[m * 3 + 0][p] * U[0][p] + G[m * 3 + 1][p] * U[1][p] + G[m * 3 + 2][p] * U[2][p];
+                st_split4(tl + FH + 16 * m + 4 * sub, tl + FL + 16 * m + 4 * sub, F);
+            }
+            if (more) load_G(ch + 1);
+            wait_st();
+        }
+        sync_to_mma();
+        if (issuer) {
+            fence_after();
+            op_wait(C::SL_DTW);
+            issue_v2u(ch);
+            if (more) {
+                op_wait(C::SL_VQ + ((ch + 1) & 1));
+                issue_v1u(ch + 1);
+            }
+            commit_w(&bar[7]);
         }
     }
+    mma_wait();                         // V2p of the last chunk
+    mma_wait_u();                       // V2u of the last chunk
 
     // ======================= surface ======================================
     float *sExtHi = sOp;                                       // [c][K-major 128 x NFPK]
@@ -434,7 +488,6 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     };
     gather(0);
     load_fg(0);
-    mma_wait();                         // V2 of the last chunk
     UMMA_MARK0(2);
     if (issuer && lane == 0) op_load(0, sFace(0), ops + C::O_FACE, C::OPS_FACE * 4);
     for (int f = 0; f < NF; ++f) {

@@ -108,7 +108,7 @@ def split_images(*blocks):
 
 def umma_operator_images(ref, ru, cfg):
     """All reference operators of the tcgen05 fused stage (csrc/wadg_fused_umma.cuh,
-    CfgU offsets): volume chunks {D_a; Vq}, {DTW_a, -Pq}; per face and 16-point
+    CfgU offsets): per volume chunk D_a, Vq, DTW_a, -Pq; per face and 16-point
     half {Vf, Vfi, -Pf}; update chunks Vu, Pu."""
     NP, NQ = ref.Np, ref.Nq
     QC, NCH, NPK, NPN, NFPK, NFH = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"], cfg["nfq8"]
@@ -125,12 +125,14 @@ def umma_operator_images(ref, ru, cfg):
         return out
 
     parts = []
-    for ch in range(NCH):                   # V1: rows a*16 + qq -> D_a, 48 + qq -> Vq
-        parts.append(split_images(np.vstack([rows(D, ch * QC, QC, NPK) for D in ref.Dq]
-                                            + [rows(ref.Vq, ch * QC, QC, NPK)])))
-    for ch in range(NCH):                   # V2: blocks (NPN rows j) x (QC columns q)
-        blocks = [rows(M.T, ch * QC, QC, NPN).T for M in DTW + [-ref.Pq]]
-        parts.append(split_images(*blocks))
+    for ch in range(NCH):                   # D_a: rows a*16 + qq
+        parts.append(split_images(np.vstack([rows(D, ch * QC, QC, NPK) for D in ref.Dq])))
+    for ch in range(NCH):                   # Vq: rows qq
+        parts.append(split_images(rows(ref.Vq, ch * QC, QC, NPK)))
+    for ch in range(NCH):                   # DTW_a: 3 blocks of (NPN rows j) x (QC columns q)
+        parts.append(split_images(*[rows(M.T, ch * QC, QC, NPN).T for M in DTW]))
+    for ch in range(NCH):                   # -Pq: (NPN rows j) x (QC columns q)
+        parts.append(split_images(rows(-ref.Pq.T, ch * QC, QC, NPN).T))
     for f in range(nf):
         for hh in range(NFH):
             Vf = rows(ref.Vfq[f * nfq:(f + 1) * nfq], hh * 16, 16, NPK)

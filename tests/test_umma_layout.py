@@ -32,16 +32,17 @@ def test_operator_image_size(N):
     ref = refelem.build_reference_element(N, refelem.ElementShape.Tetrahedron)
     rup = lambda a, b: -(-a // b) * b
     NP, NQ = ref.Np, ref.Nq
-    NPK, NPN, NFPK = rup(NP, 8), rup(NP, 16), rup(ref.nfp, 8)
+    NPK, NFPK = rup(NP, 8), rup(ref.nfp, 8)
+    NPN = NPK
     NFH, NCH, NCHU = -(-ref.nfq // 16), -(-NQ // 16), -(-NQ // 32)
     cfg = dict(qc=16, nch=NCH, npp=NPK, qcs=NPN, njs=NFPK, nfq8=NFH)
     img = device.umma_operator_images(ref, ref, cfg)
-    expect = (NCH * 2 * 64 * NPK + NCH * 2 * 4 * NPN * 16
+    expect = (NCH * 2 * 48 * NPK + NCH * 2 * 16 * NPK + NCH * 2 * 3 * NPN * 16 + NCH * 2 * NPN * 16
               + 4 * NFH * (2 * 16 * NPK + 2 * 16 * NFPK + 2 * NPN * 16) + NCHU * (2 * 32 * NPK + 2 * NPN * 32))
     assert img.size == expect and img.dtype == np.float32
     # first tile: D_r rows (quadrature points 0..15), hi + lo reproduce fp32(D_r)
-    half = 64 * NPK
-    t = (img[:half] + img[half:2 * half]).reshape(8, NPK // 4, 8, 4).transpose(0, 2, 1, 3).reshape(64, NPK)
+    half = 48 * NPK
+    t = (img[:half] + img[half:2 * half]).reshape(6, NPK // 4, 8, 4).transpose(0, 2, 1, 3).reshape(48, NPK)
     assert np.array_equal(t[:16, :NP], ref.Dq[0][:16].astype(np.float32))
 
 
