@@ -26,7 +26,7 @@
 //           epilogue: gp_i = sum_a G_ai dp_a, F_a = sum_i G_ai U_i       -> TMEM (hi, lo)
 //           V2: R_p += sum_a DTW_a F_a, R_u_i += (-Pq) gp_i              -> TMEM R
 //   surface per face, per 16-point half of the face rule:
-//           own traces Vf Q, exterior traces Vfi (gathered neighbour face nodes)
+//           own / exterior traces Vfi (own face nodes, gathered neighbour face nodes)
 //           epilogue: upwind/penalty flux * sJ/2 (* n_i)                 -> TMEM (hi, lo)
 //           lift: R_c += (-Pf) g_c
 //   update  per field pair: R_c -> shared (hi, lo); per 32-point chunk
@@ -71,13 +71,13 @@ struct CfgU {
     static constexpr int OPPF = 2 * NPN * 16;               // rows j, K = face points
     static constexpr int OPU1 = 2 * QU * NPK;
     static constexpr int OPU2 = 2 * NPN * QU;
-    static constexpr int OPS_FACE = OPVF + OPVFI + OPPF;
+    static constexpr int OPS_FACE = OPVFI + OPPF;
     // offsets (floats) of the packed operator buffer
     static constexpr size_t O_DA = 0;
     static constexpr size_t O_VQ = O_DA + (size_t)NCH * OPDA;
     static constexpr size_t O_DTW = O_VQ + (size_t)NCH * OPVQ;
     static constexpr size_t O_PQ = O_DTW + (size_t)NCH * OPDTW;
-    static constexpr size_t O_FACE = O_PQ + (size_t)NCH * OPPQ;        // [f][half]{Vf, Vfi, Pf}
+    static constexpr size_t O_FACE = O_PQ + (size_t)NCH * OPPQ;        // [f][half]{Vfi, Pf}
     static constexpr size_t O_U1 = O_FACE + (size_t)NF * NFH * OPS_FACE;
     static constexpr size_t O_U2 = O_U1 + (size_t)NCHU * OPU1;
     static constexpr size_t OP_TOTAL = O_U2 + (size_t)NCHU * OPU2;
@@ -93,7 +93,7 @@ struct CfgU {
     static constexpr size_t SMEM = MISC + 2 * SQF * 4 + S_OPS;
     // TMEM columns
     static constexpr uint32_t RACC = 0, SCR = 4 * NPN;
-    static_assert(SCR + 288 <= 512, "TMEM budget");
+    static_assert(SCR + 320 <= 512, "TMEM budget");
     // op-tile barrier slots (bar[1 + slot]) in the volume phase; the surface and update
     // phases use slots 0 and 1
     static constexpr int SL_DA = 0, SL_VQ = 2, SL_PQ = 4, SL_DTW = 5;
@@ -448,7 +448,10 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     // ======================= surface ======================================
     float *sExtHi = sOp;                                       // [c][K-major 128 x NFPK]
     auto sFace = [&](int b) { return sOp + C::S_EXT / 4 + b * C::OPS_FACE; };
-    const uint32_t OWN = SCR, EXT = SCR + 64, EXTLO = SCR + 128;
+    // TMEM: traces at the 16 face points of a half (own, exterior; the flux
+    // overwrites them as the lift A operand), exterior node lo parts, own
+    // face-node hi / lo parts (the exterior hi parts are in shared memory)
+    const uint32_t OWN = SCR, EXT = SCR + 64, EXTLO = SCR + 128, OWNH = SCR + 192, OWNL = SCR + 256;
     const int NFQT = NF * NFQ;
     // neighbour face nodes of face f for this thread's field c = sub
     float xn[NFP];
@@ -517,6 +520,23 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             }
             st8(tl + EXTLO + 16 * c, l0);
             st8(tl + EXTLO + 16 * c + 8, l1);
+            // own face nodes (from sQ through the face mask) -> TMEM hi / lo
+            float oh[16], ol[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float x = i < NFP ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4] : 0.f;
+                oh[i] = tf32_hi(x);
+                ol[i] = x - oh[i];
+            }
+            float t0[8], t1[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { t0[i] = oh[i]; t1[i] = oh[8 + i]; }
+            st8(tl + OWNH + 16 * c, t0);
+            st8(tl + OWNH + 16 * c + 8, t1);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) { t0[i] = ol[i]; t1[i] = ol[8 + i]; }
+            st8(tl + OWNL + 16 * c, t0);
+            st8(tl + OWNL + 16 * c + 8, t1);
         }
         wait_st();
         if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
@@ -532,19 +552,18 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 if (lane == 0 && step + 1 < NF * NFH)
                     op_load(buf ^ 1, sFace(buf ^ 1), ops + C::O_FACE + (size_t)(step + 1) * C::OPS_FACE,
                             C::OPS_FACE * 4);
-                const uint32_t vfh = su32(fo), vfl = vfh + C::OPVF * 2;
-                const uint32_t vih = vfh + C::OPVF * 4, vil = vih + C::OPVFI * 2;
+                const uint32_t vih = su32(fo), vil = vih + C::OPVFI * 2;
                 const uint32_t aE = su32(sExtHi);
                 const uint32_t id = idesc_tf32(128, 16);
 #pragma unroll 1
-                for (int ks = 0; ks < NPK / 8; ++ks) {    // own traces, 4 field accumulators
+                for (int ks = 0; ks < NFPK / 8; ++ks) {   // own traces from own face nodes (TMEM)
                     const uint32_t o = ks * 256;
 #pragma unroll
                     for (int t = 0; t < 3; ++t)
 #pragma unroll
                         for (int c = 0; c < 4; ++c)
-                            mma_ss_w(tm + OWN + 16 * c, desc_k((t == 0 ? aQlo : aQ) + c * FQB + o, 128, SBO_Q),
-                                     desc_k((t == 1 ? vfl : vfh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
+                            mma_ts_w(tm + OWN + 16 * c, tm + (t == 0 ? OWNL : OWNH) + 16 * c + 8 * ks,
+                                     desc_k((t == 1 ? vil : vih) + o, 128, SBO_FP), id, (ks > 0 || t > 0) ? 1u : 0u);
                 }
 #pragma unroll 1
                 for (int ks = 0; ks < NFPK / 8; ++ks) {   // exterior traces (A_lo in TMEM)
@@ -595,7 +614,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             __syncthreads();
             if (issuer) {
                 fence_after();
-                const uint32_t pfh = su32(fo) + (C::OPVF + C::OPVFI) * 4, pfl = pfh + C::OPPF * 2;
+                const uint32_t pfh = su32(fo) + C::OPVFI * 4, pfl = pfh + C::OPPF * 2;
                 const uint32_t id = idesc_tf32(128, NPN);
 #pragma unroll 1
                 for (int ks = 0; ks < 2; ++ks)

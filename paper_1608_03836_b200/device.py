@@ -109,7 +109,7 @@ def split_images(*blocks):
 def umma_operator_images(ref, ru, cfg):
     """All reference operators of the tcgen05 fused stage (csrc/wadg_fused_umma.cuh,
     CfgU offsets): per volume chunk D_a, Vq, DTW_a, -Pq; per face and 16-point
-    half {Vf, Vfi, -Pf}; update chunks Vu, Pu."""
+    half {Vfi, -Pf}; update chunks Vu, Pu."""
     NP, NQ = ref.Np, ref.Nq
     QC, NCH, NPK, NPN, NFPK, NFH = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"], cfg["nfq8"]
     QU = 32
@@ -135,10 +135,8 @@ def umma_operator_images(ref, ru, cfg):
         parts.append(split_images(rows(-ref.Pq.T, ch * QC, QC, NPN).T))
     for f in range(nf):
         for hh in range(NFH):
-            Vf = rows(ref.Vfq[f * nfq:(f + 1) * nfq], hh * 16, 16, NPK)
             Vfi = rows(ref.face_interp, hh * 16, 16, NFPK)
             Pf = rows((-ref.Pfq[:, f * nfq:(f + 1) * nfq]).T, hh * 16, 16, NPN).T
-            parts.append(split_images(Vf))
             parts.append(split_images(Vfi))
             parts.append(split_images(Pf))
     for u in range(NCHU):
