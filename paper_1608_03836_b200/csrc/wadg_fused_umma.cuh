@@ -453,28 +453,28 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     // face-node hi / lo parts (the exterior hi parts are in shared memory)
     const uint32_t OWN = SCR, EXT = SCR + 64, EXTLO = SCR + 128, OWNH = SCR + 192, OWNL = SCR + 256;
     const int NFQT = NF * NFQ;
-    // neighbour face nodes of face f for this thread's field c = sub
-    float xn[NFP];
+    // neighbour face nodes of face f for this thread's field c = sub, staged
+    // by cp.async into [c][i][128] of the (now free) sQlo region, so the
+    // gather needs no registers while the previous face is processed
+    float *sStage = sQlo;
     auto gather = [&](int f) {
         // select without dynamic indexing (keeps the tables in registers)
         const int nb = f == 0 ? nbr[0] : f == 1 ? nbr[1] : f == 2 ? nbr[2] : nbr[3];
         const int code = f == 0 ? ncode[0] : f == 1 ? ncode[1] : f == 2 ? ncode[2] : ncode[3];
-        {
-            const int c = sub;
+        const int c = sub;
+        float *dst = sStage + (size_t)c * NFP * ME + e;
 #pragma unroll
-            for (int i = 0; i < NFP; ++i) {
-                float v;
-                if (nb >= 0) {
-                    v = __ldg(Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
-                } else if (nb == -1) {   // mirror BC (solver.py:214-217): p+ = -p-, u+ = u-
-                    const float m = sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4];
-                    v = c == 0 ? -m : m;
-                } else {
-                    v = P.halo[((size_t)(-nb - 2) * 4 + c) * NFP + sPerm[(code % P.nor) * NFP + i]];
-                }
-                xn[i] = v;
+        for (int i = 0; i < NFP; ++i) {
+            if (nb >= 0) {
+                fused::cp_async_elem(dst + i * ME, Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
+            } else if (nb == -1) {   // mirror BC (solver.py:214-217): p+ = -p-, u+ = u-
+                const float m = sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4];
+                dst[i * ME] = c == 0 ? -m : m;
+            } else {
+                fused::cp_async_elem(dst + i * ME, P.halo + ((size_t)(-nb - 2) * 4 + c) * NFP + sPerm[(code % P.nor) * NFP + i]);
             }
         }
+        fused::cp_async_commit();
     };
     // face factors n_0, n_1, n_2, sJ/2 of this thread's 8 points of a (face, half) step
     float fg[4][4];
@@ -494,9 +494,12 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     UMMA_MARK0(2);
     if (issuer && lane == 0) op_load(0, sFace(0), ops + C::O_FACE, C::OPS_FACE * 4);
     for (int f = 0; f < NF; ++f) {
+        UMMA_MARK(8, f == 1 && tid == 511);
         // exterior nodes -> shared (hi) and TMEM (lo), zero K padding
+        fused::cp_async_wait<0>();      // this thread's staged neighbour nodes of face f
         {
             const int c = sub;
+            const float *xs = sStage + (size_t)c * NFP * ME + e;
             float lo[16];
 #pragma unroll
             for (int i0 = 0; i0 < NFPK; i0 += 4) {
@@ -504,7 +507,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 float *pv = reinterpret_cast<float *>(&v);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const float x = (i0 + i < NFP) ? xn[i0 + i] : 0.f;
+                    const float x = (i0 + i < NFP) ? xs[(i0 + i) * ME] : 0.f;
                     pv[i] = tf32_hi(x);
                     lo[i0 + i] = x - pv[i];
                 }
@@ -539,8 +542,10 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             st8(tl + OWNL + 16 * c + 8, t1);
         }
         wait_st();
+        UMMA_MARK(9, f == 1 && tid == 511);
         if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
         sync_to_mma();
+        UMMA_MARK(10, f == 1 && tid == 511);
         for (int hh = 0; hh < NFH; ++hh) {
             const int step = f * NFH + hh;
             const int buf = step & 1;
@@ -582,7 +587,9 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 }
                 commit_w(&bar[0]);
             }
+            UMMA_MARK(11, step == 2 && tid == 511);
             mma_wait();
+            UMMA_MARK(12, step == 2 && tid == 511);
             {
                 float mM[4][4], mP[4][4];
 #pragma unroll
@@ -610,8 +617,10 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 for (int c = 0; c < 4; ++c) st_split4(tl + OWN + 16 * c + 4 * sub, tl + EXT + 16 * c + 4 * sub, g[c]);
                 wait_st();
             }
+            UMMA_MARK(13, step == 2 && tid == 511);
             fence_before();
             __syncthreads();
+            UMMA_MARK(14, step == 2 && tid == 511);
             if (issuer) {
                 fence_after();
                 const uint32_t pfh = su32(fo) + C::OPVFI * 4, pfl = pfh + C::OPPF * 2;
@@ -627,6 +636,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 commit_w(&bar[0]);
             }
             mma_wait();
+            UMMA_MARK(15, step == 2 && tid == 511);
         }
     }
 
@@ -706,7 +716,9 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 }
                 commit_w(&bar[0]);
             }
+            UMMA_MARK(16, ustep == 1 && tid == 511);
             mma_wait();
+            UMMA_MARK(17, ustep == 1 && tid == 511);
             {   // omega z for this thread's field (lf = sub & 1) and 16 of the 32 points
                 const int lf = sub & 1, pb = 16 * (sub >> 1);
                 float wz[16];
@@ -725,6 +737,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 }
                 wait_st();
             }
+            UMMA_MARK(18, ustep == 1 && tid == 511);
             fence_before();
             __syncthreads();
             if (issuer) {
@@ -742,6 +755,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 commit_w(&bar[0]);
             }
             mma_wait();
+            UMMA_MARK(19, ustep == 1 && tid == 511);
         }
     }
 

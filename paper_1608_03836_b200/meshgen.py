@@ -208,7 +208,11 @@ def warp_cube(x, y, z, amp=0.1):
 
 def warped_cube_tet_mesh(n, N_geo, amp=0.1, nz=None, z_range=None, domain=(-1.0, 1.0)):
     """n x n x nz cubes on [-1,1]^2 x z_range, 6 Kuhn tets each, element
-    order z-major (kz, ky, kx, tet) so z-slabs are contiguous ranges.
+    order (kz, tet, ky, kx): z-major so z-slabs are contiguous ranges, and
+    within a z-layer grouped by Kuhn tet type, so that consecutive elements
+    (one warp of a kernel) are the same tet type in consecutive cubes and
+    their neighbours across any local face are consecutive elements with one
+    common face code: neighbour-trace gathers are coalesced.
 
     Default nz = n and z_range = domain (the cube of configs 2-4).  For the
     weak-scaling config 5 pass nz = 48*G and z_range = (-1, -1 + 2*nz/n) ...
@@ -223,7 +227,7 @@ def warped_cube_tet_mesh(n, N_geo, amp=0.1, nz=None, z_range=None, domain=(-1.0,
     kz, ky, kx = np.meshgrid(np.arange(nz), np.arange(n), np.arange(n), indexing="ij")
     base = np.stack([kx.ravel(), ky.ravel(), kz.ravel()], axis=1)   # (C, 3) z-major
     corners = base[:, None, None, :] + local[None]                  # (C, 6, 4, 3)
-    corners = corners.reshape(-1, 4, 3)
+    corners = corners.reshape(nz, n * n, 6, 4, 3).transpose(0, 2, 1, 3, 4).reshape(-1, 4, 3)
     vid = (corners[..., 2] * (n + 1) + corners[..., 1]) * (n + 1) + corners[..., 0]
     xyz = np.stack([gx[corners[..., 0]], gx[corners[..., 1]], gz[corners[..., 2]]], axis=-1)
     X = _simplex_map_nodes(ElementShape.Tetrahedron, N_geo, xyz)

@@ -30,7 +30,8 @@ t = buf.view(nblk, 32).cpu().numpy().astype(np.float64)
 def med(a, b):
     return float(np.median(t[:, b] - t[:, a]))
 out = {"phases": {nm: med(i, i + 1) for i, nm in enumerate(["stageQ", "volume", "surface", "update", "write"])},
-       "chunk3_issuer": {"wait_mma": med(8, 9), "tmem_ld": med(9, 10), "epilogue": med(10, 11), "sync": med(11, 12),
-                         "op_wait_v2": med(12, 13), "issue_v2": med(13, 14), "opwait+issue_v1+commit": med(14, 15)},
-       "chunk3_t511": {"wait_mma": med(16, 17), "tmem_ld": med(17, 18), "epilogue": med(18, 19), "sync": med(19, 20)}}
+       "surface_face1_t511": {"store_nodes": med(8, 9), "gather_issue+sync": med(9, 10)},
+       "surface_step2_t511": {"wait_traces": med(11, 12), "flux_epilogue": med(12, 13), "sync": med(13, 14),
+                              "lift+wait": med(14, 15)},
+       "update_step1_t511": {"wait_U1": med(16, 17), "epilogue": med(17, 18), "sync+U2+wait": med(18, 19)}}
 print(json.dumps(out, indent=1))
