@@ -60,7 +60,7 @@ struct CfgU {
     static constexpr int NFPK = rup(NFP, 8);
     static constexpr int NFQ = (N + 1) * (N + 1);
     static constexpr int NFH = cdiv(NFQ, 16);               // 16-point halves of a face rule
-    static constexpr int NF = 4, FLD = 4, ME = 128, NTH = 512;
+    static constexpr int NF = 4, FLD = 4, ME = 128, NTH = 544;   // 16 epilogue warps + 1 MMA warp
     static_assert(NFPK <= 16, "exterior-trace K extent must fit 16 TMEM columns per field");
     // operator tile images (floats, hi image then lo image)
     // volume tiles per quadrature chunk: D_a (rows a*16 + q), Vq (rows q), DTW_a (3 blocks of
@@ -163,24 +163,47 @@ __device__ __forceinline__ void st_split4(uint32_t t_hi, uint32_t t_lo, const fl
     umma::st4(t_lo, lo);
 }
 
+// named barriers between the epilogue warps (arrive) and the MMA warp (sync)
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nb_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+// wait for the k-th completion (1-based) of an mbarrier; valid while at most
+// one earlier completion can still be outstanding
+__device__ __forceinline__ void wait_k(uint64_t *bar, uint32_t k) { umma::mbar_wait_bounded(bar, (k - 1u) & 1u); }
+
+// Warp roles: warps 0..15 are the epilogue warps (element e = 32 (w % 4) + lane,
+// sub-group w / 4 owns 4 of the 16 points of a chunk / face half, or field
+// w / 4); warp 16 is the MMA warp: it issues every tcgen05.mma and TMA copy and
+// never blocks the epilogue warps, which hand over through named barriers
+// (bar.arrive) and take results back through tcgen05.commit mbarriers.
 template <int N>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(CfgU<N>::NTH, 1)
 k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *__restrict__ Qout,
              float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt, int block0) {
     using C = CfgU<N>;
     using namespace umma;
     constexpr int NP = C::NP, NPK = C::NPK, NPN = C::NPN, NQ = C::NQ, QC = C::QC, QU = C::QU;
     constexpr int NFP = C::NFP, NFPK = C::NFPK, NFQ = C::NFQ, NFH = C::NFH, NF = 4, ME = 128;
+    constexpr int NCH = C::NCH, NCHU = C::NCHU, NSTEP = NF * NFH;
     constexpr uint32_t SBO_Q = (NPK / 4) * 128;        // 8-row group stride of NPK-wide tiles
     constexpr uint32_t SBO_16 = 4 * 128;                // ... of 16-wide tiles
     constexpr uint32_t SBO_32 = 8 * 128;                // ... of 32-wide tiles
     constexpr uint32_t SBO_FP = (NFPK / 4) * 128;
     constexpr uint32_t RACC = C::RACC, SCR = C::SCR;
     constexpr uint32_t FQB = ME * NPK * 4;              // bytes of one field in sQ / sQlo
+    constexpr int NB = C::NTH;                          // named-barrier thread count
+    enum { B_P = 1, B_U = 2, B_S0 = 3, B_S1 = 4, B_R = 5, B_Z = 6 };
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);            // [0] MMA, [1..6] operator tiles, [7] MMA (u chain)
+    // mbarriers: [0] MMA group A (volume p chain, face traces, update U1), [7] MMA
+    // group B (volume u chain, lifts, update U2), [1..6] operator tiles,
+    // v2[0..1] volume V2p / V2u done (operator refills, MMA warp only)
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem);
     uint32_t *tslot = reinterpret_cast<uint32_t *>(smem + 64);
+    uint64_t *bar_v2 = reinterpret_cast<uint64_t *>(smem + 80);
     int32_t *sExt = reinterpret_cast<int32_t *>(smem + 128);       // [f2 * nor + o][i]
     int32_t *sFmask = sExt + NF * 6 * NFP;                         // [f][i]
     int32_t *sPerm = sFmask + NF * NFP;                            // [o][i]
@@ -189,19 +212,21 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     float *sOp = sQlo + C::SQF;
     const float *ops = P.opVA;                                     // packed tile images (CfgU offsets)
 
-    // warp index through a shuffle: provably warp-uniform, so the issuer branch
-    // and its descriptor arithmetic stay on the uniform datapath
+    // warp index through a shuffle: provably warp-uniform, so the MMA warp's
+    // branch and descriptor arithmetic stay on the uniform datapath
     const int tid = threadIdx.x, lane = tid & 31, warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-    const int qd = warp & 3, sub = warp >> 2;                     // lane quarter, sub-group 0..3
+    const bool mma_warp = warp == 16;
+    const int qd = warp & 3, sub = (warp >> 2) & 3;                // lane quarter, sub-group 0..3
     const int e = 32 * qd + lane;                                  // element row = TMEM lane
-    const bool issuer = warp == 0;                                 // MMA / TMA issuing warp
     const size_t S = P.Kpad;
-    const size_t kblk = (size_t)(block0 + blockIdx.x) * ME;
-    uint32_t ph_mma = 0, ph_op = 0;                                // phase bits: MMA, operator slots
+    const size_t blk = (size_t)(block0 + blockIdx.x);
+    const size_t kblk = blk * ME;
     UMMA_MARK0(0);
 
     if (tid == 0) {
         for (int i = 0; i < 8; ++i) fused::mbar_init(&bar[i], 1);
+        fused::mbar_init(&bar_v2[0], 1);
+        fused::mbar_init(&bar_v2[1], 1);
     }
     if (warp == 0) tmem_alloc<512>(tslot);
     for (int r = tid; r < NF * 6 * NFP; r += C::NTH) sExt[r] = __ldg(P.ext_node + r);
@@ -209,14 +234,13 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     for (int r = tid; r < 6 * NFP; r += C::NTH) sPerm[r] = __ldg(P.fperm + r);
     // neighbour tables of all faces (consumed in the surface phase)
     int nbr[NF], ncode[NF];
+    if (!mma_warp) {
 #pragma unroll
-    for (int f = 0; f < NF; ++f) {
-        nbr[f] = __ldg(P.nbr + (size_t)f * S + kblk + e);
-        ncode[f] = __ldg(P.ncode + (size_t)f * S + kblk + e);
-    }
-
-    // ---- fields -> sQ (raw fp32, the tf32 hi operand) and sQlo ------------
-    {
+        for (int f = 0; f < NF; ++f) {
+            nbr[f] = __ldg(P.nbr + (size_t)f * S + kblk + e);
+            ncode[f] = __ldg(P.ncode + (size_t)f * S + kblk + e);
+        }
+        // ---- fields -> sQ (raw fp32, the tf32 hi operand) and sQlo --------
         const int c = sub;
 #pragma unroll
         for (int j0 = 0; j0 < NPK; j0 += 4) {
@@ -245,122 +269,109 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     const uint32_t aQ = su32(sQ), aQlo = su32(sQlo);
     UMMA_MARK0(1);
 
-    auto mma_wait = [&]() {
-        mbar_wait_bounded(&bar[0], ph_mma & 1u);
-        ph_mma ^= 1u;
-        fence_after();
-    };
-    auto mma_wait_u = [&]() {     // second MMA barrier (volume u chain)
-        mbar_wait_bounded(&bar[7], (ph_mma >> 1) & 1u);
-        ph_mma ^= 2u;
-        fence_after();
-    };
-    auto op_load = [&](int slot, float *dst, const float *src, uint32_t bytes) {   // one lane of the issuer
-        fused::mbar_expect_tx(&bar[1 + slot], bytes);
-        fused::bulk_g2s(dst, src, bytes, &bar[1 + slot]);
-    };
-    auto op_load2 = [&](int slot, float *d0, const float *s0, uint32_t b0, float *d1, const float *s1, uint32_t b1) {
-        fused::mbar_expect_tx(&bar[1 + slot], b0 + b1);
-        fused::bulk_g2s(d0, s0, b0, &bar[1 + slot]);
-        fused::bulk_g2s(d1, s1, b1, &bar[1 + slot]);
-    };
-    auto op_wait = [&](int slot) {   // the issuing warp
-        mbar_wait_bounded(&bar[1 + slot], (ph_op >> slot) & 1u);
-        ph_op ^= 1u << slot;
-    };
-    auto sync_to_mma = [&]() {   // all threads: make smem / TMEM writes visible to the MMA issuer
-        fused::fence_proxy_async();
-        fence_before();
-        __syncthreads();
-    };
-
-    // ======================= volume =======================================
-    // Two independent chains share the geometric factors of a chunk:
-    //   p chain: dp_a = D_a p -> gp_i = sum_a G_ai dp_a -> R_u_i += (-Pq) gp_i
-    //   u chain: U_i = Vq u_i -> F_a = sum_i G_ai U_i   -> R_p   += sum_a DTW_a F_a
-    // They alternate (own TMEM regions, own MMA barriers), so the tensor core
-    // runs one chain's MMAs while the threads do the other chain's epilogue.
-    // MMA issue order: K step, split term, accumulator region, so consecutive
-    // MMAs never accumulate into the same TMEM columns.
-    const uint32_t DPO = SCR, UO = SCR + 48, GPH = SCR + 96, GPL = SCR + 144, FH = SCR + 192, FL = SCR + 240;
+    // ---- shared-memory regions and TMEM columns per phase ------------------
+    // volume
     float *sDa = sOp;                                   // [2][OPDA]
     float *sVq = sDa + 2 * C::OPDA;                     // [2][OPVQ]
     float *sPq = sVq + 2 * C::OPVQ;                     // [OPPQ]
     float *sDTW = sPq + C::OPPQ;                        // [OPDTW]
-    auto issue_v1p = [&](int ch) {                      // dp_a = D_a p
-        const uint32_t bh = su32(sDa + (ch & 1) * C::OPDA), bl = bh + C::OPDA * 2, id = idesc_tf32(128, 48);
-#pragma unroll 1
-        for (int ks = 0; ks < NPK / 8; ++ks) {
-            const uint32_t o = ks * 256;
-#pragma unroll
-            for (int t = 0; t < 3; ++t)
-                mma_ss_w(tm + DPO, desc_k((t == 0 ? aQlo : aQ) + o, 128, SBO_Q), desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q),
-                         id, (ks > 0 || t > 0) ? 1u : 0u);
-        }
-    };
-    auto issue_v1u = [&](int ch) {                      // U_i = Vq u_i
-        const uint32_t bh = su32(sVq + (ch & 1) * C::OPVQ), bl = bh + C::OPVQ * 2, id = idesc_tf32(128, 16);
-#pragma unroll 1
-        for (int ks = 0; ks < NPK / 8; ++ks) {
-            const uint32_t o = ks * 256;
-#pragma unroll
-            for (int t = 0; t < 3; ++t)
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-                    mma_ss_w(tm + UO + 16 * i, desc_k((t == 0 ? aQlo : aQ) + (1 + i) * FQB + o, 128, SBO_Q),
-                             desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
-        }
-    };
-    auto issue_v2p = [&](int ch) {                      // R_u_i += (-Pq) gp_i
-        const uint32_t bh = su32(sPq), bl = bh + C::OPPQ * 2, id = idesc_tf32(128, NPN);
-#pragma unroll 1
-        for (int ks = 0; ks < QC / 8; ++ks) {
-#pragma unroll
-            for (int t = 0; t < 3; ++t)
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-                    mma_ts_w(tm + RACC + NPN * (1 + i), tm + (t == 0 ? GPL : GPH) + 16 * i + 8 * ks,
-                             desc_k((t == 1 ? bl : bh) + ks * 256, 128, SBO_16), id, (ch > 0 || ks > 0 || t > 0) ? 1u : 0u);
-        }
-    };
-    auto issue_v2u = [&](int ch) {                      // R_p += sum_a DTW_a F_a
-        constexpr uint32_t BLK = NPN * QC * 4;
-        const uint32_t bh = su32(sDTW), bl = bh + C::OPDTW * 2, id = idesc_tf32(128, NPN);
-#pragma unroll 1
-        for (int ks = 0; ks < QC / 8; ++ks) {
-#pragma unroll
-            for (int t = 0; t < 3; ++t)
-#pragma unroll
-                for (int a = 0; a < 3; ++a)
-                    mma_ts_w(tm + RACC, tm + (t == 0 ? FL : FH) + 16 * a + 8 * ks,
-                             desc_k((t == 1 ? bl : bh) + a * BLK + ks * 256, 128, SBO_16), id,
-                             (ch > 0 || ks > 0 || t > 0 || a > 0) ? 1u : 0u);
-        }
-    };
+    const uint32_t DPO = SCR, UO = SCR + 48, GPH = SCR + 96, GPL = SCR + 144, FH = SCR + 192, FL = SCR + 240;
+    // surface: exterior node hi parts, two {Vfi, -Pf} tile buffers; neighbour nodes
+    // staged in the free sQlo region; TMEM: traces at the 16 points of a face half
+    // (own, exterior; the flux overwrites them as the lift A operand), exterior node
+    // lo parts, own face-node hi / lo parts
+    float *sExtHi = sOp;
+    auto sFace = [&](int b) { return sOp + C::S_EXT / 4 + b * C::OPS_FACE; };
+    float *sStage = sQlo;
+    const uint32_t OWN = SCR, EXT = SCR + 64, EXTLO = SCR + 128, OWNH = SCR + 192, OWNL = SCR + 256;
+    // update: R_c hi / lo of a field pair in the sQlo region, two {Vu, Pu} tile buffers
+    float *sA = sQlo;
+    auto sU = [&](int b) { return sOp + b * (C::OPU1 + C::OPU2); };
+    const uint32_t ZC = SCR, UAH = SCR + 64, UAL = SCR + 128;
 
-    // geometric factors of this thread's 4 points of a chunk, prefetched one step ahead
-    float G[9][4];
-    const size_t blk = (size_t)(block0 + blockIdx.x);
-    constexpr int GQ4 = C::NCH * 4;                 // float4 rows per geometric factor (Nq padded to 16)
-    auto load_G = [&](int ch) {
-        const float4 *src = reinterpret_cast<const float4 *>(P.geo_il) + (blk * 9 * GQ4 + ch * 4 + sub) * ME + e;
-#pragma unroll
-        for (int r = 0; r < 9; ++r) {
-            const float4 v = __ldg(src + (size_t)r * GQ4 * ME);
-            G[r][0] = v.x; G[r][1] = v.y; G[r][2] = v.z; G[r][3] = v.w;
-        }
-    };
-    load_G(0);
-    if (issuer) {
-        if (lane == 0) {
-            op_load(C::SL_DA, sDa, ops + C::O_DA, C::OPDA * 4);
-            op_load(C::SL_VQ, sVq, ops + C::O_VQ, C::OPVQ * 4);
-            op_load(C::SL_PQ, sPq, ops + C::O_PQ, C::OPPQ * 4);
-            op_load(C::SL_DTW, sDTW, ops + C::O_DTW, C::OPDTW * 4);
-            if (C::NCH > 1) {
-                op_load(C::SL_DA + 1, sDa + C::OPDA, ops + C::O_DA + C::OPDA, C::OPDA * 4);
-                op_load(C::SL_VQ + 1, sVq + C::OPVQ, ops + C::O_VQ + C::OPVQ, C::OPVQ * 4);
+    if (mma_warp) {
+        // =================== MMA warp =====================================
+        uint32_t ph_op = 0, nv2p = 0, nv2u = 0, nB = 0;
+        auto op_load = [&](int slot, float *dst, const float *src, uint32_t bytes) {
+            if (lane == 0) {
+                fused::mbar_expect_tx(&bar[1 + slot], bytes);
+                fused::bulk_g2s(dst, src, bytes, &bar[1 + slot]);
             }
+        };
+        auto op_load2 = [&](int slot, float *d0, const float *s0, uint32_t b0, float *d1, const float *s1, uint32_t b1) {
+            if (lane == 0) {
+                fused::mbar_expect_tx(&bar[1 + slot], b0 + b1);
+                fused::bulk_g2s(d0, s0, b0, &bar[1 + slot]);
+                fused::bulk_g2s(d1, s1, b1, &bar[1 + slot]);
+            }
+        };
+        auto op_wait = [&](int slot) {
+            mbar_wait_bounded(&bar[1 + slot], (ph_op >> slot) & 1u);
+            ph_op ^= 1u << slot;
+        };
+        auto from_epilogue = [&](int id) {   // epilogue warps' TMEM / smem writes are visible
+            nb_sync(id, NB);
+            fence_after();
+        };
+        // ---- volume: p chain (dp -> gp -> R_u) and u chain (U -> F -> R_p) ----
+        auto issue_v1p = [&](int ch) {
+            const uint32_t bh = su32(sDa + (ch & 1) * C::OPDA), bl = bh + C::OPDA * 2, id = idesc_tf32(128, 48);
+#pragma unroll 1
+            for (int ks = 0; ks < NPK / 8; ++ks) {
+                const uint32_t o = ks * 256;
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+                    mma_ss_w(tm + DPO, desc_k((t == 0 ? aQlo : aQ) + o, 128, SBO_Q),
+                             desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
+            }
+        };
+        auto issue_v1u = [&](int ch) {
+            const uint32_t bh = su32(sVq + (ch & 1) * C::OPVQ), bl = bh + C::OPVQ * 2, id = idesc_tf32(128, 16);
+#pragma unroll 1
+            for (int ks = 0; ks < NPK / 8; ++ks) {
+                const uint32_t o = ks * 256;
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+                        mma_ss_w(tm + UO + 16 * i, desc_k((t == 0 ? aQlo : aQ) + (1 + i) * FQB + o, 128, SBO_Q),
+                                 desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
+            }
+        };
+        auto issue_v2p = [&](int ch) {   // R_u_i += (-Pq) gp_i
+            const uint32_t bh = su32(sPq), bl = bh + C::OPPQ * 2, id = idesc_tf32(128, NPN);
+#pragma unroll 1
+            for (int ks = 0; ks < QC / 8; ++ks) {
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+                        mma_ts_w(tm + RACC + NPN * (1 + i), tm + (t == 0 ? GPL : GPH) + 16 * i + 8 * ks,
+                                 desc_k((t == 1 ? bl : bh) + ks * 256, 128, SBO_16), id,
+                                 (ch > 0 || ks > 0 || t > 0) ? 1u : 0u);
+            }
+        };
+        auto issue_v2u = [&](int ch) {   // R_p += sum_a DTW_a F_a
+            constexpr uint32_t BLK = NPN * QC * 4;
+            const uint32_t bh = su32(sDTW), bl = bh + C::OPDTW * 2, id = idesc_tf32(128, NPN);
+#pragma unroll 1
+            for (int ks = 0; ks < QC / 8; ++ks) {
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                        mma_ts_w(tm + RACC, tm + (t == 0 ? FL : FH) + 16 * a + 8 * ks,
+                                 desc_k((t == 1 ? bl : bh) + a * BLK + ks * 256, 128, SBO_16), id,
+                                 (ch > 0 || ks > 0 || t > 0 || a > 0) ? 1u : 0u);
+            }
+        };
+        op_load(C::SL_DA, sDa, ops + C::O_DA, C::OPDA * 4);
+        op_load(C::SL_VQ, sVq, ops + C::O_VQ, C::OPVQ * 4);
+        op_load(C::SL_PQ, sPq, ops + C::O_PQ, C::OPPQ * 4);
+        op_load(C::SL_DTW, sDTW, ops + C::O_DTW, C::OPDTW * 4);
+        if (NCH > 1) {
+            op_load(C::SL_DA + 1, sDa + C::OPDA, ops + C::O_DA + C::OPDA, C::OPDA * 4);
+            op_load(C::SL_VQ + 1, sVq + C::OPVQ, ops + C::O_VQ + C::OPVQ, C::OPVQ * 4);
         }
         __syncwarp();
         op_wait(C::SL_DA);
@@ -369,228 +380,281 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         op_wait(C::SL_VQ);
         issue_v1u(0);
         commit_w(&bar[7]);
-    }
-    for (int ch = 0; ch < C::NCH; ++ch) {
-        const bool more = ch + 1 < C::NCH;
-        // ---- p chain
-        mma_wait();                     // V1p(ch), V2p(ch-1) complete
-        if (issuer && lane == 0 && ch > 0) {
-            op_load(C::SL_PQ, sPq, ops + C::O_PQ + (size_t)ch * C::OPPQ, C::OPPQ * 4);
-            if (more)
-                op_load(C::SL_DA + ((ch + 1) & 1), sDa + ((ch + 1) & 1) * C::OPDA, ops + C::O_DA + (size_t)(ch + 1) * C::OPDA,
-                        C::OPDA * 4);
-        }
-        {
-            float dp[3][4];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) ld4(tl + DPO + 16 * a + 4 * sub, dp[a]);
-            wait_ld();
-#pragma unroll
-            for (int m = 0; m < 3; ++m) {
-                float gp[4];
-#pragma unroll
-                for (int p = 0; p < 4; ++p)
-                    gp[p] = G[0 * 3 + m][p] * dp[0][p] + G[1 * 3 + m][p] * dp[1][p] + G[2 * 3 + m][p] * dp[2][p];
-                st_split4(tl + GPH + 16 * m + 4 * sub, tl + GPL + 16 * m + 4 * sub, gp);
-            }
-            wait_st();
-        }
-        sync_to_mma();
-        if (issuer) {
-            fence_after();
+        for (int ch = 0; ch < NCH; ++ch) {
+            const bool more = ch + 1 < NCH;
+            from_epilogue(B_P);              // gp(ch) in TMEM, dp(ch) consumed
             op_wait(C::SL_PQ);
             issue_v2p(ch);
+            commit_w(&bar_v2[0]);
             if (more) {
                 op_wait(C::SL_DA + ((ch + 1) & 1));
                 issue_v1p(ch + 1);
             }
             commit_w(&bar[0]);
-        }
-        // ---- u chain
-        mma_wait_u();                   // V1u(ch), V2u(ch-1) complete
-        if (issuer && lane == 0 && ch > 0) {
-            op_load(C::SL_DTW, sDTW, ops + C::O_DTW + (size_t)ch * C::OPDTW, C::OPDTW * 4);
-            if (more)
-                op_load(C::SL_VQ + ((ch + 1) & 1), sVq + ((ch + 1) & 1) * C::OPVQ, ops + C::O_VQ + (size_t)(ch + 1) * C::OPVQ,
-                        C::OPVQ * 4);
-        }
-        {
-            float U[3][4];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) ld4(tl + UO + 16 * i + 4 * sub, U[i]);
-            wait_ld();
-#pragma unroll
-            for (int m = 0; m < 3; ++m) {
-                float F[4];
-#pragma unroll
-                for (int p = 0; p < 4; ++p)
-                    F[p] = G[m * 3 + 0][p] * U[0][p] + G[m * 3 + 1][p] * U[1][p] + G[m * 3 + 2][p] * U[2][p];
-                st_split4(tl + FH + 16 * m + 4 * sub, tl + FL + 16 * m + 4 * sub, F);
-            }
-            if (more) load_G(ch + 1);
-            wait_st();
-        }
-        sync_to_mma();
-        if (issuer) {
-            fence_after();
+            from_epilogue(B_U);              // F(ch) in TMEM, U(ch) consumed
             op_wait(C::SL_DTW);
             issue_v2u(ch);
+            commit_w(&bar_v2[1]);
             if (more) {
                 op_wait(C::SL_VQ + ((ch + 1) & 1));
                 issue_v1u(ch + 1);
             }
             commit_w(&bar[7]);
+            // refills: the -Pq / D_a(ch) tiles are free once V2p(ch) (issued after V1p(ch))
+            // is done, the DTW / Vq(ch) tiles once V2u(ch) is
+            wait_k(&bar_v2[0], ++nv2p);
+            if (more) op_load(C::SL_PQ, sPq, ops + C::O_PQ + (size_t)(ch + 1) * C::OPPQ, C::OPPQ * 4);
+            if (ch + 2 < NCH)
+                op_load(C::SL_DA + (ch & 1), sDa + (ch & 1) * C::OPDA, ops + C::O_DA + (size_t)(ch + 2) * C::OPDA,
+                        C::OPDA * 4);
+            wait_k(&bar_v2[1], ++nv2u);
+            if (more) op_load(C::SL_DTW, sDTW, ops + C::O_DTW + (size_t)(ch + 1) * C::OPDTW, C::OPDTW * 4);
+            if (ch + 2 < NCH)
+                op_load(C::SL_VQ + (ch & 1), sVq + (ch & 1) * C::OPVQ, ops + C::O_VQ + (size_t)(ch + 2) * C::OPVQ,
+                        C::OPVQ * 4);
         }
-    }
-    mma_wait();                         // V2p of the last chunk
-    mma_wait_u();                       // V2u of the last chunk
-
-    // ======================= surface ======================================
-    float *sExtHi = sOp;                                       // [c][K-major 128 x NFPK]
-    auto sFace = [&](int b) { return sOp + C::S_EXT / 4 + b * C::OPS_FACE; };
-    // TMEM: traces at the 16 face points of a half (own, exterior; the flux
-    // overwrites them as the lift A operand), exterior node lo parts, own
-    // face-node hi / lo parts (the exterior hi parts are in shared memory)
-    const uint32_t OWN = SCR, EXT = SCR + 64, EXTLO = SCR + 128, OWNH = SCR + 192, OWNL = SCR + 256;
-    const int NFQT = NF * NFQ;
-    // neighbour face nodes of face f for this thread's field c = sub, staged
-    // by cp.async into [c][i][128] of the (now free) sQlo region, so the
-    // gather needs no registers while the previous face is processed
-    float *sStage = sQlo;
-    auto gather = [&](int f) {
-        // select without dynamic indexing (keeps the tables in registers)
-        const int nb = f == 0 ? nbr[0] : f == 1 ? nbr[1] : f == 2 ? nbr[2] : nbr[3];
-        const int code = f == 0 ? ncode[0] : f == 1 ? ncode[1] : f == 2 ? ncode[2] : ncode[3];
-        const int c = sub;
-        float *dst = sStage + (size_t)c * NFP * ME + e;
-#pragma unroll
-        for (int i = 0; i < NFP; ++i) {
-            if (nb >= 0) {
-                fused::cp_async_elem(dst + i * ME, Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
-            } else if (nb == -1) {   // mirror BC (solver.py:214-217): p+ = -p-, u+ = u-
-                const float m = sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4];
-                dst[i * ME] = c == 0 ? -m : m;
-            } else {
-                fused::cp_async_elem(dst + i * ME, P.halo + ((size_t)(-nb - 2) * 4 + c) * NFP + sPerm[(code % P.nor) * NFP + i]);
-            }
-        }
-        fused::cp_async_commit();
-    };
-    // face factors n_0, n_1, n_2, sJ/2 of this thread's 8 points of a (face, half) step
-    float fg[4][4];
-    constexpr int FQ4 = NFH * 4;                    // float4 rows per face (face rule padded to 16)
-    auto load_fg = [&](int step) {
-        const int f = step / NFH, hh = step % NFH;
-        const int fq4 = 4 * hh + sub;
-        const float4 *src = reinterpret_cast<const float4 *>(P.fgeo_il) + (blk * 4 * NF * FQ4 + f * FQ4 + fq4) * ME + e;
-#pragma unroll
-        for (int d = 0; d < 4; ++d) {
-            const float4 v = 4 * fq4 < NFQ ? __ldg(src + (size_t)d * NF * FQ4 * ME) : make_float4(0.f, 0.f, 0.f, 0.f);
-            fg[d][0] = v.x; fg[d][1] = v.y; fg[d][2] = v.z; fg[d][3] = v.w;
-        }
-    };
-    gather(0);
-    load_fg(0);
-    UMMA_MARK0(2);
-    if (issuer && lane == 0) op_load(0, sFace(0), ops + C::O_FACE, C::OPS_FACE * 4);
-    for (int f = 0; f < NF; ++f) {
-        UMMA_MARK(8, f == 1 && tid == 511);
-        // exterior nodes -> shared (hi) and TMEM (lo), zero K padding
-        fused::cp_async_wait<0>();      // this thread's staged neighbour nodes of face f
-        {
-            const int c = sub;
-            const float *xs = sStage + (size_t)c * NFP * ME + e;
-            float lo[16];
-#pragma unroll
-            for (int i0 = 0; i0 < NFPK; i0 += 4) {
-                float4 v;
-                float *pv = reinterpret_cast<float *>(&v);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float x = (i0 + i < NFP) ? xs[(i0 + i) * ME] : 0.f;
-                    pv[i] = tf32_hi(x);
-                    lo[i0 + i] = x - pv[i];
-                }
-                *reinterpret_cast<float4 *>(sExtHi + c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4) = v;
-            }
-#pragma unroll
-            for (int i = NFPK; i < 16; ++i) lo[i] = 0.f;
-            float l0[8], l1[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                l0[i] = lo[i];
-                l1[i] = lo[8 + i];
-            }
-            st8(tl + EXTLO + 16 * c, l0);
-            st8(tl + EXTLO + 16 * c + 8, l1);
-            // own face nodes (from sQ through the face mask) -> TMEM hi / lo
-            float oh[16], ol[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float x = i < NFP ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4] : 0.f;
-                oh[i] = tf32_hi(x);
-                ol[i] = x - oh[i];
-            }
-            float t0[8], t1[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) { t0[i] = oh[i]; t1[i] = oh[8 + i]; }
-            st8(tl + OWNH + 16 * c, t0);
-            st8(tl + OWNH + 16 * c + 8, t1);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) { t0[i] = ol[i]; t1[i] = ol[8 + i]; }
-            st8(tl + OWNL + 16 * c, t0);
-            st8(tl + OWNL + 16 * c + 8, t1);
-        }
-        wait_st();
-        UMMA_MARK(9, f == 1 && tid == 511);
-        if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
-        sync_to_mma();
-        UMMA_MARK(10, f == 1 && tid == 511);
-        for (int hh = 0; hh < NFH; ++hh) {
-            const int step = f * NFH + hh;
+        nB = NCH + 1;                        // group-B completions so far (V1u(0), per-chunk u commits)
+        // ---- surface: per (face, half) step traces (group A), lift (group B) ----
+        op_load(0, sFace(0), ops + C::O_FACE, C::OPS_FACE * 4);
+        for (int step = 0; step < NSTEP; ++step) {
             const int buf = step & 1;
-            const float *fo = sFace(buf);
-            if (issuer) {
-                fence_after();
+            const uint32_t fo = su32(sFace(buf));
+            if (step % NFH == 0) from_epilogue(B_S0);   // this face's own / exterior nodes written
+            else {
+                wait_k(&bar[7], nB);                     // previous lift done with the trace columns
+            }
+            if (step > 0 && step % NFH == 0) wait_k(&bar[7], nB);
+            op_wait(buf);
+            if (step + 1 < NSTEP) op_load(buf ^ 1, sFace(buf ^ 1), ops + C::O_FACE + (size_t)(step + 1) * C::OPS_FACE, C::OPS_FACE * 4);
+            const uint32_t vih = fo, vil = vih + C::OPVFI * 2;
+            const uint32_t aE = su32(sExtHi);
+            const uint32_t id = idesc_tf32(128, 16);
+#pragma unroll 1
+            for (int ks = 0; ks < NFPK / 8; ++ks) {
+                const uint32_t o = ks * 256;
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const uint64_t db = desc_k((t == 1 ? vil : vih) + o, 128, SBO_FP);
+                        const uint32_t acc = (ks > 0 || t > 0) ? 1u : 0u;
+                        mma_ts_w(tm + OWN + 16 * c, tm + (t == 0 ? OWNL : OWNH) + 16 * c + 8 * ks, db, id, acc);
+                        if (t == 0)
+                            mma_ts_w(tm + EXT + 16 * c, tm + EXTLO + 16 * c + 8 * ks, db, id, acc);
+                        else
+                            mma_ss_w(tm + EXT + 16 * c, desc_k(aE + c * ME * NFPK * 4 + o, 128, SBO_FP), db, id, acc);
+                    }
+            }
+            commit_w(&bar[0]);
+            from_epilogue(B_S1);             // flux (lift A operand) written over the traces
+            const uint32_t pfh = fo + C::OPVFI * 4, pfl = pfh + C::OPPF * 2;
+            const uint32_t idl = idesc_tf32(128, NPN);
+#pragma unroll 1
+            for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        mma_ts_w(tm + RACC + NPN * c, tm + (t == 0 ? EXT : OWN) + 16 * c + 8 * ks,
+                                 desc_k((t == 1 ? pfl : pfh) + ks * 256, 128, SBO_16), idl, 1u);
+            commit_w(&bar[7]);
+            ++nB;
+        }
+        // ---- update: per field pair, per 32-point chunk: U1 (group A), U2 (group B) ----
+        wait_k(&bar[7], nB);                 // last lift done: its tile buffer and columns are free
+        op_load2(0, sU(0), ops + C::O_U1, C::OPU1 * 4, sU(0) + C::OPU1, ops + C::O_U2, C::OPU2 * 4);
+        int ustep = 0;
+        for (int pr = 0; pr < 2; ++pr) {
+            from_epilogue(B_R);              // R of the pair in shared memory (hi, lo)
+            for (int u = 0; u < NCHU; ++u, ++ustep) {
+                const int buf = ustep & 1;
+                const uint32_t uo = su32(sU(buf));
+                if (ustep > 0) wait_k(&bar[7], nB);   // U2 of the previous chunk done: z / U2A / tiles free
                 op_wait(buf);
-                // next (face, half) operators into the other buffer (its last readers finished)
-                if (lane == 0 && step + 1 < NF * NFH)
-                    op_load(buf ^ 1, sFace(buf ^ 1), ops + C::O_FACE + (size_t)(step + 1) * C::OPS_FACE,
-                            C::OPS_FACE * 4);
-                const uint32_t vih = su32(fo), vil = vih + C::OPVFI * 2;
-                const uint32_t aE = su32(sExtHi);
-                const uint32_t id = idesc_tf32(128, 16);
-#pragma unroll 1
-                for (int ks = 0; ks < NFPK / 8; ++ks) {   // own traces from own face nodes (TMEM)
-                    const uint32_t o = ks * 256;
-#pragma unroll
-                    for (int t = 0; t < 3; ++t)
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            mma_ts_w(tm + OWN + 16 * c, tm + (t == 0 ? OWNL : OWNH) + 16 * c + 8 * ks,
-                                     desc_k((t == 1 ? vil : vih) + o, 128, SBO_FP), id, (ks > 0 || t > 0) ? 1u : 0u);
+                const int nx = ustep + 1;
+                if (nx < 2 * NCHU) {
+                    const int un = nx % NCHU;
+                    float *d = sU(nx & 1);
+                    op_load2(nx & 1, d, ops + C::O_U1 + (size_t)un * C::OPU1, C::OPU1 * 4, d + C::OPU1,
+                             ops + C::O_U2 + (size_t)un * C::OPU2, C::OPU2 * 4);
                 }
+                const uint32_t sA0 = su32(sA), id = idesc_tf32(128, QU);
 #pragma unroll 1
-                for (int ks = 0; ks < NFPK / 8; ++ks) {   // exterior traces (A_lo in TMEM)
+                for (int ks = 0; ks < NPK / 8; ++ks) {
                     const uint32_t o = ks * 256;
 #pragma unroll
                     for (int t = 0; t < 3; ++t)
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const uint64_t db = desc_k((t == 1 ? vil : vih) + o, 128, SBO_FP);
-                            const uint32_t acc = (ks > 0 || t > 0) ? 1u : 0u;
-                            if (t == 0)
-                                mma_ts_w(tm + EXT + 16 * c, tm + EXTLO + 16 * c + 8 * ks, db, id, acc);
-                            else
-                                mma_ss_w(tm + EXT + 16 * c, desc_k(aE + c * ME * NFPK * 4 + o, 128, SBO_FP), db, id, acc);
-                        }
+                        for (int lf = 0; lf < 2; ++lf)
+                            mma_ss_w(tm + ZC + 32 * lf, desc_k(sA0 + (t == 0 ? 2 + lf : lf) * FQB + o, 128, SBO_Q),
+                                     desc_k(uo + (t == 1 ? C::OPU1 * 2 : 0) + o, 128, SBO_Q), id,
+                                     (ks > 0 || t > 0) ? 1u : 0u);
                 }
                 commit_w(&bar[0]);
+                from_epilogue(B_Z);          // omega z (hi, lo) in TMEM
+                const uint32_t bh = uo + C::OPU1 * 4, bl = bh + C::OPU2 * 2, idu = idesc_tf32(128, NPN);
+#pragma unroll 1
+                for (int ks = 0; ks < QU / 8; ++ks)
+#pragma unroll
+                    for (int t = 0; t < 3; ++t)
+#pragma unroll
+                        for (int lf = 0; lf < 2; ++lf)
+                            mma_ts_w(tm + RACC + NPN * (2 * pr + lf), tm + (t == 0 ? UAL : UAH) + 32 * lf + 8 * ks,
+                                     desc_k((t == 1 ? bl : bh) + ks * 256, 128, SBO_32), idu,
+                                     (u > 0 || ks > 0 || t > 0) ? 1u : 0u);
+                commit_w(&bar[7]);
+                ++nB;
             }
-            UMMA_MARK(11, step == 2 && tid == 511);
-            mma_wait();
-            UMMA_MARK(12, step == 2 && tid == 511);
+        }
+    } else {
+        // =================== epilogue warps ===============================
+        uint32_t nA = 0, nB = 0;             // consumed completions of MMA groups A and B
+        auto wait_A = [&]() { wait_k(&bar[0], ++nA); fence_after(); };
+        auto wait_B = [&]() { wait_k(&bar[7], ++nB); fence_after(); };
+        auto to_mma = [&](int id) {           // hand TMEM / smem writes to the MMA warp
+            fused::fence_proxy_async();
+            fence_before();
+            nb_arrive(id, NB);
+        };
+        // ---- volume ----
+        float G[9][4];
+        constexpr int GQ4 = NCH * 4;                    // float4 rows per geometric factor (Nq padded to 16)
+        auto load_G = [&](int ch) {
+            const float4 *src = reinterpret_cast<const float4 *>(P.geo_il) + (blk * 9 * GQ4 + ch * 4 + sub) * ME + e;
+#pragma unroll
+            for (int r = 0; r < 9; ++r) {
+                const float4 v = __ldg(src + (size_t)r * GQ4 * ME);
+                G[r][0] = v.x; G[r][1] = v.y; G[r][2] = v.z; G[r][3] = v.w;
+            }
+        };
+        load_G(0);
+        for (int ch = 0; ch < NCH; ++ch) {
+            wait_A();                        // V1p(ch) and V2p(ch-1) done
             {
+                float dp[3][4];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) ld4(tl + DPO + 16 * a + 4 * sub, dp[a]);
+                wait_ld();
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    float gp[4];
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+                        gp[p] = G[0 * 3 + m][p] * dp[0][p] + G[1 * 3 + m][p] * dp[1][p] + G[2 * 3 + m][p] * dp[2][p];
+                    st_split4(tl + GPH + 16 * m + 4 * sub, tl + GPL + 16 * m + 4 * sub, gp);
+                }
+                wait_st();
+            }
+            to_mma(B_P);
+            wait_B();                        // V1u(ch) and V2u(ch-1) done
+            {
+                float U[3][4];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) ld4(tl + UO + 16 * i + 4 * sub, U[i]);
+                wait_ld();
+#pragma unroll
+                for (int m = 0; m < 3; ++m) {
+                    float F[4];
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+                        F[p] = G[m * 3 + 0][p] * U[0][p] + G[m * 3 + 1][p] * U[1][p] + G[m * 3 + 2][p] * U[2][p];
+                    st_split4(tl + FH + 16 * m + 4 * sub, tl + FL + 16 * m + 4 * sub, F);
+                }
+                if (ch + 1 < NCH) load_G(ch + 1);
+                wait_st();
+            }
+            to_mma(B_U);
+        }
+        wait_A();                            // V2p of the last chunk
+        wait_B();                            // V2u of the last chunk
+        UMMA_MARK0(2);
+        // ---- surface ----
+        auto gather = [&](int f) {   // neighbour face nodes of face f, field sub -> sStage [c][i][128]
+            const int nb = f == 0 ? nbr[0] : f == 1 ? nbr[1] : f == 2 ? nbr[2] : nbr[3];
+            const int code = f == 0 ? ncode[0] : f == 1 ? ncode[1] : f == 2 ? ncode[2] : ncode[3];
+            const int c = sub;
+            float *dst = sStage + (size_t)c * NFP * ME + e;
+#pragma unroll
+            for (int i = 0; i < NFP; ++i) {
+                if (nb >= 0) {
+                    fused::cp_async_elem(dst + i * ME, Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
+                } else if (nb == -1) {   // mirror BC (solver.py:214-217): p+ = -p-, u+ = u-
+                    const float m = sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4];
+                    dst[i * ME] = c == 0 ? -m : m;
+                } else {
+                    fused::cp_async_elem(dst + i * ME,
+                                         P.halo + ((size_t)(-nb - 2) * 4 + c) * NFP + sPerm[(code % P.nor) * NFP + i]);
+                }
+            }
+            fused::cp_async_commit();
+        };
+        float fg[4][4];
+        constexpr int FQ4 = NFH * 4;                    // float4 rows per face (face rule padded to 16)
+        auto load_fg = [&](int step) {
+            const int f = step / NFH, hh = step % NFH;
+            const int fq4 = 4 * hh + sub;
+            const float4 *src = reinterpret_cast<const float4 *>(P.fgeo_il) + (blk * 4 * NF * FQ4 + f * FQ4 + fq4) * ME + e;
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                const float4 v = 4 * fq4 < NFQ ? __ldg(src + (size_t)d * NF * FQ4 * ME) : make_float4(0.f, 0.f, 0.f, 0.f);
+                fg[d][0] = v.x; fg[d][1] = v.y; fg[d][2] = v.z; fg[d][3] = v.w;
+            }
+        };
+        gather(0);
+        load_fg(0);
+        for (int f = 0; f < NF; ++f) {
+            fused::cp_async_wait<0>();       // this thread's staged neighbour nodes of face f
+            {
+                const int c = sub;
+                const float *xs = sStage + (size_t)c * NFP * ME + e;
+                float lo[16];
+#pragma unroll
+                for (int i0 = 0; i0 < NFPK; i0 += 4) {
+                    float4 v;
+                    float *pv = reinterpret_cast<float *>(&v);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float x = (i0 + i < NFP) ? xs[(i0 + i) * ME] : 0.f;
+                        pv[i] = tf32_hi(x);
+                        lo[i0 + i] = x - pv[i];
+                    }
+                    *reinterpret_cast<float4 *>(sExtHi + c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4) = v;
+                }
+#pragma unroll
+                for (int i = NFPK; i < 16; ++i) lo[i] = 0.f;
+                float l0[8], l1[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    l0[i] = lo[i];
+                    l1[i] = lo[8 + i];
+                }
+                st8(tl + EXTLO + 16 * c, l0);
+                st8(tl + EXTLO + 16 * c + 8, l1);
+                // own face nodes (from sQ through the face mask) -> TMEM hi / lo
+                float oh[16], ol[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float x = i < NFP ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4] : 0.f;
+                    oh[i] = tf32_hi(x);
+                    ol[i] = x - oh[i];
+                }
+                float t0[8], t1[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { t0[i] = oh[i]; t1[i] = oh[8 + i]; }
+                st8(tl + OWNH + 16 * c, t0);
+                st8(tl + OWNH + 16 * c + 8, t1);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) { t0[i] = ol[i]; t1[i] = ol[8 + i]; }
+                st8(tl + OWNL + 16 * c, t0);
+                st8(tl + OWNL + 16 * c + 8, t1);
+            }
+            wait_st();
+            to_mma(B_S0);
+            if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
+            for (int hh = 0; hh < NFH; ++hh) {
+                const int step = f * NFH + hh;
+                wait_A();                    // traces of this step
+                if (step > 0) wait_B();      // lift of the previous step (issued before these traces)
                 float mM[4][4], mP[4][4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -612,120 +676,65 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     g[2][p] = fuu * (sJh * n1);
                     g[3][p] = fuu * (sJh * n2);
                 }
-                if (step + 1 < NF * NFH) load_fg(step + 1);
+                if (step + 1 < NSTEP) load_fg(step + 1);
 #pragma unroll
                 for (int c = 0; c < 4; ++c) st_split4(tl + OWN + 16 * c + 4 * sub, tl + EXT + 16 * c + 4 * sub, g[c]);
                 wait_st();
+                to_mma(B_S1);
             }
-            UMMA_MARK(13, step == 2 && tid == 511);
-            fence_before();
-            __syncthreads();
-            UMMA_MARK(14, step == 2 && tid == 511);
-            if (issuer) {
-                fence_after();
-                const uint32_t pfh = su32(fo) + C::OPVFI * 4, pfl = pfh + C::OPPF * 2;
-                const uint32_t id = idesc_tf32(128, NPN);
-#pragma unroll 1
-                for (int ks = 0; ks < 2; ++ks)
+        }
+        wait_B();                            // last lift: R complete
+        UMMA_MARK0(3);
+        // ---- update ----
+        float w[16];
+        constexpr int WQ4 = NCHU * 8;                   // float4 rows of the weights (Nq padded to 32)
+        auto load_w = [&](int pr, int u) {
+            const int c = 2 * pr + (sub & 1);
+            const float *base = (c > 0 || !P.wp) ? P.wu_il : P.wp_il;
+            const float sc = (c > 0 || P.wp) ? 1.f : P.c2;
+            const float4 *src = reinterpret_cast<const float4 *>(base) + (blk * WQ4 + u * 8 + 4 * (sub >> 1)) * ME + e;
 #pragma unroll
-                    for (int t = 0; t < 3; ++t)
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            mma_ts_w(tm + RACC + NPN * c, tm + (t == 0 ? EXT : OWN) + 16 * c + 8 * ks,
-                                     desc_k((t == 1 ? pfl : pfh) + ks * 256, 128, SBO_16), id, 1u);
-                commit_w(&bar[0]);
+            for (int k = 0; k < 4; ++k) {
+                const float4 v = __ldg(src + (size_t)k * ME);
+                w[4 * k + 0] = sc * v.x; w[4 * k + 1] = sc * v.y; w[4 * k + 2] = sc * v.z; w[4 * k + 3] = sc * v.w;
             }
-            mma_wait();
-            UMMA_MARK(15, step == 2 && tid == 511);
-        }
-    }
-
-    UMMA_MARK0(3);
-    // ======================= WADG update + LSRK ===========================
-    // the surface left no TMA in flight; sQlo now holds the update A operand
-    float *sA = sQlo;                                          // [hi f0, hi f1, lo f0, lo f1] x (128 x NPK)
-    auto sU = [&](int b) { return sOp + b * (C::OPU1 + C::OPU2); };
-    const uint32_t ZC = SCR, UAH = SCR + 64, UAL = SCR + 128;
-    // WADG weight of this thread's field (lf = sub & 1 of the pair) at its 16 of the
-    // 32 points of an update chunk
-    float w[16];
-    constexpr int WQ4 = C::NCHU * 8;                // float4 rows of the weights (Nq padded to 32)
-    auto load_w = [&](int pr, int u) {
-        const int c = 2 * pr + (sub & 1);
-        const float *base = (c > 0 || !P.wp) ? P.wu_il : P.wp_il;
-        const float sc = (c > 0 || P.wp) ? 1.f : P.c2;
-        const float4 *src = reinterpret_cast<const float4 *>(base) + (blk * WQ4 + u * 8 + 4 * (sub >> 1)) * ME + e;
+        };
+        load_w(0, 0);
+        int ustep = 0;
+        for (int pr = 0; pr < 2; ++pr) {
+            if (pr > 0) wait_B();            // U2 of the last chunk of pair 0 (U1 reads of sA are done too)
+            {   // R_c (c = 2 pr + lf) -> shared hi / lo, node groups of 8 split between sub >> 1
+                const int lf = sub & 1, c = 2 * pr + lf;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float4 v = __ldg(src + (size_t)k * ME);
-            w[4 * k + 0] = sc * v.x; w[4 * k + 1] = sc * v.y; w[4 * k + 2] = sc * v.z; w[4 * k + 3] = sc * v.w;
-        }
-    };
-    load_w(0, 0);
-    if (issuer && lane == 0)
-        op_load2(0, sU(0), ops + C::O_U1, C::OPU1 * 4, sU(0) + C::OPU1, ops + C::O_U2, C::OPU2 * 4);
-    int ustep = 0;
-    for (int pr = 0; pr < 2; ++pr) {
-        {   // R_c (c = 2 pr + lf) -> shared hi / lo, node groups of 8 split between sub >> 1
-            const int lf = sub & 1, c = 2 * pr + lf;
+                for (int j0 = 8 * (sub >> 1); j0 < NPK; j0 += 16) {
+                    float v[8];
+                    ld8(tl + RACC + NPN * c + j0, v);
+                    wait_ld();
 #pragma unroll
-            for (int j0 = 8 * (sub >> 1); j0 < NPK; j0 += 16) {
-                float v[8];
-                ld8(tl + RACC + NPN * c + j0, v);
-                wait_ld();
+                    for (int jj = 0; jj < 8; jj += 4) {
+                        float4 hv, lv;
+                        float *ph = reinterpret_cast<float *>(&hv), *pl = reinterpret_cast<float *>(&lv);
 #pragma unroll
-                for (int jj = 0; jj < 8; jj += 4) {
-                    float4 hv, lv;
-                    float *ph = reinterpret_cast<float *>(&hv), *pl = reinterpret_cast<float *>(&lv);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        ph[i] = tf32_hi(v[jj + i]);
-                        pl[i] = v[jj + i] - ph[i];
+                        for (int i = 0; i < 4; ++i) {
+                            ph[i] = tf32_hi(v[jj + i]);
+                            pl[i] = v[jj + i] - ph[i];
+                        }
+                        const uint32_t o = kmaj_off<NPK>(e, j0 + jj) / 4;
+                        *reinterpret_cast<float4 *>(sA + lf * ME * NPK + o) = hv;
+                        *reinterpret_cast<float4 *>(sA + (2 + lf) * ME * NPK + o) = lv;
                     }
-                    const uint32_t o = kmaj_off<NPK>(e, j0 + jj) / 4;
-                    *reinterpret_cast<float4 *>(sA + lf * ME * NPK + o) = hv;
-                    *reinterpret_cast<float4 *>(sA + (2 + lf) * ME * NPK + o) = lv;
                 }
             }
-        }
-        sync_to_mma();
-        for (int u = 0; u < C::NCHU; ++u, ++ustep) {
-            const int buf = ustep & 1;
-            const uint32_t uo = su32(sU(buf));
-            if (issuer) {
-                fence_after();
-                op_wait(buf);
-                const int nx = ustep + 1;   // prefetch the next chunk's tiles
-                if (lane == 0 && nx < 2 * C::NCHU) {
-                    const int un = nx % C::NCHU;
-                    float *d = sU(nx & 1);
-                    op_load2(nx & 1, d, ops + C::O_U1 + (size_t)un * C::OPU1, C::OPU1 * 4, d + C::OPU1,
-                             ops + C::O_U2 + (size_t)un * C::OPU2, C::OPU2 * 4);
-                }
-                const uint32_t sA0 = su32(sA), id = idesc_tf32(128, QU);
-#pragma unroll 1
-                for (int ks = 0; ks < NPK / 8; ++ks) {
-                    const uint32_t o = ks * 256;
-#pragma unroll
-                    for (int t = 0; t < 3; ++t)
-#pragma unroll
-                        for (int lf = 0; lf < 2; ++lf)
-                            mma_ss_w(tm + ZC + 32 * lf, desc_k(sA0 + (t == 0 ? 2 + lf : lf) * FQB + o, 128, SBO_Q),
-                                     desc_k(uo + (t == 1 ? C::OPU1 * 2 : 0) + o, 128, SBO_Q), id,
-                                     (ks > 0 || t > 0) ? 1u : 0u);
-                }
-                commit_w(&bar[0]);
-            }
-            UMMA_MARK(16, ustep == 1 && tid == 511);
-            mma_wait();
-            UMMA_MARK(17, ustep == 1 && tid == 511);
-            {   // omega z for this thread's field (lf = sub & 1) and 16 of the 32 points
+            to_mma(B_R);
+            for (int u = 0; u < NCHU; ++u, ++ustep) {
+                wait_A();                    // U1(u) done (and every MMA issued before it)
+                if (ustep > 0 && u > 0) wait_B();   // U2 of the previous chunk (issued before U1(u))
                 const int lf = sub & 1, pb = 16 * (sub >> 1);
                 float wz[16];
 #pragma unroll
                 for (int p = 0; p < 16; ++p) wz[p] = w[p];
                 const int nx = ustep + 1;
-                if (nx < 2 * C::NCHU) load_w(nx / C::NCHU, nx % C::NCHU);
+                if (nx < 2 * NCHU) load_w(nx / NCHU, nx % NCHU);
 #pragma unroll
                 for (int p0 = 0; p0 < 16; p0 += 8) {
                     float z[8];
@@ -736,46 +745,28 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     st_split8(tl + UAH + 32 * lf + pb + p0, tl + UAL + 32 * lf + pb + p0, z);
                 }
                 wait_st();
+                to_mma(B_Z);
             }
-            UMMA_MARK(18, ustep == 1 && tid == 511);
-            fence_before();
-            __syncthreads();
-            if (issuer) {
-                fence_after();
-                const uint32_t bh = uo + C::OPU1 * 4, bl = bh + C::OPU2 * 2, id = idesc_tf32(128, NPN);
-#pragma unroll 1
-                for (int ks = 0; ks < QU / 8; ++ks)
-#pragma unroll
-                    for (int t = 0; t < 3; ++t)
-#pragma unroll
-                        for (int lf = 0; lf < 2; ++lf)
-                            mma_ts_w(tm + RACC + NPN * (2 * pr + lf), tm + (t == 0 ? UAL : UAH) + 32 * lf + 8 * ks,
-                                     desc_k((t == 1 ? bl : bh) + ks * 256, 128, SBO_32), id,
-                                     (u > 0 || ks > 0 || t > 0) ? 1u : 0u);
-                commit_w(&bar[0]);
-            }
-            mma_wait();
-            UMMA_MARK(19, ustep == 1 && tid == 511);
         }
-    }
-
-    UMMA_MARK0(4);
-    // res = a res + dt Minv(rhs); Q_out = Q_in + b res   (field c = sub)
-    {
-        const int c = sub;
+        wait_B();                            // U2 of the last chunk
+        UMMA_MARK0(4);
+        // res = a res + dt Minv(rhs); Q_out = Q_in + b res   (field c = sub)
+        {
+            const int c = sub;
 #pragma unroll
-        for (int j0 = 0; j0 < NPK; j0 += 8) {
-            float v[8];
-            ld8(tl + RACC + NPN * c + j0, v);
-            wait_ld();
+            for (int j0 = 0; j0 < NPK; j0 += 8) {
+                float v[8];
+                ld8(tl + RACC + NPN * c + j0, v);
+                wait_ld();
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int j = j0 + i;
-                if (j < NP) {
-                    const size_t o = (size_t)(c * NP + j) * S + kblk + e;
-                    const float r = (a_rk == 0.f) ? dt * v[i] : a_rk * res[o] + dt * v[i];
-                    res[o] = r;
-                    Qout[o] = sQ[c * ME * NPK + kmaj_off<NPK>(e, j) / 4] + b_rk * r;
+                for (int i = 0; i < 8; ++i) {
+                    const int j = j0 + i;
+                    if (j < NP) {
+                        const size_t o = (size_t)(c * NP + j) * S + kblk + e;
+                        const float r = (a_rk == 0.f) ? dt * v[i] : a_rk * res[o] + dt * v[i];
+                        res[o] = r;
+                        Qout[o] = sQ[c * ME * NPK + kmaj_off<NPK>(e, j) / 4] + b_rk * r;
+                    }
                 }
             }
         }

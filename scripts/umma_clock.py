@@ -33,5 +33,10 @@ out = {"phases": {nm: med(i, i + 1) for i, nm in enumerate(["stageQ", "volume", 
        "surface_face1_t511": {"store_nodes": med(8, 9), "gather_issue+sync": med(9, 10)},
        "surface_step2_t511": {"wait_traces": med(11, 12), "flux_epilogue": med(12, 13), "sync": med(13, 14),
                               "lift+wait": med(14, 15)},
+       "volume_chunk3": {"t511_wait_p": med(20, 21), "t511_epi_p": med(21, 22), "t511_sync_p": med(22, 23),
+                         "t511_wait_u": med(23, 24), "t511_epi_u": med(24, 25), "t511_sync_u": med(25, 26),
+                         "issuer_p_opwait_to_commit": med(28, 29), "issuer_p_commit_to_u_opwait": med(29, 30),
+                         "issuer_u_opwait_to_commit": med(30, 31),
+                         "sync_p_to_issuer_p_opwait_done": med(23, 28)},
        "update_step1_t511": {"wait_U1": med(16, 17), "epilogue": med(17, 18), "sync+U2+wait": med(18, 19)}}
 print(json.dumps(out, indent=1))
