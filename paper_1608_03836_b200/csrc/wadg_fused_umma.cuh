@@ -55,7 +55,7 @@ struct CfgU {
     static constexpr int NPN = NPK;             // N extent over nodes (M = 128 accepts N % 8 == 0 on sm_100a)
     static constexpr int NQ = (N + 1) * (N + 1) * (N + 1);
     static constexpr int QC = 16, NCH = cdiv(NQ, QC);       // volume quadrature chunks
-    static constexpr int QU = 32, NCHU = cdiv(NQ, QU);      // update quadrature chunks
+    static constexpr int QU = 16, NCHU = cdiv(NQ, QU);      // update quadrature chunks
     static constexpr int NFP = fused::nfp_tri(N);
     static constexpr int NFPK = rup(NFP, 8);
     static constexpr int NFQ = (N + 1) * (N + 1);
@@ -93,7 +93,7 @@ struct CfgU {
     static constexpr size_t SMEM = MISC + 2 * SQF * 4 + S_OPS;
     // TMEM columns
     static constexpr uint32_t RACC = 0, SCR = 4 * NPN;
-    static_assert(SCR + 320 <= 512, "TMEM budget");
+    static_assert(SCR + 320 <= 512 && SCR + 192 + 4 * NPK <= 512, "TMEM budget");
     // op-tile barrier slots (bar[1 + slot]) in the volume phase; the surface and update
     // phases use slots 0 and 1
     static constexpr int SL_DA = 0, SL_VQ = 2, SL_PQ = 4, SL_DTW = 5;
@@ -195,7 +195,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     constexpr uint32_t RACC = C::RACC, SCR = C::SCR;
     constexpr uint32_t FQB = ME * NPK * 4;              // bytes of one field in sQ / sQlo
     constexpr int NB = C::NTH;                          // named-barrier thread count
-    enum { B_P = 1, B_U = 2, B_S0 = 3, B_S1 = 4, B_R = 5, B_Z = 6 };
+    enum { B_P = 1, B_U = 2, B_S0 = 3, B_S1 = 4, B_R = 5, B_Z0 = 6, B_Z1 = 7 };
 
     extern __shared__ __align__(1024) unsigned char smem[];
     // mbarriers: [0] MMA group A (volume p chain, face traces, update U1), [7] MMA
@@ -284,10 +284,13 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     auto sFace = [&](int b) { return sOp + C::S_EXT / 4 + b * C::OPS_FACE; };
     float *sStage = sQlo;
     const uint32_t OWN = SCR, EXT = SCR + 64, EXTLO = SCR + 128, OWNH = SCR + 192, OWNL = SCR + 256;
-    // update: R_c hi / lo of a field pair in the sQlo region, two {Vu, Pu} tile buffers
+    // update: two chains, one per field pair (0: p, u1; 1: u2, u3).  R of pair 0
+    // (hi, lo) in the sQlo region, R of pair 1 (hi, lo) in TMEM; per chain z and
+    // omega z (hi, lo) in TMEM; two {Vu, Pu} tile buffers
     float *sA = sQlo;
     auto sU = [&](int b) { return sOp + b * (C::OPU1 + C::OPU2); };
-    const uint32_t ZC = SCR, UAH = SCR + 64, UAL = SCR + 128;
+    const uint32_t Z0 = SCR, Z1 = SCR + 32, UA0H = SCR + 64, UA0L = SCR + 96, UA1H = SCR + 128, UA1L = SCR + 160;
+    const uint32_t RA1 = SCR + 192;                    // [hi f2, hi f3, lo f2, lo f3] x NPK
 
     if (mma_warp) {
         // =================== MMA warp =====================================
@@ -460,50 +463,69 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             commit_w(&bar[7]);
             ++nB;
         }
-        // ---- update: per field pair, per 32-point chunk: U1 (group A), U2 (group B) ----
+        // ---- update: chain 0 (pair 0, group A) and chain 1 (pair 1, group B), per
+        // 16-point chunk: U1 (z = Vu R_c), then U2 (R_c (+)= Pu omega z) ----
         wait_k(&bar[7], nB);                 // last lift done: its tile buffer and columns are free
         op_load2(0, sU(0), ops + C::O_U1, C::OPU1 * 4, sU(0) + C::OPU1, ops + C::O_U2, C::OPU2 * 4);
-        int ustep = 0;
-        for (int pr = 0; pr < 2; ++pr) {
-            from_epilogue(B_R);              // R of the pair in shared memory (hi, lo)
-            for (int u = 0; u < NCHU; ++u, ++ustep) {
-                const int buf = ustep & 1;
-                const uint32_t uo = su32(sU(buf));
-                if (ustep > 0) wait_k(&bar[7], nB);   // U2 of the previous chunk done: z / U2A / tiles free
-                op_wait(buf);
-                const int nx = ustep + 1;
-                if (nx < 2 * NCHU) {
-                    const int un = nx % NCHU;
-                    float *d = sU(nx & 1);
-                    op_load2(nx & 1, d, ops + C::O_U1 + (size_t)un * C::OPU1, C::OPU1 * 4, d + C::OPU1,
-                             ops + C::O_U2 + (size_t)un * C::OPU2, C::OPU2 * 4);
-                }
-                const uint32_t sA0 = su32(sA), id = idesc_tf32(128, QU);
+        if (NCHU > 1)
+            op_load2(1, sU(1), ops + C::O_U1 + C::OPU1, C::OPU1 * 4, sU(1) + C::OPU1, ops + C::O_U2 + C::OPU2,
+                     C::OPU2 * 4);
+        const uint32_t sA0 = su32(sA), idz = idesc_tf32(128, QU), idu = idesc_tf32(128, NPN);
+        auto issue_u1 = [&](int chain, int u) {
+            const uint32_t uo = su32(sU(u & 1));
 #pragma unroll 1
-                for (int ks = 0; ks < NPK / 8; ++ks) {
-                    const uint32_t o = ks * 256;
+            for (int ks = 0; ks < NPK / 8; ++ks) {
+                const uint32_t o = ks * 256;
 #pragma unroll
-                    for (int t = 0; t < 3; ++t)
+                for (int t = 0; t < 3; ++t)
 #pragma unroll
-                        for (int lf = 0; lf < 2; ++lf)
-                            mma_ss_w(tm + ZC + 32 * lf, desc_k(sA0 + (t == 0 ? 2 + lf : lf) * FQB + o, 128, SBO_Q),
-                                     desc_k(uo + (t == 1 ? C::OPU1 * 2 : 0) + o, 128, SBO_Q), id,
-                                     (ks > 0 || t > 0) ? 1u : 0u);
-                }
-                commit_w(&bar[0]);
-                from_epilogue(B_Z);          // omega z (hi, lo) in TMEM
-                const uint32_t bh = uo + C::OPU1 * 4, bl = bh + C::OPU2 * 2, idu = idesc_tf32(128, NPN);
+                    for (int lf = 0; lf < 2; ++lf) {
+                        const uint64_t db = desc_k(uo + (t == 1 ? C::OPU1 * 2 : 0) + o, 128, SBO_Q);
+                        const uint32_t acc = (ks > 0 || t > 0) ? 1u : 0u;
+                        if (chain == 0)
+                            mma_ss_w(tm + Z0 + 16 * lf, desc_k(sA0 + (t == 0 ? 2 + lf : lf) * FQB + o, 128, SBO_Q), db,
+                                     idz, acc);
+                        else
+                            mma_ts_w(tm + Z1 + 16 * lf, tm + RA1 + (t == 0 ? 2 * NPK : 0) + NPK * lf + 8 * ks, db, idz, acc);
+                    }
+            }
+        };
+        auto issue_u2 = [&](int chain, int u) {
+            const uint32_t bh = su32(sU(u & 1)) + C::OPU1 * 4, bl = bh + C::OPU2 * 2;
+            const uint32_t zh = chain ? UA1H : UA0H, zl = chain ? UA1L : UA0L;
 #pragma unroll 1
-                for (int ks = 0; ks < QU / 8; ++ks)
+            for (int ks = 0; ks < QU / 8; ++ks)
 #pragma unroll
-                    for (int t = 0; t < 3; ++t)
+                for (int t = 0; t < 3; ++t)
 #pragma unroll
-                        for (int lf = 0; lf < 2; ++lf)
-                            mma_ts_w(tm + RACC + NPN * (2 * pr + lf), tm + (t == 0 ? UAL : UAH) + 32 * lf + 8 * ks,
-                                     desc_k((t == 1 ? bl : bh) + ks * 256, 128, SBO_32), idu,
-                                     (u > 0 || ks > 0 || t > 0) ? 1u : 0u);
-                commit_w(&bar[7]);
-                ++nB;
+                    for (int lf = 0; lf < 2; ++lf)
+                        mma_ts_w(tm + RACC + NPN * (2 * chain + lf), tm + (t == 0 ? zl : zh) + 16 * lf + 8 * ks,
+                                 desc_k((t == 1 ? bl : bh) + ks * 256, 128, SBO_16), idu, (u > 0 || ks > 0 || t > 0) ? 1u : 0u);
+        };
+        from_epilogue(B_R);                  // R of both pairs in place (shared memory, TMEM)
+        op_wait(0);
+        issue_u1(0, 0);
+        commit_w(&bar[0]);
+        issue_u1(1, 0);
+        commit_w(&bar[7]);
+        for (int u = 0; u < NCHU; ++u) {
+            const bool more = u + 1 < NCHU;
+            from_epilogue(B_Z0);             // omega z of chain 0 in TMEM, z consumed
+            issue_u2(0, u);
+            if (more) {
+                op_wait((u + 1) & 1);
+                issue_u1(0, u + 1);
+            }
+            commit_w(&bar[0]);
+            from_epilogue(B_Z1);
+            issue_u2(1, u);
+            commit_w(&bar_v2[0]);            // last reader of the chunk-u tiles
+            if (more) issue_u1(1, u + 1);
+            commit_w(&bar[7]);
+            if (u + 2 < NCHU) {
+                wait_k(&bar_v2[0], ++nv2p);
+                op_load2(u & 1, sU(u & 1), ops + C::O_U1 + (size_t)(u + 2) * C::OPU1, C::OPU1 * 4,
+                         sU(u & 1) + C::OPU1, ops + C::O_U2 + (size_t)(u + 2) * C::OPU2, C::OPU2 * 4);
             }
         }
     } else {
@@ -686,68 +708,83 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         wait_B();                            // last lift: R complete
         UMMA_MARK0(3);
         // ---- update ----
-        float w[16];
-        constexpr int WQ4 = NCHU * 8;                   // float4 rows of the weights (Nq padded to 32)
-        auto load_w = [&](int pr, int u) {
-            const int c = 2 * pr + (sub & 1);
-            const float *base = (c > 0 || !P.wp) ? P.wu_il : P.wp_il;
-            const float sc = (c > 0 || P.wp) ? 1.f : P.c2;
-            const float4 *src = reinterpret_cast<const float4 *>(base) + (blk * WQ4 + u * 8 + 4 * (sub >> 1)) * ME + e;
+        // thread (e, sub): field lf = sub & 1 of each pair, points 8 (sub >> 1) .. +7 of a chunk
+        const int lf = sub & 1, pb = 8 * (sub >> 1);
+        float w0[8], w1[8];
+        constexpr int WQ4 = NCHU * QU / 4;              // float4 rows of the weights (Nq padded to QU)
+        auto load_w = [&](int u) {
+            const float *b0 = (lf > 0 || !P.wp) ? P.wu_il : P.wp_il;      // chain 0: field lf (p: c^2/J)
+            const float sc = (lf > 0 || P.wp) ? 1.f : P.c2;
+            const float4 *s0 = reinterpret_cast<const float4 *>(b0) + (blk * WQ4 + u * 4 + pb / 4) * ME + e;
+            const float4 *s1 = reinterpret_cast<const float4 *>(P.wu_il) + (blk * WQ4 + u * 4 + pb / 4) * ME + e;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float4 v = __ldg(src + (size_t)k * ME);
-                w[4 * k + 0] = sc * v.x; w[4 * k + 1] = sc * v.y; w[4 * k + 2] = sc * v.z; w[4 * k + 3] = sc * v.w;
+            for (int k = 0; k < 2; ++k) {
+                const float4 v = __ldg(s0 + (size_t)k * ME), x = __ldg(s1 + (size_t)k * ME);
+                w0[4 * k + 0] = sc * v.x; w0[4 * k + 1] = sc * v.y; w0[4 * k + 2] = sc * v.z; w0[4 * k + 3] = sc * v.w;
+                w1[4 * k + 0] = x.x; w1[4 * k + 1] = x.y; w1[4 * k + 2] = x.z; w1[4 * k + 3] = x.w;
             }
         };
-        load_w(0, 0);
-        int ustep = 0;
-        for (int pr = 0; pr < 2; ++pr) {
-            if (pr > 0) wait_B();            // U2 of the last chunk of pair 0 (U1 reads of sA are done too)
-            {   // R_c (c = 2 pr + lf) -> shared hi / lo, node groups of 8 split between sub >> 1
-                const int lf = sub & 1, c = 2 * pr + lf;
+        load_w(0);
+        {   // R -> A operands: pair 0 (fields lf) to shared memory, pair 1 (fields 2 + lf) to TMEM;
+            // node groups of 8 split between sub >> 1
 #pragma unroll
-                for (int j0 = 8 * (sub >> 1); j0 < NPK; j0 += 16) {
-                    float v[8];
-                    ld8(tl + RACC + NPN * c + j0, v);
-                    wait_ld();
+            for (int j0 = 8 * (sub >> 1); j0 < NPK; j0 += 16) {
+                float v[8], hi[8], lo[8];
+                ld8(tl + RACC + NPN * lf + j0, v);
+                wait_ld();
 #pragma unroll
-                    for (int jj = 0; jj < 8; jj += 4) {
-                        float4 hv, lv;
-                        float *ph = reinterpret_cast<float *>(&hv), *pl = reinterpret_cast<float *>(&lv);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            ph[i] = tf32_hi(v[jj + i]);
-                            pl[i] = v[jj + i] - ph[i];
-                        }
-                        const uint32_t o = kmaj_off<NPK>(e, j0 + jj) / 4;
-                        *reinterpret_cast<float4 *>(sA + lf * ME * NPK + o) = hv;
-                        *reinterpret_cast<float4 *>(sA + (2 + lf) * ME * NPK + o) = lv;
-                    }
+                for (int i = 0; i < 8; ++i) {
+                    hi[i] = tf32_hi(v[i]);
+                    lo[i] = v[i] - hi[i];
                 }
-            }
-            to_mma(B_R);
-            for (int u = 0; u < NCHU; ++u, ++ustep) {
-                wait_A();                    // U1(u) done (and every MMA issued before it)
-                if (ustep > 0 && u > 0) wait_B();   // U2 of the previous chunk (issued before U1(u))
-                const int lf = sub & 1, pb = 16 * (sub >> 1);
-                float wz[16];
 #pragma unroll
-                for (int p = 0; p < 16; ++p) wz[p] = w[p];
-                const int nx = ustep + 1;
-                if (nx < 2 * NCHU) load_w(nx / NCHU, nx % NCHU);
-#pragma unroll
-                for (int p0 = 0; p0 < 16; p0 += 8) {
-                    float z[8];
-                    ld8(tl + ZC + 32 * lf + pb + p0, z);
-                    wait_ld();
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) z[i] *= wz[p0 + i];
-                    st_split8(tl + UAH + 32 * lf + pb + p0, tl + UAL + 32 * lf + pb + p0, z);
+                for (int jj = 0; jj < 8; jj += 4) {
+                    const uint32_t o = kmaj_off<NPK>(e, j0 + jj) / 4;
+                    *reinterpret_cast<float4 *>(sA + lf * ME * NPK + o) = make_float4(hi[jj], hi[jj + 1], hi[jj + 2], hi[jj + 3]);
+                    *reinterpret_cast<float4 *>(sA + (2 + lf) * ME * NPK + o) = make_float4(lo[jj], lo[jj + 1], lo[jj + 2], lo[jj + 3]);
                 }
-                wait_st();
-                to_mma(B_Z);
+                ld8(tl + RACC + NPN * (2 + lf) + j0, v);
+                wait_ld();
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    hi[i] = tf32_hi(v[i]);
+                    lo[i] = v[i] - hi[i];
+                }
+                st8(tl + RA1 + NPK * lf + j0, hi);
+                st8(tl + RA1 + 2 * NPK + NPK * lf + j0, lo);
             }
+            wait_st();
         }
+        to_mma(B_R);
+        for (int u = 0; u < NCHU; ++u) {
+            float wa[8], wb[8];
+#pragma unroll
+            for (int p = 0; p < 8; ++p) { wa[p] = w0[p]; wb[p] = w1[p]; }
+            if (u + 1 < NCHU) load_w(u + 1);
+            wait_A();                        // chain 0: U1(u) done (and U2(u-1))
+            {
+                float z[8];
+                ld8(tl + Z0 + 16 * lf + pb, z);
+                wait_ld();
+#pragma unroll
+                for (int i = 0; i < 8; ++i) z[i] *= wa[i];
+                st_split8(tl + UA0H + 16 * lf + pb, tl + UA0L + 16 * lf + pb, z);
+                wait_st();
+            }
+            to_mma(B_Z0);
+            wait_B();                        // chain 1: U1(u) done (and U2(u-1))
+            {
+                float z[8];
+                ld8(tl + Z1 + 16 * lf + pb, z);
+                wait_ld();
+#pragma unroll
+                for (int i = 0; i < 8; ++i) z[i] *= wb[i];
+                st_split8(tl + UA1H + 16 * lf + pb, tl + UA1L + 16 * lf + pb, z);
+                wait_st();
+            }
+            to_mma(B_Z1);
+        }
+        wait_A();                            // U2 of the last chunk, chain 0
         wait_B();                            // U2 of the last chunk
         UMMA_MARK0(4);
         // res = a res + dt Minv(rhs); Q_out = Q_in + b res   (field c = sub)

@@ -112,7 +112,7 @@ def umma_operator_images(ref, ru, cfg):
     half {Vfi, -Pf}; update chunks Vu, Pu."""
     NP, NQ = ref.Np, ref.Nq
     QC, NCH, NPK, NPN, NFPK, NFH = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"], cfg["nfq8"]
-    QU = 32
+    QU = 16
     NCHU = -(-NQ // QU)
     nf, nfq, nfp = ref.n_faces, ref.nfq, ref.nfp
     DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
@@ -273,13 +273,13 @@ class DeviceProblem:
             for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
                 setattr(self.struct, name, self.ops["umma"].data_ptr())
             # block-interleaved per-element data (include/wadg_b200.h, *_il)
-            nch, nchu, nfh = cfg["nch"], -(-ru.Nq // 32), cfg["nfq8"]
+            nch, nchu, nfh = cfg["nch"], -(-ru.Nq // 16), cfg["nfq8"]
             self.geo_il = interleave_blocks(self.geo, nch * 16, kb)
             fg = self.fgeo.view(self.dim + 1, ref.n_faces, ref.nfq, self.Kpad)
             self.fgeo_il = interleave_blocks(fg.reshape((self.dim + 1) * ref.n_faces, ref.nfq, self.Kpad),
                                              nfh * 16, kb)
-            self.wu_il = interleave_blocks(self.wu.unsqueeze(0), nchu * 32, kb)
-            self.wp_il = interleave_blocks(self.wp.unsqueeze(0), nchu * 32, kb) if self.wp is not None else None
+            self.wu_il = interleave_blocks(self.wu.unsqueeze(0), nchu * 16, kb)
+            self.wp_il = interleave_blocks(self.wp.unsqueeze(0), nchu * 16, kb) if self.wp is not None else None
             s = self.struct
             s.geo_il, s.fgeo_il, s.wu_il = self.geo_il.data_ptr(), self.fgeo_il.data_ptr(), self.wu_il.data_ptr()
             s.wp_il = self.wp_il.data_ptr() if self.wp_il is not None else None
