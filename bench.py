@@ -387,7 +387,8 @@ def main():
     achieved = B[top] / (avg[top] * 1e-3) / 1e9
     # measured DRAM traffic per launch from the committed ncu --set full capture
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", f"r01_ncu_stage_fused_{'f32' if cfg.dtype == 'float32' else 'f64'}"
+    kname = {2: "umma", 1: "fused_tc"}.get(getattr(d, "fused_kind", 0), "fused")
+    tpath = os.path.join(ROOT, "profiles", f"r01_ncu_stage_{kname}_{'f32' if cfg.dtype == 'float32' else 'f64'}"
                          f"_N{N}_{args.config}.json")
     if fused and world == 1 and os.path.exists(tpath):
         with open(tpath) as f:
