@@ -127,8 +127,8 @@ def umma_operator_images(ref, ru, cfg):
     parts = []
     for ch in range(NCH):                   # D_a: rows a*16 + qq
         parts.append(split_images(np.vstack([rows(D, ch * QC, QC, NPK) for D in ref.Dq])))
-    for ch in range(NCH):                   # Vq: rows qq
-        parts.append(split_images(rows(ref.Vq, ch * QC, QC, NPK)))
+    for pr in range(-(-NCH // 2)):          # Vq: rows qq of a chunk pair (2 QC quadrature points)
+        parts.append(split_images(rows(ref.Vq, pr * 2 * QC, 2 * QC, NPK)))
     for ch in range(NCH):                   # DTW_a: 3 blocks of (NPN rows j) x (QC columns q)
         parts.append(split_images(*[rows(M.T, ch * QC, QC, NPN).T for M in DTW]))
     for ch in range(NCH):                   # -Pq: (NPN rows j) x (QC columns q)

@@ -37,7 +37,7 @@ def test_operator_image_size(N):
     NFH, NCH, NCHU = -(-ref.nfq // 16), -(-NQ // 16), -(-NQ // 16)
     cfg = dict(qc=16, nch=NCH, npp=NPK, qcs=NPN, njs=NFPK, nfq8=NFH)
     img = device.umma_operator_images(ref, ref, cfg)
-    expect = (NCH * 2 * 48 * NPK + NCH * 2 * 16 * NPK + NCH * 2 * 3 * NPN * 16 + NCH * 2 * NPN * 16
+    expect = (NCH * 2 * 48 * NPK + (-(-NCH // 2)) * 2 * 32 * NPK + NCH * 2 * 3 * NPN * 16 + NCH * 2 * NPN * 16
               + 4 * NFH * (2 * 16 * NFPK + 2 * NPN * 16) + NCHU * (2 * 16 * NPK + 2 * NPN * 16))
     assert img.size == expect and img.dtype == np.float32
     # first tile: D_r rows (quadrature points 0..15), hi + lo reproduce fp32(D_r)
