@@ -79,8 +79,9 @@ struct CfgU {
     static constexpr size_t O_VQ = O_DA + (size_t)NCH * OPDA;
     static constexpr size_t O_DTW = O_VQ + (size_t)NPAIR * OPVQ;
     static constexpr size_t O_PQ = O_DTW + (size_t)NCH * OPDTW;
-    static constexpr size_t O_FACE = O_PQ + (size_t)NCH * OPPQ;        // [f][half]{Vfi, Pf}
-    static constexpr size_t O_U1 = O_FACE + (size_t)NF * NFH * OPS_FACE;
+    static constexpr size_t O_VFI = O_PQ + (size_t)NCH * OPPQ;         // [half] Vfi
+    static constexpr size_t O_PF = O_VFI + (size_t)NFH * OPVFI;         // [f][half] -Pf
+    static constexpr size_t O_U1 = O_PF + (size_t)NF * NFH * OPPF;
     static constexpr size_t O_U2 = O_U1 + (size_t)NCHU * OPU1;
     static constexpr size_t OP_TOTAL = O_U2 + (size_t)NCHU * OPU2;
     // shared memory (bytes)
@@ -88,14 +89,17 @@ struct CfgU {
     static_assert(128 + 4 * (NF * 6 * NFP + NF * NFP + 6 * NFP) <= MISC, "index tables exceed MISC");
     static constexpr size_t SQF = (size_t)FLD * ME * NPK;              // floats of one field set
     static constexpr size_t S_VOL = (size_t)(2 * OPDA + OPVQ + OPDTW + OPPQ) * 4;
-    static constexpr size_t S_EXT = (size_t)FLD * ME * NFPK * 4;
-    static constexpr size_t S_SURF = S_EXT + (size_t)2 * OPS_FACE * 4;
+    static constexpr size_t S_EXT = (size_t)FLD * ME * NFPK * 4;      // one K-major face-node operand
     static constexpr size_t S_UPD = (size_t)2 * (OPU1 + OPU2) * 4;
-    static constexpr size_t S_OPS = fused::maxz(S_VOL, fused::maxz(S_SURF, S_UPD));
-    static constexpr size_t SMEM = MISC + 2 * SQF * 4 + S_OPS;
+    static constexpr size_t S_OPS = fused::maxz(S_VOL, S_UPD);
+    // surface buffers (union with sQlo + ops): exterior hi, exterior lo, own lo,
+    // resident Vfi tiles, two -Pf tiles, neighbour-node staging
+    static constexpr size_t S_SURF = 3 * S_EXT + (size_t)(NFH * OPVFI + 2 * OPPF + FLD * NFP * ME) * 4;
+    static constexpr size_t S_UNION = fused::maxz(SQF * 4 + S_OPS, S_SURF);
+    static constexpr size_t SMEM = MISC + SQF * 4 + S_UNION;
     // TMEM columns
     static constexpr uint32_t RACC = 0, SCR = 4 * NPN;
-    static_assert(SCR + 336 <= 512 && SCR + 192 + 4 * NPK <= 512, "TMEM budget");
+    static_assert(SCR + 336 <= 512 && SCR + 192 + 4 * NPK <= 512 && SCR + 320 <= 512, "TMEM budget");
     // op-tile barrier slots (bar[1 + slot]) in the volume phase; the surface and update
     // phases use slots 0 and 1
     static constexpr int SL_DA = 0, SL_VQ = 2, SL_PQ = 4, SL_DTW = 5;
@@ -174,7 +178,9 @@ __device__ __forceinline__ void nb_sync(int id, int n) {
 }
 // wait for the k-th completion (1-based) of an mbarrier; valid while at most
 // one earlier completion can still be outstanding
-__device__ __forceinline__ void wait_k(uint64_t *bar, uint32_t k) { umma::mbar_wait_bounded(bar, (k - 1u) & 1u); }
+__device__ __forceinline__ void wait_k(uint64_t *bar, uint32_t k, int site = -1) {
+    umma::mbar_wait_bounded(bar, (k - 1u) & 1u, site);
+}
 
 // Warp roles: warps 0..15 are the epilogue warps (element e = 32 (w % 4) + lane,
 // sub-group w / 4 owns 4 of the 16 points of a chunk / face half, or field
@@ -197,7 +203,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     constexpr uint32_t RACC = C::RACC, SCR = C::SCR;
     constexpr uint32_t FQB = ME * NPK * 4;              // bytes of one field in sQ / sQlo
     constexpr int NB = C::NTH;                          // named-barrier thread count
-    enum { B_P = 1, B_U = 2, B_S0 = 3, B_S1 = 4, B_R = 5, B_Z0 = 6, B_Z1 = 7 };
+    enum { B_P = 1, B_U = 2, B_S0 = 3, B_S1 = 4, B_R = 5, B_Z0 = 6, B_Z1 = 7, B_S2 = 8 };
 
     extern __shared__ __align__(1024) unsigned char smem[];
     // mbarriers: [0] MMA group A (volume p chain, face traces, update U1), [7] MMA
@@ -279,14 +285,15 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     float *sDTW = sPq + C::OPPQ;                        // [OPDTW]
     // U of a chunk pair: field i at UO + 32 i, chunk ch at + 16 (ch & 1)
     const uint32_t DPO = SCR, UO = SCR + 48, GPH = SCR + 144, GPL = SCR + 192, FH = SCR + 240, FL = SCR + 288;
-    // surface: exterior node hi parts, two {Vfi, -Pf} tile buffers; neighbour nodes
-    // staged in the free sQlo region; TMEM: traces at the 16 points of a face half
-    // (own, exterior; the flux overwrites them as the lift A operand), exterior node
-    // lo parts, own face-node hi / lo parts
-    float *sExtHi = sOp;
-    auto sFace = [&](int b) { return sOp + C::S_EXT / 4 + b * C::OPS_FACE; };
-    float *sStage = sQlo;
-    const uint32_t OWN = SCR, EXT = SCR + 64, EXTLO = SCR + 128, OWNH = SCR + 192, OWNL = SCR + 256;
+    // surface (over the sQlo + ops union): exterior node hi / lo and own node lo
+    // parts (K-major operands), resident Vfi tiles, two -Pf tiles, neighbour-node
+    // staging; TMEM: traces at the 16 points of a face half (own, exterior), the
+    // flux g (hi, lo: the lift A operand), own face-node hi parts
+    float *sExtHi = sQlo, *sExtLo = sQlo + C::S_EXT / 4, *sOwnLo = sQlo + C::S_EXT / 2;
+    float *sVfi = sQlo + 3 * C::S_EXT / 4;
+    auto sPf = [&](int b) { return sVfi + NFH * C::OPVFI + b * C::OPPF; };
+    float *sStage = sVfi + NFH * C::OPVFI + 2 * C::OPPF;
+    const uint32_t OWN = SCR, EXT = SCR + 64, GH = SCR + 128, GL = SCR + 192, OWNH = SCR + 256;
     // update: two chains, one per field pair (0: p, u1; 1: u2, u3).  R of pair 0
     // (hi, lo) in the sQlo region, R of pair 1 (hi, lo) in TMEM; per chain z and
     // omega z (hi, lo) in TMEM; two {Vu, Pu} tile buffers
@@ -312,7 +319,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             }
         };
         auto op_wait = [&](int slot) {
-            mbar_wait_bounded(&bar[1 + slot], (ph_op >> slot) & 1u);
+            mbar_wait_bounded(&bar[1 + slot], (ph_op >> slot) & 1u, 3000 + slot);
             ph_op ^= 1u << slot;
         };
         auto from_epilogue = [&](int id) {   // epilogue warps' TMEM / smem writes are visible
@@ -416,20 +423,32 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 op_load(C::SL_VQ, sVq, ops + C::O_VQ + (size_t)(ch / 2 + 1) * C::OPVQ, C::OPVQ * 4);
         }
         nB = NCH + 1;                        // group-B completions so far (V1u(0), per-chunk u commits)
-        // ---- surface: per (face, half) step traces (group A), lift (group B) ----
-        op_load(0, sFace(0), ops + C::O_FACE, C::OPS_FACE * 4);
+        // ---- surface: per (face, half) step s: traces(s) (group A) are issued as
+        // soon as the epilogue has read traces(s-1) out of TMEM, the lift of s-1
+        // (group B) once its flux is written; the flux has its own columns ----
+        op_load(2, sVfi, ops + C::O_VFI, NFH * C::OPVFI * 4);   // resident for the whole surface
+        op_load(0, sPf(0), ops + C::O_PF, C::OPPF * 4);
+        if (NSTEP > 1) op_load(1, sPf(1), ops + C::O_PF + C::OPPF, C::OPPF * 4);
+        op_wait(2);
+        const uint32_t aEH = su32(sExtHi), aEL = su32(sExtLo), aOL = su32(sOwnLo);
+        auto issue_lift = [&](int st) {
+            op_wait(st & 1);
+            const uint32_t pfh = su32(sPf(st & 1)), pfl = pfh + C::OPPF * 2, idl = idesc_tf32(128, NPN);
+#pragma unroll 1
+            for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        mma_ts_w(tm + RACC + NPN * c, tm + (t == 0 ? GL : GH) + 16 * c + 8 * ks,
+                                 desc_k((t == 1 ? pfl : pfh) + ks * 256, 128, SBO_16), idl, 1u);
+            commit_w(&bar[7]);
+        };
         for (int step = 0; step < NSTEP; ++step) {
-            const int buf = step & 1;
-            const uint32_t fo = su32(sFace(buf));
-            if (step % NFH == 0) from_epilogue(B_S0);   // this face's own / exterior nodes written
-            else {
-                wait_k(&bar[7], nB);                     // previous lift done with the trace columns
-            }
-            if (step > 0 && step % NFH == 0) wait_k(&bar[7], nB);
-            op_wait(buf);
-            if (step + 1 < NSTEP) op_load(buf ^ 1, sFace(buf ^ 1), ops + C::O_FACE + (size_t)(step + 1) * C::OPS_FACE, C::OPS_FACE * 4);
-            const uint32_t vih = fo, vil = vih + C::OPVFI * 2;
-            const uint32_t aE = su32(sExtHi);
+            const int hh = step % NFH;
+            if (hh == 0) from_epilogue(B_S0);   // this face's own / exterior nodes written
+            if (step > 0) from_epilogue(B_S2);  // traces(step-1) read out of TMEM
+            const uint32_t vih = su32(sVfi + hh * C::OPVFI), vil = vih + C::OPVFI * 2;
             const uint32_t id = idesc_tf32(128, 16);
 #pragma unroll 1
             for (int ks = 0; ks < NFPK / 8; ++ks) {
@@ -440,31 +459,33 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     for (int c = 0; c < 4; ++c) {
                         const uint64_t db = desc_k((t == 1 ? vil : vih) + o, 128, SBO_FP);
                         const uint32_t acc = (ks > 0 || t > 0) ? 1u : 0u;
-                        mma_ts_w(tm + OWN + 16 * c, tm + (t == 0 ? OWNL : OWNH) + 16 * c + 8 * ks, db, id, acc);
+                        const uint32_t co = c * ME * NFPK * 4 + o;
                         if (t == 0)
-                            mma_ts_w(tm + EXT + 16 * c, tm + EXTLO + 16 * c + 8 * ks, db, id, acc);
+                            mma_ss_w(tm + OWN + 16 * c, desc_k(aOL + co, 128, SBO_FP), db, id, acc);
                         else
-                            mma_ss_w(tm + EXT + 16 * c, desc_k(aE + c * ME * NFPK * 4 + o, 128, SBO_FP), db, id, acc);
+                            mma_ts_w(tm + OWN + 16 * c, tm + OWNH + 16 * c + 8 * ks, db, id, acc);
+                        mma_ss_w(tm + EXT + 16 * c, desc_k((t == 0 ? aEL : aEH) + co, 128, SBO_FP), db, id, acc);
                     }
             }
             commit_w(&bar[0]);
-            from_epilogue(B_S1);             // flux (lift A operand) written over the traces
-            const uint32_t pfh = fo + C::OPVFI * 4, pfl = pfh + C::OPPF * 2;
-            const uint32_t idl = idesc_tf32(128, NPN);
-#pragma unroll 1
-            for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-                for (int t = 0; t < 3; ++t)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        mma_ts_w(tm + RACC + NPN * c, tm + (t == 0 ? EXT : OWN) + 16 * c + 8 * ks,
-                                 desc_k((t == 1 ? pfl : pfh) + ks * 256, 128, SBO_16), idl, 1u);
-            commit_w(&bar[7]);
-            ++nB;
+            if (step >= 2) {                 // lift(step-2) done: its -Pf buffer takes step
+                wait_k(&bar[7], ++nB, 4000 + step);
+                op_load(step & 1, sPf(step & 1), ops + C::O_PF + (size_t)step * C::OPPF, C::OPPF * 4);
+            }
+            if (step > 0) {
+                from_epilogue(B_S1);         // flux of step-1 written
+                issue_lift(step - 1);
+            }
         }
+        // An mbarrier parity wait is only unambiguous while at most one completion is
+        // outstanding, so lift(NSTEP-2) is waited for before the last lift is issued.
+        if (NSTEP >= 2) wait_k(&bar[7], ++nB, 4100);
+        from_epilogue(B_S2);
+        from_epilogue(B_S1);
+        issue_lift(NSTEP - 1);
+        wait_k(&bar[7], ++nB, 4101);         // all lifts done: R complete, tiles and columns free
         // ---- update: chain 0 (pair 0, group A) and chain 1 (pair 1, group B), per
         // 16-point chunk: U1 (z = Vu R_c), then U2 (R_c (+)= Pu omega z) ----
-        wait_k(&bar[7], nB);                 // last lift done: its tile buffer and columns are free
         op_load2(0, sU(0), ops + C::O_U1, C::OPU1 * 4, sU(0) + C::OPU1, ops + C::O_U2, C::OPU2 * 4);
         if (NCHU > 1)
             op_load2(1, sU(1), ops + C::O_U1 + C::OPU1, C::OPU1 * 4, sU(1) + C::OPU1, ops + C::O_U2 + C::OPU2,
@@ -628,46 +649,32 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             {
                 const int c = sub;
                 const float *xs = sStage + (size_t)c * NFP * ME + e;
-                float lo[16];
 #pragma unroll
                 for (int i0 = 0; i0 < NFPK; i0 += 4) {
-                    float4 v;
-                    float *pv = reinterpret_cast<float *>(&v);
+                    float4 vh, vl, oh4, ol4;
+                    float *ph = reinterpret_cast<float *>(&vh), *pl = reinterpret_cast<float *>(&vl);
+                    float *qh = reinterpret_cast<float *>(&oh4), *ql = reinterpret_cast<float *>(&ol4);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const float x = (i0 + i < NFP) ? xs[(i0 + i) * ME] : 0.f;
-                        pv[i] = tf32_hi(x);
-                        lo[i0 + i] = x - pv[i];
+                        const bool in = i0 + i < NFP;
+                        const float x = in ? xs[(i0 + i) * ME] : 0.f;
+                        const float y = in ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i0 + i]) / 4] : 0.f;
+                        ph[i] = tf32_hi(x);
+                        pl[i] = x - ph[i];
+                        qh[i] = tf32_hi(y);
+                        ql[i] = y - qh[i];
                     }
-                    *reinterpret_cast<float4 *>(sExtHi + c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4) = v;
+                    const uint32_t o = c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4;
+                    *reinterpret_cast<float4 *>(sExtHi + o) = vh;
+                    *reinterpret_cast<float4 *>(sExtLo + o) = vl;
+                    *reinterpret_cast<float4 *>(sOwnLo + o) = ol4;
+                    st4(tl + OWNH + 16 * c + i0, *reinterpret_cast<float (*)[4]>(qh));
                 }
 #pragma unroll
-                for (int i = NFPK; i < 16; ++i) lo[i] = 0.f;
-                float l0[8], l1[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    l0[i] = lo[i];
-                    l1[i] = lo[8 + i];
+                for (int i0 = NFPK; i0 < 16; i0 += 4) {
+                    const float z4[4] = {0.f, 0.f, 0.f, 0.f};
+                    st4(tl + OWNH + 16 * c + i0, z4);
                 }
-                st8(tl + EXTLO + 16 * c, l0);
-                st8(tl + EXTLO + 16 * c + 8, l1);
-                // own face nodes (from sQ through the face mask) -> TMEM hi / lo
-                float oh[16], ol[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float x = i < NFP ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4] : 0.f;
-                    oh[i] = tf32_hi(x);
-                    ol[i] = x - oh[i];
-                }
-                float t0[8], t1[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) { t0[i] = oh[i]; t1[i] = oh[8 + i]; }
-                st8(tl + OWNH + 16 * c, t0);
-                st8(tl + OWNH + 16 * c + 8, t1);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) { t0[i] = ol[i]; t1[i] = ol[8 + i]; }
-                st8(tl + OWNL + 16 * c, t0);
-                st8(tl + OWNL + 16 * c + 8, t1);
             }
             wait_st();
             to_mma(B_S0);
@@ -675,7 +682,6 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             for (int hh = 0; hh < NFH; ++hh) {
                 const int step = f * NFH + hh;
                 wait_A();                    // traces of this step
-                if (step > 0) wait_B();      // lift of the previous step (issued before these traces)
                 float mM[4][4], mP[4][4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -683,6 +689,8 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     ld4(tl + EXT + 16 * c + 4 * sub, mP[c]);
                 }
                 wait_ld();
+                fence_before();
+                nb_arrive(B_S2, NB);         // trace columns free for the next step's MMAs
                 float g[4][4];
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {
@@ -698,8 +706,9 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     g[3][p] = fuu * (sJh * n2);
                 }
                 if (step + 1 < NSTEP) load_fg(step + 1);
+                if (step > 0) wait_B();      // lift(step-1) done with the flux columns
 #pragma unroll
-                for (int c = 0; c < 4; ++c) st_split4(tl + OWN + 16 * c + 4 * sub, tl + EXT + 16 * c + 4 * sub, g[c]);
+                for (int c = 0; c < 4; ++c) st_split4(tl + GH + 16 * c + 4 * sub, tl + GL + 16 * c + 4 * sub, g[c]);
                 wait_st();
                 to_mma(B_S1);
             }

@@ -157,9 +157,15 @@ __device__ __forceinline__ void st8(uint32_t taddr, const float (&v)[8]) {
                  : "memory");
 }
 
-// mbarrier wait with a bound: a protocol bug traps (launch error) instead of
-// spinning forever
-__device__ __forceinline__ void mbar_wait_bounded(uint64_t *bar, uint32_t phase) {
+__device__ __noinline__ void wait_timeout(int site, uint32_t bar, uint32_t phase) {
+    printf("wadg: mbarrier wait timed out: cta %d thread %d site %d bar-offset %u parity %u\n", (int)blockIdx.x,
+           (int)threadIdx.x, site, bar, phase);
+    __trap();
+}
+
+// mbarrier wait with a bound: a protocol bug reports the wait site and traps
+// (launch error) instead of spinning forever
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t *bar, uint32_t phase, int site = -1) {
     uint32_t done = 0;
     for (uint32_t it = 0; it < (1u << 24) && !done; ++it) {
         asm volatile(

@@ -108,8 +108,8 @@ def split_images(*blocks):
 
 def umma_operator_images(ref, ru, cfg):
     """All reference operators of the tcgen05 fused stage (csrc/wadg_fused_umma.cuh,
-    CfgU offsets): per volume chunk D_a, Vq, DTW_a, -Pq; per face and 16-point
-    half {Vfi, -Pf}; update chunks Vu, Pu."""
+    CfgU offsets): per volume chunk D_a, DTW_a, -Pq and per chunk pair Vq; Vfi per
+    16-point half of the face rule; -Pf per face and half; update chunks Vu, Pu."""
     NP, NQ = ref.Np, ref.Nq
     QC, NCH, NPK, NPN, NFPK, NFH = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"], cfg["nfq8"]
     QU = 16
@@ -133,12 +133,11 @@ def umma_operator_images(ref, ru, cfg):
         parts.append(split_images(*[rows(M.T, ch * QC, QC, NPN).T for M in DTW]))
     for ch in range(NCH):                   # -Pq: (NPN rows j) x (QC columns q)
         parts.append(split_images(rows(-ref.Pq.T, ch * QC, QC, NPN).T))
-    for f in range(nf):
+    for hh in range(NFH):                   # Vfi per 16-point half of the face rule
+        parts.append(split_images(rows(ref.face_interp, hh * 16, 16, NFPK)))
+    for f in range(nf):                     # -Pf per face and half
         for hh in range(NFH):
-            Vfi = rows(ref.face_interp, hh * 16, 16, NFPK)
-            Pf = rows((-ref.Pfq[:, f * nfq:(f + 1) * nfq]).T, hh * 16, 16, NPN).T
-            parts.append(split_images(Vfi))
-            parts.append(split_images(Pf))
+            parts.append(split_images(rows((-ref.Pfq[:, f * nfq:(f + 1) * nfq]).T, hh * 16, 16, NPN).T))
     for u in range(NCHU):
         parts.append(split_images(rows(ru.Vq, u * QU, QU, NPK)))
     for u in range(NCHU):

@@ -38,7 +38,7 @@ def test_operator_image_size(N):
     cfg = dict(qc=16, nch=NCH, npp=NPK, qcs=NPN, njs=NFPK, nfq8=NFH)
     img = device.umma_operator_images(ref, ref, cfg)
     expect = (NCH * 2 * 48 * NPK + (-(-NCH // 2)) * 2 * 32 * NPK + NCH * 2 * 3 * NPN * 16 + NCH * 2 * NPN * 16
-              + 4 * NFH * (2 * 16 * NFPK + 2 * NPN * 16) + NCHU * (2 * 16 * NPK + 2 * NPN * 16))
+              + NFH * 2 * 16 * NFPK + 4 * NFH * 2 * NPN * 16 + NCHU * (2 * 16 * NPK + 2 * NPN * 16))
     assert img.size == expect and img.dtype == np.float32
     # first tile: D_r rows (quadrature points 0..15), hi + lo reproduce fp32(D_r)
     half = 48 * NPK
