@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define WADG_ABI_VERSION 4
+#define WADG_ABI_VERSION 5
 #define WADG_ELEMS_PER_BLOCK 32
 
 enum { WADG_F64 = 0, WADG_F32 = 1 };
@@ -101,6 +101,13 @@ typedef struct wadg_problem {
     const void *fgeo_il;
     const void *wu_il;
     const void *wp_il;    /* NULL when wp is NULL */
+    /* ExactCurvedMass comparator (R/.../solver.py:156-167, 302-306): when minv_p
+     * is not NULL, wadg_mass_inverse / wadg_update_lsrk / wadg_stage apply the
+     * stored dense per-element operators A_k = M_k^-1 Mhat (M_k the J/c^2- and
+     * J-weighted mass matrices at quadrature degree 2N + 2N_geo) instead of the
+     * matrix-free WADG inverse:  [Np][Np][Kpad] each, row j, column l.      */
+    const void *minv_p;
+    const void *minv_u;
 } wadg_problem;
 
 int wadg_abi_version(void);

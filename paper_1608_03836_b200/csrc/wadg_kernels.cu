@@ -639,6 +639,69 @@ static int upd_lsrk(const wadg_problem *P, const void *rhs, void *res, void *Q, 
     return launch_update<T, DIM, RJ, 1>(P, rhs, res, Q, a, b, dt, st);
 }
 
+// ---- ExactCurvedMass comparator -----------------------------------------------
+// One thread per element applies the stored dense operator A_k = M_k^-1 Mhat
+// (R/.../solver.py:302-306 with the Mhat product folded in at setup):
+//   mode 0: out = A rhs;   mode 1: res = a res + dt A rhs, Q += b res.
+// Coalesced: element index fastest in A ([j][l][Kpad]), rhs, out and Q.  The
+// kernel is bound by reading A: 2 Np^2 words per element (p and u operators),
+// the storage the paper's weight-adjusted inverse avoids.
+namespace wadg {
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128) k_dense_minv(int Kpad, int Np, int fld, const T *__restrict__ Ap,
+                                                    const T *__restrict__ Au, const T *__restrict__ rhs,
+                                                    T *__restrict__ out, T *__restrict__ Q, T a, T b, T dt) {
+    const int e = blockIdx.x * 128 + threadIdx.x;
+    if (e >= Kpad) return;
+    const size_t S = Kpad;
+    for (int c = 0; c < fld; ++c) {
+        const T *A = c == 0 ? Ap : Au;
+        const T *x = rhs + (size_t)c * Np * S + e;
+        for (int j = 0; j < Np; ++j) {
+            const T *Aj = A + (size_t)j * Np * S + e;
+            T acc = 0;
+            for (int l = 0; l < Np; ++l) acc += Aj[(size_t)l * S] * x[(size_t)l * S];
+            const size_t o = ((size_t)c * Np + j) * S + e;
+            if (MODE == 0) {
+                out[o] = acc;
+            } else {
+                const T r = (a == (T)0) ? dt * acc : a * out[o] + dt * acc;
+                out[o] = r;
+                Q[o] += b * r;
+            }
+        }
+    }
+}
+}  // namespace wadg
+
+static int dense_minv(const wadg_problem *P, const void *rhs, void *out, void *Q, int mode, double a,
+                      double b, double dt, cudaStream_t st) {
+    if (!P->minv_u) return fail("minv_p set but minv_u is NULL");
+    const dim3 grid((P->Kpad + 127) / 128);
+    const int fld = P->dim + 1;
+    if (P->dtype == WADG_F64) {
+        if (mode == 0)
+            wadg::k_dense_minv<double, 0><<<grid, 128, 0, st>>>(P->Kpad, P->Np, fld, (const double *)P->minv_p,
+                                                                (const double *)P->minv_u, (const double *)rhs,
+                                                                (double *)out, nullptr, 0., 0., 0.);
+        else
+            wadg::k_dense_minv<double, 1><<<grid, 128, 0, st>>>(P->Kpad, P->Np, fld, (const double *)P->minv_p,
+                                                                (const double *)P->minv_u, (const double *)rhs,
+                                                                (double *)out, (double *)Q, a, b, dt);
+    } else {
+        if (mode == 0)
+            wadg::k_dense_minv<float, 0><<<grid, 128, 0, st>>>(P->Kpad, P->Np, fld, (const float *)P->minv_p,
+                                                               (const float *)P->minv_u, (const float *)rhs,
+                                                               (float *)out, nullptr, 0.f, 0.f, 0.f);
+        else
+            wadg::k_dense_minv<float, 1><<<grid, 128, 0, st>>>(P->Kpad, P->Np, fld, (const float *)P->minv_p,
+                                                               (const float *)P->minv_u, (const float *)rhs,
+                                                               (float *)out, (float *)Q, (float)a, (float)b,
+                                                               (float)dt);
+    }
+    return check_launch("dense mass inverse");
+}
+
 // ---- fused tetrahedral stage -------------------------------------------------
 static long long *g_prof = nullptr;   // debug: per-CTA phase clocks of the next fused launches
 
@@ -835,12 +898,14 @@ int wadg_surface(const wadg_problem *P, const void *Q, void *rhs, double tau_p, 
 
 int wadg_mass_inverse(const wadg_problem *P, const void *rhs, void *out, void *stream) {
     if (validate(P)) return 1;
+    if (P->minv_p) return dense_minv(P, rhs, out, nullptr, 0, 0, 0, 0, (cudaStream_t)stream);
     WADG_DISPATCH(P, upd_minv, P, rhs, out, (cudaStream_t)stream);
 }
 
 int wadg_update_lsrk(const wadg_problem *P, const void *rhs, void *res, void *Q, double a, double b,
                      double dt, void *stream) {
     if (validate(P)) return 1;
+    if (P->minv_p) return dense_minv(P, rhs, res, Q, 1, a, b, dt, (cudaStream_t)stream);
     WADG_DISPATCH(P, upd_lsrk, P, rhs, res, Q, a, b, dt, (cudaStream_t)stream);
 }
 
@@ -927,6 +992,7 @@ int wadg_stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void *r
                      void *stream) {
     if (validate(P)) return 1;
     if (P->dim != 3 || P->formulation != WADG_STRONG_WEAK) return fail("fused stage: 3D strong-weak only");
+    if (P->minv_p) return fail("fused stage: WADG mass inverse only (use wadg_stage for ExactCurvedMass)");
     if (!P->opVA || !P->opVB || !P->opU1 || !P->opU2 || !P->liftT) return fail("fused operators not packed");
     if (Qin == Qout) return fail("fused stage needs distinct Q_in / Q_out buffers");
     if (P->n_halo > 0 && !P->halo) return fail("n_halo > 0 but halo is NULL");

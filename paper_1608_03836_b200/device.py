@@ -152,7 +152,7 @@ class DeviceProblem:
     the C struct pointing at them."""
 
     def __init__(self, mesh, ref, ref_upd, c2, formulation_sw, dtype="float64", device="cuda",
-                 k0=0, k1=None, halo=None):
+                 k0=0, k1=None, halo=None, exact_mass=False):
         if not torch.cuda.is_available() and str(device).startswith("cuda"):
             raise RuntimeError("paper_1608_03836_b200 needs a CUDA device (no CPU fallback)")
         _native.load()
@@ -175,8 +175,12 @@ class DeviceProblem:
         if halo is not None and halo.n_recv:
             self.halo_buf = torch.zeros((halo.n_recv, self.fld, ref.nfp), dtype=self.dtype,
                                         device=self.device)
+        self.exact_mass = bool(exact_mass)
+        self.minv_p = self.minv_u = None
+        if self.exact_mass:
+            self._exact_mass_operators(c2)
         self.struct = self._make_struct()
-        self.fused = self._fused_ops()
+        self.fused = None if self.exact_mass else self._fused_ops()
         self._energy_ready = False
         self.energy_partials = torch.empty(self.Kpad // _native.ELEMS_PER_BLOCK, dtype=torch.float64,
                                            device=self.device)
@@ -246,6 +250,49 @@ class DeviceProblem:
             self.send_f = torch.as_tensor(self.halo.send_f, device=dev)
             self.send_buf = torch.zeros((len(self.halo.send_k), self.fld, ref.nfp), dtype=dt,
                                         device=dev)
+
+    def _exact_mass_operators(self, c2):
+        """ExactCurvedMass comparator (R/.../solver.py:156-167, 302-306): per
+        element A = M^-1 Mhat for the J/c^2- (pressure) and J-weighted (velocity)
+        mass matrices at quadrature degree 2N + 2 N_geo, assembled, inverted and
+        stored on the device in element chunks: (Np, Np, Kpad) each."""
+        ref, mesh, dev = self.ref, self.mesh, self.device
+        N, Np, K = ref.N, ref.Np, self.K
+        ref_m = refelem.build_reference_element(N, mesh.shape, 2 * N + 2 * mesh.N_geo, 1)
+        mm = geometry.map_operators(mesh.shape, mesh.N_geo, ref_m).to(dev)
+        Vq = torch.as_tensor(ref_m.Vq, dtype=torch.float64, device=dev)
+        wq = torch.as_tensor(ref_m.wq, dtype=torch.float64, device=dev)
+        Mhat = torch.as_tensor(ref.Mhat, dtype=torch.float64, device=dev)
+        self.minv_p = torch.zeros((Np, Np, self.Kpad), dtype=self.dtype, device=dev)
+        self.minv_u = torch.zeros((Np, Np, self.Kpad), dtype=self.dtype, device=dev)
+        chunk = max(1, min(CHUNK, (1 << 28) // (8 * Np * Np * 4)))
+        for c0 in range(0, K, chunk):
+            c1 = min(K, c0 + chunk)
+            X = torch.as_tensor(np.asarray(self.mesh.elem_map_nodes[self.k0 + c0:self.k0 + c1],
+                                           dtype=np.float64), device=dev)
+            g = geometry.geometric_factors(X, mm, k_offset=self.k0 + c0)
+            J = g["J"]
+            if callable(c2):
+                xyz = [a.cpu().numpy() for a in g["xq"]]
+                cv = torch.as_tensor(np.array(np.broadcast_to(np.asarray(c2(*xyz), dtype=float), J.shape)), device=dev)
+            else:
+                cv = float(c2)
+            for w, dst in ((J / cv, self.minv_p), (J, self.minv_u)):
+                M = torch.einsum("kq,qi,qj->kij", w * wq, Vq, Vq)
+                M = 0.5 * (M + M.transpose(1, 2))
+                A = torch.linalg.solve(M, Mhat.expand(M.shape[0], Np, Np))
+                dst[:, :, c0:c1] = A.permute(1, 2, 0).to(self.dtype)
+            del g, X
+
+    def host_mass_inverses(self):
+        """(K, Np, Np) numpy M_k^-1 for pressure and velocity (the reference's
+        disc.mass_inv_p / mass_inv_u), recovered from the stored A = M^-1 Mhat."""
+        Mi = np.asarray(self.ref.Mhat_inv)
+        out = []
+        for A in (self.minv_p, self.minv_u):
+            a = A[:, :, :self.K].permute(2, 0, 1).to(torch.float64).cpu().numpy()
+            out.append(a @ Mi)
+        return out
 
     def _fused_ops(self):
         """Repack the operators for wadg_stage_fused (3D strong-weak with the
@@ -377,6 +424,8 @@ class DeviceProblem:
         s.nbr, s.ncode = self.nbr.data_ptr(), self.ncode.data_ptr()
         s.halo = self.halo_buf.data_ptr() if self.halo_buf is not None else None
         s.n_halo = self.halo.n_recv if self.halo is not None else 0
+        if self.minv_p is not None:
+            s.minv_p, s.minv_u = self.minv_p.data_ptr(), self.minv_u.data_ptr()
         return s
 
     def with_formulation(self, strong_weak):
@@ -394,5 +443,6 @@ class DeviceProblem:
 
     def nbytes(self):
         tensors = [self.geo, self.fgeo, self.wu, self.nbr, self.ncode] + (
-            [self.wp] if self.wp is not None else [])
+            [self.wp] if self.wp is not None else []) + (
+            [self.minv_p, self.minv_u] if self.minv_p is not None else [])
         return sum(t.numel() * t.element_size() for t in tensors)

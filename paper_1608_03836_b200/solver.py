@@ -167,9 +167,6 @@ class Discretization:
 
     def __init__(self, mesh, config, medium=MediumField(), device="cuda", k_range=None, halo=None):
         vol_deg, face_deg = _degrees(mesh, config)
-        if config.mass_mode is MassMode.ExactCurvedMass:
-            raise ConfigError("ExactCurvedMass is the dense storage comparator; the device path "
-                              "implements the matrix-free WADG inverse only")
         if config.dtype not in ("float64", "float32"):
             raise ConfigError(f"dtype must be float64 or float32, got {config.dtype!r}")
         self.mesh, self.config, self.medium = mesh, config, medium
@@ -180,8 +177,7 @@ class Discretization:
         upd_deg = config.update_quad_degree or (2 * config.N + 1)
         self.ref_upd = refelem.build_reference_element(
             config.N, mesh.shape, volume_quad_degree=upd_deg, face_quad_degree=1)
-        self.mass_inv_p = None
-        self.mass_inv_u = None
+        self.exact_mass = config.mass_mode is MassMode.ExactCurvedMass
         self.strong_weak = config.formulation is Formulation.StrongWeak
         self.dim = mesh.shape.dim
         self._device = device
@@ -198,8 +194,25 @@ class Discretization:
             k0, k1 = self._k_range if self._k_range is not None else (0, self.mesh.K)
             self._dev = DeviceProblem(self.mesh, self.ref, self.ref_upd, self.c2_spec,
                                       self.strong_weak, self.config.dtype, self._device,
-                                      k0, k1, self._halo)
+                                      k0, k1, self._halo, exact_mass=self.exact_mass)
         return self._dev
+
+    # -- ExactCurvedMass comparator: dense per-element inverses (solver.py:156-167);
+    # None in WADG mode, which stores only pointwise weights
+    @property
+    def mass_inv_p(self):
+        if not self.exact_mass:
+            return None
+        if "mass_inv" not in self._host:
+            self._host["mass_inv"] = self.dev.host_mass_inverses()
+        return self._host["mass_inv"][0]
+
+    @property
+    def mass_inv_u(self):
+        if not self.exact_mass:
+            return None
+        self.mass_inv_p
+        return self._host["mass_inv"][1]
 
     # -- host reference attributes (diagnostics / compatibility) -------------
     def _host_geo(self):
@@ -359,7 +372,8 @@ def rhs_pre_mass(state, disc):
 
 
 def apply_mass_inverse(rhs_pre, disc):
-    """WADG mass inverse on a premultiplied RHS (R/.../solver.py:290-301)."""
+    """Mass inverse on a premultiplied RHS (R/.../solver.py:290-306): matrix-free
+    WADG, or the stored dense inverses of the ExactCurvedMass comparator."""
     import ctypes
     _check_state(rhs_pre, disc)
     d = disc.dev

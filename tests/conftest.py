@@ -43,4 +43,5 @@ GOLDEN_CASES = {
     "tri_strong_het": het_c2,
     "quad_sw": 1.0,
     "quad_strong": het_c2,
+    "tri_exact": het_c2,          # ExactCurvedMass comparator
 }

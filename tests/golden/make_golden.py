@@ -83,7 +83,10 @@ def dump_case(name, rmesh, cfg, medium, steps, dt, ic=cos_mode, run_T=None, exac
         end_p=s.p, end_u1=s.u1, end_u2=s.u2, end_t=s.t,
         energy_ic=rsv.energy(s0, disc), energy_end=rsv.energy(s, disc),
         energy_rand=rsv.energy(st, disc),
+        exact_mass=int(cfg.mass_mode is rsv.MassMode.ExactCurvedMass),
     )
+    if disc.mass_inv_p is not None:
+        out.update(mass_inv_p=disc.mass_inv_p, mass_inv_u=disc.mass_inv_u)
     if run_T is not None:
         _, diag = rsv.run(rmesh, cfg, ic, run_T, medium, exact_p=exact, n_outputs=2, dt=dt)
         out.update(run_T=run_T, run_t=diag["t"], run_energy=diag["energy"],
@@ -108,6 +111,9 @@ def main():
     dump_case("quad_sw", mq, SC(N=3, formulation=F.StrongWeak), rsv.MediumField(1.0), 3, 2e-3)
     dump_case("quad_strong", mq, SC(N=2, formulation=F.Strong, flux=FP(0.0, 0.5)),
               rsv.MediumField(het_c2), 2, 2e-3)
+    # ExactCurvedMass comparator: dense per-element inverses (solver.py:156-167, 302-306)
+    dump_case("tri_exact", m2, SC(N=3, formulation=F.StrongWeak, mass_mode=rsv.MassMode.ExactCurvedMass),
+              rsv.MediumField(het_c2), 3, 1e-3)
 
 
 if __name__ == "__main__":

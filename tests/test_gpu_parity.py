@@ -30,7 +30,8 @@ def golden_disc(name, dtype="float64"):
     g = load_golden(name)
     mesh = golden_mesh(g)
     form = Formulation.StrongWeak if int(g["strong_weak"]) else Formulation.Strong
-    cfg = SolverConfig(N=int(g["N"]), formulation=form,
+    mode = solver.MassMode.ExactCurvedMass if int(g["exact_mass"]) else solver.MassMode.WADG
+    cfg = SolverConfig(N=int(g["N"]), formulation=form, mass_mode=mode,
                        flux=FluxParams(float(g["tau_p"]), float(g["tau_u"])), dtype=dtype)
     disc = solver.Discretization(mesh, cfg, solver.MediumField(GOLDEN_CASES[name]))
     return g, mesh, disc
@@ -278,3 +279,70 @@ def test_tensor_core_and_cuda_core_fused_kernels_agree(N, rng):
 
 def refelem_np(N):
     return (N + 1) * (N + 2) * (N + 3) // 6
+
+
+def _cube_mode_ic(x, y, z):
+    p = np.cos(np.pi * x / 2) * np.cos(np.pi * y / 2) * np.cos(np.pi * z / 2)
+    return p, 0 * p, 0 * p, 0 * p
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_exact_mass_comparator_matches_oracle_3d(dtype, rng):
+    """ExactCurvedMass on curved tets with a heterogeneous medium: the device
+    dense-inverse path (wadg_mass_inverse / wadg_stage with minv_p) against the
+    oracle's restatement of R/.../solver.py:156-167, 302-306."""
+    N = 3
+    mesh = meshgen.warped_cube_tet_mesh(3, N)
+    c2 = lambda x, y, z: 1.0 + 0.5 * np.sin(np.pi * x) * np.sin(np.pi * y) * np.sin(np.pi * z)
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, mass_mode=solver.MassMode.ExactCurvedMass,
+                       dtype=dtype)
+    disc = solver.Discretization(mesh, cfg, solver.MediumField(c2))
+    od = O.OracleDiscretization(mesh, N, True, c2=c2, exact_mass=True)
+    fl = [rng.standard_normal((mesh.K, refelem_np(N))) for _ in range(4)]
+    got = solver.rhs_full(FieldState.from_fields(fl), disc).fields()
+    want = O.rhs_full(O.State(fl[0], fl[1:]), od).fields()
+    assert rel(got, want) < (1e-12 if dtype == "float64" else 1e-5)
+    # stored dense inverses equal the oracle's (host view of the device data)
+    assert np.max(np.abs(disc.mass_inv_p - od.mass_inv_p)) < (1e-10 if dtype == "float64" else 1e-4) * np.abs(
+        od.mass_inv_p).max()
+    # two LSRK steps through the three-kernel stage (the fused stage is WADG-only)
+    st, ost = FieldState.from_fields(fl), O.State(fl[0], fl[1:])
+    for _ in range(2):
+        st = solver.lsrk_step(st, 2e-3, disc.rhs)
+        ost = O.lsrk_step(ost, 2e-3, lambda y: O.rhs_full(y, od))
+    assert rel(st.fields(), ost.fields()) < TOL[dtype]
+
+
+def test_exact_mass_equals_wadg_on_affine_unit_speed(rng):
+    """R/pkg/tests/test_solver.py:118-126 on affine tetrahedra with c = 1."""
+    N = 3
+    mesh = meshgen.warped_cube_tet_mesh(2, N, amp=0.0)
+    fl = [rng.standard_normal((mesh.K, refelem_np(N))) for _ in range(4)]
+    outs = []
+    for mode in (solver.MassMode.WADG, solver.MassMode.ExactCurvedMass):
+        disc = solver.Discretization(mesh, SolverConfig(N=N, formulation=Formulation.StrongWeak, mass_mode=mode))
+        outs.append(solver.rhs_full(FieldState.from_fields(fl), disc).fields())
+    for x, y in zip(*outs):
+        assert np.max(np.abs(np.asarray(x) - np.asarray(y))) < 1e-10 * max(1.0, np.abs(np.asarray(y)).max())
+
+
+def test_wadg_vs_exact_mass_error_ratio_3d():
+    """The paper's accuracy claim, the 3D analogue of R/pkg/tests/test_solver.py:
+    143-152: on curved tetrahedra the WADG solution error against the exact
+    Dirichlet eigenmode equals the exact-mass solution error to within 1 %."""
+    N, T, steps = 3, 0.25, 25
+    mesh = meshgen.warped_cube_tet_mesh(4, N)
+    w = np.pi * np.sqrt(3) / 2
+    od = O.OracleDiscretization(mesh, N, True)
+    xq = od.geo.xyzq
+    pex = np.cos(np.pi * xq[0] / 2) * np.cos(np.pi * xq[1] / 2) * np.cos(np.pi * xq[2] / 2) * np.cos(w * T)
+    W = od.ref.wq[None, :] * od.geo.Jq
+    errs = {}
+    for mode in (solver.MassMode.WADG, solver.MassMode.ExactCurvedMass):
+        disc = solver.Discretization(mesh, SolverConfig(N=N, formulation=Formulation.StrongWeak, mass_mode=mode))
+        st = solver.project_initial_condition(mesh, disc.config, _cube_mode_ic)
+        for _ in range(steps):
+            st = solver.lsrk_step(st, T / steps, disc.rhs)
+        errs[mode] = np.sqrt(np.sum(W * (od.interp(np.asarray(st.p)) - pex) ** 2))
+    ratio = errs[solver.MassMode.WADG] / errs[solver.MassMode.ExactCurvedMass]
+    assert 0.99 <= ratio <= 1.01

@@ -35,8 +35,12 @@ def test_bad_dtype_and_exact_mass_mode():
     mesh = meshgen.warped_triangle_mesh(2, 2)
     with pytest.raises(ConfigError):
         solver.Discretization(mesh, SolverConfig(N=2, dtype="float16"))
-    with pytest.raises(ConfigError):
-        solver.Discretization(mesh, SolverConfig(N=2, mass_mode=MassMode.ExactCurvedMass))
+    # the ExactCurvedMass comparator is accepted; WADG mode stores no dense matrices
+    # (R/pkg/tests/test_solver.py:128-133)
+    dE = solver.Discretization(mesh, SolverConfig(N=2, mass_mode=MassMode.ExactCurvedMass))
+    assert dE.exact_mass
+    dW = solver.Discretization(mesh, SolverConfig(N=2))
+    assert dW.mass_inv_p is None and dW.mass_inv_u is None
 
 
 def test_sufficient_quadrature_degrees():

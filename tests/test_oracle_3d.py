@@ -164,3 +164,28 @@ def test_dirichlet_eigenmode_convergence():
         hs.append(2 / n)
     slope = np.log(errs[0] / errs[1]) / np.log(hs[0] / hs[1])
     assert slope > N + 0.5
+
+
+def test_wadg_and_exact_mass_errors_agree_on_curved_tets():
+    """The paper's accuracy claim in 3D (analogue of R/pkg/tests/test_solver.py:
+    143-152): against the exact Dirichlet eigenmode, WADG and the dense
+    ExactCurvedMass inverse give the same error to within 1 %."""
+    N, n, T, steps = 2, 3, 0.2, 10
+    mesh = meshgen.warped_cube_tet_mesh(n, N)
+    w = np.pi * np.sqrt(3) / 2
+
+    def ic(x, y, z):
+        p = np.cos(np.pi * x / 2) * np.cos(np.pi * y / 2) * np.cos(np.pi * z / 2)
+        return p, 0 * p, 0 * p, 0 * p
+
+    errs = []
+    for exact in (False, True):
+        od = O.OracleDiscretization(mesh, N, True, exact_mass=exact)
+        st = O.project_initial_condition(mesh, N, ic)
+        for _ in range(steps):
+            st = O.lsrk_step(st, T / steps, lambda y: O.rhs_full(y, od))
+        xq = od.geo.xyzq
+        pex = np.cos(np.pi * xq[0] / 2) * np.cos(np.pi * xq[1] / 2) * np.cos(np.pi * xq[2] / 2) * np.cos(w * T)
+        W = od.ref.wq[None, :] * od.geo.Jq
+        errs.append(np.sqrt(np.sum(W * (od.interp(st.p) - pex) ** 2)))
+    assert 0.99 <= errs[0] / errs[1] <= 1.01

@@ -20,8 +20,17 @@ def setup(name, exterior):
     g = load_golden(name)
     mesh = golden_mesh(g)
     od = O.OracleDiscretization(mesh, int(g["N"]), bool(g["strong_weak"]), float(g["tau_p"]),
-                                float(g["tau_u"]), GOLDEN_CASES[name], exterior=exterior)
+                                float(g["tau_u"]), GOLDEN_CASES[name], exterior=exterior,
+                                exact_mass=bool(g["exact_mass"]))
     return g, mesh, od
+
+
+def test_exact_mass_inverses_match_reference():
+    """ExactCurvedMass comparator: the dense inverses of the J/c^2- and
+    J-weighted mass matrices (R/.../solver.py:156-167) equal the reference's."""
+    g, mesh, od = setup("tri_exact", "gather")
+    for mine, ref in ((od.mass_inv_p, g["mass_inv_p"]), (od.mass_inv_u, g["mass_inv_u"])):
+        assert np.max(np.abs(mine - ref)) < 1e-11 * np.abs(ref).max()
 
 
 def fields(g, pfx):
