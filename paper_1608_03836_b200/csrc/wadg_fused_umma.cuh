@@ -553,8 +553,11 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         uint32_t nA = 0, nB = 0;             // consumed completions of MMA groups A and B
         auto wait_A = [&]() { wait_k(&bar[0], ++nA); fence_after(); };
         auto wait_B = [&]() { wait_k(&bar[7], ++nB); fence_after(); };
-        auto to_mma = [&](int id) {           // hand TMEM / smem writes to the MMA warp
-            fused::fence_proxy_async();
+        // hand TMEM (and, with smem = true, shared-memory operand) writes to the
+        // MMA warp; the proxy fence is only needed for shared memory the tensor
+        // core reads through descriptors
+        auto to_mma = [&](int id, bool smem = false) {
+            if (smem) fused::fence_proxy_async();
             fence_before();
             nb_arrive(id, NB);
         };
@@ -677,7 +680,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 }
             }
             wait_st();
-            to_mma(B_S0);
+            to_mma(B_S0, true);
             if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
             for (int hh = 0; hh < NFH; ++hh) {
                 const int step = f * NFH + hh;
@@ -763,7 +766,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             }
             wait_st();
         }
-        to_mma(B_R);
+        to_mma(B_R, true);
         for (int u = 0; u < NCHU; ++u) {
             float wa[8], wb[8];
 #pragma unroll
