@@ -645,57 +645,68 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 fg[d][0] = v.x; fg[d][1] = v.y; fg[d][2] = v.z; fg[d][3] = v.w;
             }
         };
-        gather(0);
-        load_fg(0);
-        for (int f = 0; f < NF; ++f) {
+        // own / exterior face-node operands of face f (shared memory + TMEM hi)
+        auto node_store = [&](int f) {
             fused::cp_async_wait<0>();       // this thread's staged neighbour nodes of face f
-            {
-                const int c = sub;
-                const float *xs = sStage + (size_t)c * NFP * ME + e;
+            const int c = sub;
+            const float *xs = sStage + (size_t)c * NFP * ME + e;
 #pragma unroll
-                for (int i0 = 0; i0 < NFPK; i0 += 4) {
-                    float4 vh, vl, oh4, ol4;
-                    float *ph = reinterpret_cast<float *>(&vh), *pl = reinterpret_cast<float *>(&vl);
-                    float *qh = reinterpret_cast<float *>(&oh4), *ql = reinterpret_cast<float *>(&ol4);
+            for (int i0 = 0; i0 < NFPK; i0 += 4) {
+                float4 vh, vl, oh4, ol4;
+                float *ph = reinterpret_cast<float *>(&vh), *pl = reinterpret_cast<float *>(&vl);
+                float *qh = reinterpret_cast<float *>(&oh4), *ql = reinterpret_cast<float *>(&ol4);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const bool in = i0 + i < NFP;
-                        const float x = in ? xs[(i0 + i) * ME] : 0.f;
-                        const float y = in ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i0 + i]) / 4] : 0.f;
-                        ph[i] = tf32_hi(x);
-                        pl[i] = x - ph[i];
-                        qh[i] = tf32_hi(y);
-                        ql[i] = y - qh[i];
-                    }
-                    const uint32_t o = c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4;
-                    *reinterpret_cast<float4 *>(sExtHi + o) = vh;
-                    *reinterpret_cast<float4 *>(sExtLo + o) = vl;
-                    *reinterpret_cast<float4 *>(sOwnLo + o) = ol4;
-                    st4(tl + OWNH + 16 * c + i0, *reinterpret_cast<float (*)[4]>(qh));
+                for (int i = 0; i < 4; ++i) {
+                    const bool in = i0 + i < NFP;
+                    const float x = in ? xs[(i0 + i) * ME] : 0.f;
+                    const float y = in ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i0 + i]) / 4] : 0.f;
+                    ph[i] = tf32_hi(x);
+                    pl[i] = x - ph[i];
+                    qh[i] = tf32_hi(y);
+                    ql[i] = y - qh[i];
                 }
+                const uint32_t o = c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4;
+                *reinterpret_cast<float4 *>(sExtHi + o) = vh;
+                *reinterpret_cast<float4 *>(sExtLo + o) = vl;
+                *reinterpret_cast<float4 *>(sOwnLo + o) = ol4;
+                st4(tl + OWNH + 16 * c + i0, *reinterpret_cast<float (*)[4]>(qh));
+            }
 #pragma unroll
-                for (int i0 = NFPK; i0 < 16; i0 += 4) {
-                    const float z4[4] = {0.f, 0.f, 0.f, 0.f};
-                    st4(tl + OWNH + 16 * c + i0, z4);
-                }
+            for (int i0 = NFPK; i0 < 16; i0 += 4) {
+                const float z4[4] = {0.f, 0.f, 0.f, 0.f};
+                st4(tl + OWNH + 16 * c + i0, z4);
             }
             wait_st();
             to_mma(B_S0, true);
-            if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
-            for (int hh = 0; hh < NFH; ++hh) {
-                const int step = f * NFH + hh;
-                wait_A();                    // traces of this step
+        };
+        // Face-node operands of the next face: with one step per face (N <= 3) they go
+        // in right after that step has read its traces, so the next face's traces
+        // overlap the step's flux; with two or more steps per face (N = 4) they go in
+        // at the face boundary, off the flux critical path.
+        if constexpr (NFH == 1) {
+            // face has read its traces (so the next traces overlap that step's flux)
+            gather(0);
+            load_fg(0);
+            node_store(0);
+            if (NF > 1) gather(1);
+            for (int step = 0; step < NSTEP; ++step) {
+                const int f = step / NFH, hh = step % NFH;
+                wait_A();                        // traces of this step
                 float mM[4][4], mP[4][4];
-#pragma unroll
+    #pragma unroll
                 for (int c = 0; c < 4; ++c) {
                     ld4(tl + OWN + 16 * c + 4 * sub, mM[c]);
                     ld4(tl + EXT + 16 * c + 4 * sub, mP[c]);
                 }
                 wait_ld();
                 fence_before();
-                nb_arrive(B_S2, NB);         // trace columns free for the next step's MMAs
+                nb_arrive(B_S2, NB);             // trace columns free for the next step's MMAs
+                // the last half of a face has consumed the face-node operands: the next
+                // face's go in now, so its traces overlap this step's flux
+                const bool next_face = hh == NFH - 1 && f + 1 < NF;
+                if (next_face) node_store(f + 1);
                 float g[4][4];
-#pragma unroll
+    #pragma unroll
                 for (int p = 0; p < 4; ++p) {
                     const float n0 = fg[0][p], n1 = fg[1][p], n2 = fg[2][p], sJh = fg[3][p];
                     const float dpj = mP[0][p] - mM[0][p];
@@ -709,11 +720,86 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     g[3][p] = fuu * (sJh * n2);
                 }
                 if (step + 1 < NSTEP) load_fg(step + 1);
-                if (step > 0) wait_B();      // lift(step-1) done with the flux columns
-#pragma unroll
+                if (step > 0) wait_B();          // lift(step-1) done with the flux columns
+    #pragma unroll
                 for (int c = 0; c < 4; ++c) st_split4(tl + GH + 16 * c + 4 * sub, tl + GL + 16 * c + 4 * sub, g[c]);
                 wait_st();
                 to_mma(B_S1);
+                // neighbour nodes of the face after next: issued off the flux critical path,
+                // they have at least one step to land before node_store needs them
+                if (next_face && f + 2 < NF) gather(f + 2);
+            }
+        } else {
+            gather(0);
+            load_fg(0);
+            for (int f = 0; f < NF; ++f) {
+                fused::cp_async_wait<0>();       // this thread's staged neighbour nodes of face f
+                {
+                    const int c = sub;
+                    const float *xs = sStage + (size_t)c * NFP * ME + e;
+    #pragma unroll
+                    for (int i0 = 0; i0 < NFPK; i0 += 4) {
+                        float4 vh, vl, oh4, ol4;
+                        float *ph = reinterpret_cast<float *>(&vh), *pl = reinterpret_cast<float *>(&vl);
+                        float *qh = reinterpret_cast<float *>(&oh4), *ql = reinterpret_cast<float *>(&ol4);
+    #pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const bool in = i0 + i < NFP;
+                            const float x = in ? xs[(i0 + i) * ME] : 0.f;
+                            const float y = in ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i0 + i]) / 4] : 0.f;
+                            ph[i] = tf32_hi(x);
+                            pl[i] = x - ph[i];
+                            qh[i] = tf32_hi(y);
+                            ql[i] = y - qh[i];
+                        }
+                        const uint32_t o = c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4;
+                        *reinterpret_cast<float4 *>(sExtHi + o) = vh;
+                        *reinterpret_cast<float4 *>(sExtLo + o) = vl;
+                        *reinterpret_cast<float4 *>(sOwnLo + o) = ol4;
+                        st4(tl + OWNH + 16 * c + i0, *reinterpret_cast<float (*)[4]>(qh));
+                    }
+    #pragma unroll
+                    for (int i0 = NFPK; i0 < 16; i0 += 4) {
+                        const float z4[4] = {0.f, 0.f, 0.f, 0.f};
+                        st4(tl + OWNH + 16 * c + i0, z4);
+                    }
+                }
+                wait_st();
+                to_mma(B_S0, true);
+                if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
+                for (int hh = 0; hh < NFH; ++hh) {
+                    const int step = f * NFH + hh;
+                    wait_A();                    // traces of this step
+                    float mM[4][4], mP[4][4];
+    #pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        ld4(tl + OWN + 16 * c + 4 * sub, mM[c]);
+                        ld4(tl + EXT + 16 * c + 4 * sub, mP[c]);
+                    }
+                    wait_ld();
+                    fence_before();
+                    nb_arrive(B_S2, NB);         // trace columns free for the next step's MMAs
+                    float g[4][4];
+    #pragma unroll
+                    for (int p = 0; p < 4; ++p) {
+                        const float n0 = fg[0][p], n1 = fg[1][p], n2 = fg[2][p], sJh = fg[3][p];
+                        const float dpj = mP[0][p] - mM[0][p];
+                        const float dUn = (mP[1][p] - mM[1][p]) * n0 + (mP[2][p] - mM[2][p]) * n1 + (mP[3][p] - mM[3][p]) * n2;
+                        const float avg = (mP[1][p] + mM[1][p]) * n0 + (mP[2][p] + mM[2][p]) * n1 + (mP[3][p] + mM[3][p]) * n2;
+                        const float fpp = avg - tau_p * dpj;
+                        const float fuu = dpj - tau_u * dUn;
+                        g[0][p] = fpp * sJh;
+                        g[1][p] = fuu * (sJh * n0);
+                        g[2][p] = fuu * (sJh * n1);
+                        g[3][p] = fuu * (sJh * n2);
+                    }
+                    if (step + 1 < NSTEP) load_fg(step + 1);
+                    if (step > 0) wait_B();      // lift(step-1) done with the flux columns
+    #pragma unroll
+                    for (int c = 0; c < 4; ++c) st_split4(tl + GH + 16 * c + 4 * sub, tl + GL + 16 * c + 4 * sub, g[c]);
+                    wait_st();
+                    to_mma(B_S1);
+                }
             }
         }
         wait_B();                            // last lift: R complete
