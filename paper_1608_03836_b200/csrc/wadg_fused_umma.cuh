@@ -689,6 +689,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             load_fg(0);
             node_store(0);
             if (NF > 1) gather(1);
+#pragma unroll 1
             for (int step = 0; step < NSTEP; ++step) {
                 const int f = step / NFH, hh = step % NFH;
                 wait_A();                        // traces of this step
