@@ -1,10 +1,14 @@
-# GPU checkpoint: tests, bench (config 4), ncu launch list + full capture of the stage kernel
+# GPU checkpoint: smoke, tests, bench (config 4) + reference arm, ncu launch list + full capture
 set -x
 mkdir -p gpurun_out
+timeout 600 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+tail -2 gpurun_out/smoke.log
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 tail -3 gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo bench_rc=$?
 cat gpurun_out/bench_c4.json
+timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_rc=$?
+cat gpurun_out/bench_ref.json
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:k_stage --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1; echo ncu1=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage -s 3 -c 1 -o gpurun_out/prof_umma_c4 $CMD > gpurun_out/ncu2.log 2>&1; echo ncu2=$?
