@@ -408,7 +408,11 @@ def main():
             host[i].copy_(bufs["Q"][i, :, :K_local].T.cpu())
         hstate = solver.FieldState.from_fields(host)
         n_e2e = max(2, min(args.steps, 5))
-        hstate = solver.lsrk_step(hstate, dt, disc.rhs)
+        # two untimed calls: the first fills torch's pinned-host block cache with the
+        # output buffer, the second with the one the next call writes while its input
+        # (the previous output) is still alive; later calls reuse the two blocks
+        for _ in range(2):
+            hstate = solver.lsrk_step(hstate, dt, disc.rhs)
         torch.cuda.synchronize()
         e0, e1 = _t.cuda.Event(enable_timing=True), _t.cuda.Event(enable_timing=True)
         e0.record(stream)
