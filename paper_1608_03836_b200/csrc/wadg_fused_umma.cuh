@@ -854,6 +854,33 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             wait_st();
         }
         to_mma(B_R, true);
+        {   // L2 prefetch while the update runs on the tensor core: this tile's res rows
+            // (read by the LSRK write) and the fields, neighbour tables and first
+            // geometric-factor chunk of the tile that will most likely start on this SM
+            // next (launch order: one resident CTA per SM)
+            uint32_t nsm;
+            asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+            const size_t nxt = blk + nsm;
+            const bool has_next = nxt < (size_t)(P.Kpad / ME);
+            const int t512 = warp * 32 + lane;                   // 0..511
+            auto pf = [](const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); };
+            for (int r = t512; r < 4 * NP * 4; r += 512) {     // 4 x 128 B lines per 512 B row
+                const size_t row = r >> 2, off = (r & 3) * 32;
+                pf(res + row * S + kblk + off);
+                if (has_next) pf(Qin + row * S + nxt * ME + off);
+            }
+            if (has_next) {
+                for (int r = t512; r < 2 * NF * 4; r += 512) {
+                    const int row = r >> 2, off = (r & 3) * 32;
+                    pf((row < NF ? P.nbr + (size_t)row * S : P.ncode + (size_t)(row - NF) * S) + nxt * ME + off);
+                }
+                constexpr int GQ4n = NCH * 4;
+                for (int r = t512; r < 9 * 4 * 16; r += 512) {  // chunk 0: 4 float4 rows of 2 KB per factor
+                    const int gr = r / 64, q4 = (r / 16) % 4, ln = r % 16;
+                    pf(reinterpret_cast<const float4 *>(P.geo_il) + ((nxt * 9 + gr) * GQ4n + q4) * ME + ln * 8);
+                }
+            }
+        }
         for (int u = 0; u < NCHU; ++u) {
             float wa[8], wb[8];
 #pragma unroll
