@@ -424,7 +424,7 @@ def main():
         nb = sum(h.numel() * h.element_size() for h in host)
         e2e = {"value": dof_stage * 5 / (e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
                "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "ms_per_step": e_ms,
-               "api": "solver.lsrk_step(FieldState(pinned host tensors), dt, disc.rhs)"}
+               "api": "solver.lsrk_step(FieldState(pinned host tensors), dt, disc.rhs) -> HostPipeline (chunked H2D / stages / D2H overlap)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -167,6 +167,15 @@ int wadg_stage_fused(const wadg_problem *P, const void *Q_in, void *Q_out, void 
                      double tau_p, double tau_u, double a, double b, double dt,
                      int block_begin, int block_end, void *stream);
 
+/* wadg_stage_fused with fields in the host row layout (see
+ * wadg_rows_to_fields): layout 1 = Q_in is (dim+1, K, Np) (the first stage of
+ * a step on a host state), 2 = Q_out is (the last stage).  res stays in the
+ * field layout.  Only the tcgen05 stage (fp32, N = 2..4) supports 1 and 2;
+ * otherwise it fails and the caller converts with wadg_rows_to_fields. */
+int wadg_stage_fused_rows(const wadg_problem *P, const void *Q_in, void *Q_out, void *res,
+                          double tau_p, double tau_u, double a, double b, double dt,
+                          int block_begin, int block_end, int layout, void *stream);
+
 /* Debug: when buf != NULL, each CTA of subsequent wadg_stage_fused launches
  * writes clock64() at 7 phase boundaries to buf[cta*8 + 0..6] (int64). */
 int wadg_debug_set_phase_clock_buffer(void *buf);
@@ -184,6 +193,21 @@ int wadg_debug_umma_test(const void *A, const void *B, void *C, int N, int K, in
 /* buf[(s*(dim+1) + fld)*Nfp + i] = Q[fld][fmask[send_f[s]][i]][send_k[s]] */
 int wadg_pack_halo(const wadg_problem *P, const void *Q, const int32_t *send_k,
                    const int32_t *send_f, int32_t n_send, void *buf, void *stream);
+
+/* Host-layout conversion for element range [k0, k1) (the pipelined
+ * host-state LSRK step): `rows` is the FieldState layout, (dim+1) fields of
+ * (K, Np) row-major (R/pkg/src/wadg/solver.py:94 FieldState), dense on the
+ * device; Q the (dim+1, Np, Kpad) field layout.  Only [k0, k1) is touched. */
+int wadg_rows_to_fields(const wadg_problem *P, const void *rows, int32_t k0, int32_t k1, void *Q,
+                        void *stream);
+int wadg_fields_to_rows(const wadg_problem *P, const void *Q, int32_t k0, int32_t k1, void *rows,
+                        void *stream);
+
+/* Debug / measurement: tcgen05.mma issue rate.  One CTA, one warp issues
+ * `count` kind::tf32 MMAs (M = 128, K = 8, N = n) back to back; out[0] =
+ * clock64 cycles of the issue loop, out[1] = until the commit completed.
+ * mode 0: A from shared memory, 1: A from TMEM, 2: as 0, 8 MMAs per asm block. */
+int wadg_debug_umma_rate(void *out, int n, int count, int mode, void *stream);
 
 #ifdef __cplusplus
 }

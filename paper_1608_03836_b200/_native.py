@@ -60,10 +60,16 @@ EXPORTS = {
     "wadg_stage_fused": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, ctypes.c_double, ctypes.c_double,
                           ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
                           _vp], ctypes.c_int),
+    "wadg_stage_fused_rows": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, ctypes.c_double, ctypes.c_double,
+                               ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                               ctypes.c_int, _vp], ctypes.c_int),
     "wadg_debug_set_phase_clock_buffer": ([_vp], ctypes.c_int),
     "wadg_microbench_fma": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp], ctypes.c_int),
     "wadg_debug_umma_test": ([_vp, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
     "wadg_pack_halo": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, _i32, _vp, _vp], ctypes.c_int),
+    "wadg_rows_to_fields": ([ctypes.POINTER(WadgProblem), _vp, _i32, _i32, _vp, _vp], ctypes.c_int),
+    "wadg_fields_to_rows": ([ctypes.POINTER(WadgProblem), _vp, _i32, _i32, _vp, _vp], ctypes.c_int),
+    "wadg_debug_umma_rate": ([_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp], ctypes.c_int),
 }
 
 _lib = None

@@ -187,7 +187,10 @@ __device__ __forceinline__ void wait_k(uint64_t *bar, uint32_t k, int site = -1)
 // w / 4); warp 16 is the MMA warp: it issues every tcgen05.mma and TMA copy and
 // never blocks the epilogue warps, which hand over through named barriers
 // (bar.arrive) and take results back through tcgen05.commit mbarriers.
-template <int N>
+// LAY bit 0: Qin in the host row layout (fld, K, Np) (first stage of the host
+// pipeline), bit 1: Qout in the row layout (last stage); res is always in the
+// field layout.
+template <int N, int LAY>
 __global__ void __launch_bounds__(CfgU<N>::NTH, 1)
 k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *__restrict__ Qout,
              float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt, int block0) {
@@ -250,22 +253,43 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         }
         // ---- fields -> sQ (raw fp32, the tf32 hi operand) and sQlo --------
         const int c = sub;
-#pragma unroll
-        for (int j0 = 0; j0 < NPK; j0 += 4) {
-            float4 v;
-            float *pv = reinterpret_cast<float *>(&v);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int j = j0 + i;
-                pv[i] = j < NP ? __ldg(Qin + (size_t)(c * NP + j) * S + kblk + e) : 0.f;
+        if constexpr (LAY & 1) {
+            // row layout: this warp's 32 elements of field c are one contiguous run
+            // of 32 Np values; read it coalesced and scatter into the K-major tiles
+            const long long e0 = (long long)kblk + 32 * qd;
+            const int cnt = (int)max(0LL, min(32LL, (long long)P.K - e0)) * NP;
+            const float *src = Qin + ((size_t)c * P.K + e0) * NP;
+            for (int t = lane; t < 32 * NP; t += 32) {
+                const float v = t < cnt ? __ldg(src + t) : 0.f;
+                const int el = t / NP, j = t - el * NP;
+                const uint32_t o = c * ME * NPK + kmaj_off<NPK>(32 * qd + el, j) / 4;
+                sQ[o] = v;
+                sQlo[o] = tf32_lo(v);
             }
-            float4 l;
-            float *pl = reinterpret_cast<float *>(&l);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) pl[i] = tf32_lo(pv[i]);
-            const uint32_t o = kmaj_off<NPK>(e, j0) / 4;
-            *reinterpret_cast<float4 *>(sQ + c * ME * NPK + o) = v;
-            *reinterpret_cast<float4 *>(sQlo + c * ME * NPK + o) = l;
+            for (int j = NP; j < NPK; ++j) {
+                const uint32_t o = c * ME * NPK + kmaj_off<NPK>(e, j) / 4;
+                sQ[o] = 0.f;
+                sQlo[o] = 0.f;
+            }
+        } else {
+#pragma unroll
+            for (int j0 = 0; j0 < NPK; j0 += 4) {
+                float4 v;
+                float *pv = reinterpret_cast<float *>(&v);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = j0 + i;
+                    pv[i] = j < NP ? __ldg(Qin + (size_t)(c * NP + j) * S + kblk + e) : 0.f;
+                }
+                float4 l;
+                float *pl = reinterpret_cast<float *>(&l);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) pl[i] = tf32_lo(pv[i]);
+                const uint32_t o = kmaj_off<NPK>(e, j0) / 4;
+                *reinterpret_cast<float4 *>(sQ + c * ME * NPK + o) = v;
+                *reinterpret_cast<float4 *>(sQlo + c * ME * NPK + o) = l;
+            }
         }
     }
     fused::fence_proxy_async();
@@ -622,7 +646,10 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 #pragma unroll
             for (int i = 0; i < NFP; ++i) {
                 if (nb >= 0) {
-                    fused::cp_async_elem(dst + i * ME, Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
+                    if constexpr (LAY & 1)
+                        fused::cp_async_elem(dst + i * ME, Qin + ((size_t)c * P.K + nb) * NP + sExt[code * NFP + i]);
+                    else
+                        fused::cp_async_elem(dst + i * ME, Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
                 } else if (nb == -1) {   // mirror BC (solver.py:214-217): p+ = -p-, u+ = u-
                     const float m = sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4];
                     dst[i * ME] = c == 0 ? -m : m;
@@ -867,7 +894,13 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             for (int r = t512; r < 4 * NP * 4; r += 512) {     // 4 x 128 B lines per 512 B row
                 const size_t row = r >> 2, off = (r & 3) * 32;
                 pf(res + row * S + kblk + off);
-                if (has_next) pf(Qin + row * S + nxt * ME + off);
+                if constexpr (LAY & 1) {     // next tile: 4 contiguous runs of 128 Np floats
+                    const size_t c = r / (NP * 4), ln = r % (NP * 4);
+                    if (has_next && nxt * ME < (size_t)P.K)
+                        pf(Qin + (c * P.K + nxt * ME) * NP + ln * 32);
+                } else {
+                    if (has_next) pf(Qin + row * S + nxt * ME + off);
+                }
             }
             if (has_next) {
                 for (int r = t512; r < 2 * NF * 4; r += 512) {
@@ -927,8 +960,23 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                         const size_t o = (size_t)(c * NP + j) * S + kblk + e;
                         const float r = (a_rk == 0.f) ? dt * v[i] : a_rk * res[o] + dt * v[i];
                         res[o] = r;
-                        Qout[o] = sQ[c * ME * NPK + kmaj_off<NPK>(e, j) / 4] + b_rk * r;
+                        const uint32_t so = c * ME * NPK + kmaj_off<NPK>(e, j) / 4;
+                        const float q = sQ[so] + b_rk * r;
+                        if constexpr (LAY & 2)
+                            sQ[so] = q;      // in place (this thread's own entry), stored below
+                        else
+                            Qout[o] = q;
                     }
+                }
+            }
+            if constexpr (LAY & 2) {   // row layout: the warp's 32 elements of field c, one coalesced run
+                __syncwarp();
+                const long long e0 = (long long)kblk + 32 * qd;
+                const int cnt = (int)max(0LL, min(32LL, (long long)P.K - e0)) * NP;
+                float *dst = Qout + ((size_t)c * P.K + e0) * NP;
+                for (int t = lane; t < cnt; t += 32) {
+                    const int el = t / NP, j = t - el * NP;
+                    dst[t] = sQ[c * ME * NPK + kmaj_off<NPK>(32 * qd + el, j) / 4];
                 }
             }
         }

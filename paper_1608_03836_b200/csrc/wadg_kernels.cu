@@ -813,9 +813,9 @@ static int fused_launch_tc(const wadg_problem *Pc, const void *Qin, void *Qout, 
     return check_launch("wadg_stage_fused(tc)");
 }
 
-template <int N>
-static int fused_launch_umma(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
-                             double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
+template <int N, int LAY>
+static int launch_umma_lay(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
+                           double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
     using C = uk::CfgU<N>;
     if (Pc->Kpad % C::ME) return fail("Kpad must be a multiple of the fused block size");
     if (!Pc->geo_il || !Pc->fgeo_il || !Pc->wu_il || (Pc->wp && !Pc->wp_il))
@@ -826,23 +826,35 @@ static int fused_launch_umma(const wadg_problem *Pc, const void *Qin, void *Qout
     if (b1 <= b0) return 0;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(uk::k_stage_umma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(uk::k_stage_umma<N, LAY>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
         if (e != cudaSuccess) return fail(cudaGetErrorString(e));
         attr_set = true;
     }
-    uk::k_stage_umma<N><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin, (float *)Qout,
-                                                        (float *)res, (float)tp, (float)tu, (float)a, (float)b,
-                                                        (float)dt, b0);
+    uk::k_stage_umma<N, LAY><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin,
+                                                             (float *)Qout, (float *)res, (float)tp, (float)tu,
+                                                             (float)a, (float)b, (float)dt, b0);
     return check_launch("wadg_stage_fused(umma)");
+}
+
+template <int N>
+static int fused_launch_umma(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
+                             double tu, double a, double b, double dt, int b0, int b1, int lay, cudaStream_t st) {
+    switch (lay) {
+        case 0: return launch_umma_lay<N, 0>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+        case 1: return launch_umma_lay<N, 1>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+        case 2: return launch_umma_lay<N, 2>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+        default: return fail("row layout on both Q_in and Q_out is not supported");
+    }
 }
 
 template <typename T, int N>
 static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
-                        double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
+                        double tu, double a, double b, double dt, int b0, int b1, int lay, cudaStream_t st) {
     if constexpr (umma_available<T, N>()) {
-        if (use_umma<T, N>()) return fused_launch_umma<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+        if (use_umma<T, N>()) return fused_launch_umma<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, lay, st);
     }
+    if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
     if constexpr (tc_available<T, N>()) {
         if (use_tc<T, N>()) return fused_launch_tc<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
     }
@@ -876,6 +888,53 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
         case 7: return FN<T, 7>(__VA_ARGS__);     \
         default: return fail("fused stage compiled for N = 1..7 only"); \
     }
+
+// host row layout (fld, K, Np) <-> device field layout (fld, Np, Kpad) for
+// elements [k0, k1): 32 x 32 tiles through shared memory, both sides coalesced
+namespace wadg {
+template <typename T, bool TO_FIELDS>
+__global__ void __launch_bounds__(256) k_rows_fields(const T *__restrict__ src, T *__restrict__ dst, int K, int Kpad,
+                                                      int Np, int k0, int k1) {
+    __shared__ T tile[32][33];
+    const int f = blockIdx.z, kb = k0 + 32 * blockIdx.x, jb = 32 * blockIdx.y;
+    const size_t rows = (size_t)f * K * Np, flds = (size_t)f * Np * Kpad;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int r = ty; r < 32; r += 8) {
+        if (TO_FIELDS) {                 // read row k = kb + r, node jb + tx
+            const int k = kb + r, j = jb + tx;
+            if (k < k1 && j < Np) tile[r][tx] = src[rows + (size_t)k * Np + j];
+        } else {                         // read field node j = jb + r, element kb + tx
+            const int j = jb + r, k = kb + tx;
+            if (k < k1 && j < Np) tile[r][tx] = src[flds + (size_t)j * Kpad + k];
+        }
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        if (TO_FIELDS) {                 // write node j = jb + r, element kb + tx
+            const int j = jb + r, k = kb + tx;
+            if (k < k1 && j < Np) dst[flds + (size_t)j * Kpad + k] = tile[tx][r];
+        } else {                         // write row k = kb + r, node jb + tx
+            const int k = kb + r, j = jb + tx;
+            if (k < k1 && j < Np) dst[rows + (size_t)k * Np + j] = tile[tx][r];
+        }
+    }
+}
+}  // namespace wadg
+
+template <bool TO_FIELDS>
+static int rows_fields(const wadg_problem *P, const void *src, void *dst, int k0, int k1, cudaStream_t st) {
+    if (validate(P)) return 1;
+    if (k0 < 0 || k1 > P->K || k0 > k1) return fail("element range outside [0, K]");
+    if (k0 == k1) return 0;
+    const dim3 grid((k1 - k0 + 31) / 32, (P->Np + 31) / 32, P->dim + 1);
+    if (P->dtype == WADG_F64)
+        wadg::k_rows_fields<double, TO_FIELDS><<<grid, 256, 0, st>>>((const double *)src, (double *)dst, P->K,
+                                                                     P->Kpad, P->Np, k0, k1);
+    else
+        wadg::k_rows_fields<float, TO_FIELDS><<<grid, 256, 0, st>>>((const float *)src, (float *)dst, P->K,
+                                                                    P->Kpad, P->Np, k0, k1);
+    return check_launch(TO_FIELDS ? "wadg_rows_to_fields" : "wadg_fields_to_rows");
+}
 
 extern "C" {
 
@@ -970,6 +1029,14 @@ int wadg_pack_halo(const wadg_problem *P, const void *Q, const int32_t *send_k, 
     return check_launch("wadg_pack_halo");
 }
 
+int wadg_rows_to_fields(const wadg_problem *P, const void *rows, int32_t k0, int32_t k1, void *Q, void *stream) {
+    return rows_fields<true>(P, rows, Q, k0, k1, (cudaStream_t)stream);
+}
+
+int wadg_fields_to_rows(const wadg_problem *P, const void *Q, int32_t k0, int32_t k1, void *rows, void *stream) {
+    return rows_fields<false>(P, Q, rows, k0, k1, (cudaStream_t)stream);
+}
+
 int wadg_debug_set_phase_clock_buffer(void *buf) {
     g_prof = (long long *)buf;
     return 0;
@@ -987,9 +1054,8 @@ int wadg_fused_config(int dtype, int order, int32_t *info, int64_t *smem) {
     return fail("bad dtype");
 }
 
-int wadg_stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void *res, double tau_p,
-                     double tau_u, double a, double b, double dt, int block_begin, int block_end,
-                     void *stream) {
+static int stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void *res, double tau_p, double tau_u,
+                       double a, double b, double dt, int block_begin, int block_end, int lay, void *stream) {
     if (validate(P)) return 1;
     if (P->dim != 3 || P->formulation != WADG_STRONG_WEAK) return fail("fused stage: 3D strong-weak only");
     if (P->minv_p) return fail("fused stage: WADG mass inverse only (use wadg_stage for ExactCurvedMass)");
@@ -999,10 +1065,23 @@ int wadg_stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void *r
     cudaStream_t st = (cudaStream_t)stream;
     if (P->dtype == WADG_F64) {
         WADG_FUSED_SWITCH(double, P->order, fused_launch, P, Qin, Qout, res, tau_p, tau_u, a, b, dt,
-                          block_begin, block_end, st);
+                          block_begin, block_end, lay, st);
     }
     WADG_FUSED_SWITCH(float, P->order, fused_launch, P, Qin, Qout, res, tau_p, tau_u, a, b, dt,
-                      block_begin, block_end, st);
+                      block_begin, block_end, lay, st);
+}
+
+int wadg_stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void *res, double tau_p,
+                     double tau_u, double a, double b, double dt, int block_begin, int block_end,
+                     void *stream) {
+    return stage_fused(P, Qin, Qout, res, tau_p, tau_u, a, b, dt, block_begin, block_end, 0, stream);
+}
+
+int wadg_stage_fused_rows(const wadg_problem *P, const void *Qin, void *Qout, void *res, double tau_p,
+                          double tau_u, double a, double b, double dt, int block_begin, int block_end,
+                          int layout, void *stream) {
+    if (layout < 0 || layout > 2) return fail("layout must be 0, 1 or 2");
+    return stage_fused(P, Qin, Qout, res, tau_p, tau_u, a, b, dt, block_begin, block_end, layout, stream);
 }
 
 }  // extern "C"
@@ -1189,4 +1268,73 @@ extern "C" int wadg_debug_umma_test(const void *A, const void *B, void *C, int N
     wadg::k_umma_test<<<1, 128, smem, (cudaStream_t)stream>>>((const float *)A, (const float *)B, (float *)C, N, K,
                                                               mode);
     return check_launch("wadg_debug_umma_test");
+}
+
+// Debug / measurement: tcgen05.mma issue rate from one warp.  CTA of 128 threads;
+// warp 0 issues `count` MMAs (M=128, K=8, N=n) back to back on zeroed operands and
+// commits; returns clock64 cycles between the first issue and the commit completion.
+// mode 0: A from shared memory (SS) via the per-MMA elected wrapper; 1: A from TMEM
+// (TS); 2: SS with 8 MMAs per asm block under one elect (descriptor adds in PTX).
+namespace wadg {
+__global__ void __launch_bounds__(128) k_umma_rate(long long *out, int n, int count, int mode) {
+    using namespace umma;
+    extern __shared__ __align__(128) unsigned char sm[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(sm + 8);
+    float *sA = reinterpret_cast<float *>(sm + 1024);
+    float *sB = sA + 128 * 8;
+    for (int i = threadIdx.x; i < 128 * 8 + 256 * 8; i += 128) sA[i] = 0.f;
+    const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);
+    if (threadIdx.x == 0) fused::mbar_init(bar, 1);
+    if (warp == 0) tmem_alloc<512>(slot);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tm = *slot;
+    if (warp == 0) {
+        const uint32_t id = idesc_tf32(128, n);
+        const uint64_t da = desc_k(su32(sA), 128, 256), db = desc_k(su32(sB), 128, 256);
+        const long long t0 = clock64();
+        if (mode == 0) {
+            for (int i = 0; i < count; ++i) mma_ss_w(tm, da, db, id, i > 0);
+        } else if (mode == 1) {
+            for (int i = 0; i < count; ++i) mma_ts_w(tm, tm + 256, db, id, i > 0);
+        } else {
+            for (int i = 0; i < count; i += 8) {
+                asm volatile(
+                    "{\n\t.reg .pred e;\n\t.reg .b32 t;\n\t"
+                    "elect.sync t|e, 0xffffffff;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t"
+                    "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n\t}\n" ::"r"(tm),
+                    "l"(da), "l"(db), "r"(id)
+                    : "memory");
+            }
+        }
+        const long long t1 = clock64();
+        commit_w(bar);
+        mbar_wait_bounded(bar, 0);
+        const long long t2 = clock64();
+        if ((threadIdx.x & 31) == 0) {
+            out[0] = t1 - t0;
+            out[1] = t2 - t0;
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tm);
+}
+}  // namespace wadg
+
+extern "C" int wadg_debug_umma_rate(void *out, int n, int count, int mode, void *stream) {
+    const size_t smem = 1024 + (128 * 8 + 256 * 8) * 4;
+    cudaFuncSetAttribute(wadg::k_umma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    wadg::k_umma_rate<<<1, 128, smem, (cudaStream_t)stream>>>((long long *)out, n, count, mode);
+    return check_launch("wadg_debug_umma_rate");
 }

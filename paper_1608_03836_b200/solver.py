@@ -485,11 +485,183 @@ class DeviceStepper:
         return Q
 
 
+def pipeline_chunks(nblk, sms, wave_chunk=3):
+    """Chunk sizes (in fused blocks) for the host pipeline: whole waves of
+    ``sms`` blocks, ``wave_chunk`` waves in the middle and one wave at both
+    ends.  Small first chunks shorten the fill (stage 1 waits for the first
+    chunks to arrive) and small last chunks the drain (the last chunk's copy
+    back)."""
+    big = sms * wave_chunk
+    if nblk <= 4 * big:
+        cb = max(1, min(nblk, sms))
+        return [min(cb, nblk - b) for b in range(0, nblk, cb)]
+    head = [sms] * wave_chunk
+    tail = [sms] * wave_chunk
+    mid = nblk - sum(head) - sum(tail)
+    body = [big] * (mid // big)
+    rest = mid - sum(body)
+    if rest:
+        body.append(rest)
+    return head + body + tail
+
+
+def wavefront_schedule(lo, hi, n_stages=5):
+    """Launch order of (stage, chunk) pairs for a chunked multi-stage sweep on
+    one in-order stream.  Chunk c reads the chunks lo[c]..hi[c] of the
+    previous stage.  Stage s on c runs once stage s-1 has finished every chunk
+    c reads (read after write).  It must also wait for every chunk that reads
+    c, because it overwrites that stage's input buffer (write after read).
+    Among the ready pairs the highest stage goes first, so finished chunks
+    leave early."""
+    nc = len(lo)
+    reach = [max([hi[c]] + [c2 for c2 in range(nc) if lo[c2] <= c <= hi[c2]]) for c in range(nc)]
+    done = [nc] + [0] * n_stages              # chunks finished per stage (stage 0 = input)
+    order = []
+    while done[n_stages] < nc:
+        for s in range(n_stages, 0, -1):
+            c = done[s]
+            if c < nc and done[s - 1] > (reach[c] if s > 1 else -1):
+                order.append((s, c))
+                done[s] += 1
+                break
+    return order
+
+
+class HostPipeline:
+    """LSRK45 step on a host-resident state, pipelined over element chunks.
+
+    The state is split into chunks of whole fused-stage blocks (a multiple of
+    the SM count by default).  Three streams overlap the work:
+      * a copy stream moves chunk c host -> device and converts it to the field
+        layout (wadg_rows_to_fields);
+      * the current stream runs the five stage kernels on block ranges in a
+        wavefront order;
+      * a second copy stream converts each chunk back (wadg_fields_to_rows) and
+        copies it device -> host as soon as stage 5 has finished it.
+    Stage s of chunk c needs stage s-1 on every chunk that holds a face
+    neighbour of c.  The ping-pong buffer it writes is also read by stage s-1
+    of those chunks, so one in-order stream and that dependency suffice; the
+    neighbour chunk range comes from the nbr table.  Needs the fused stage,
+    one rank and pinned host tensors of the device dtype (FieldState layout,
+    (K, Np) per field).  The input is converted by wadg_rows_to_fields on the
+    copy stream.  With the tcgen05 stage the last stage writes the row layout
+    itself (wadg_stage_fused_rows); other kernels convert back with
+    wadg_fields_to_rows on the second copy stream."""
+
+    def __init__(self, disc, chunk_blocks=None, direct=True):
+        d = disc.dev
+        if d.fused is None:
+            raise ConfigError("host pipeline needs the fused stage kernel")
+        if d.halo is not None and d.halo.n_recv:
+            raise ConfigError("host pipeline is single-rank")
+        self.disc = disc
+        self.stepper = DeviceStepper(disc, fused=True)
+        eb = d.fused
+        assert d.Kpad % eb == 0
+        nblk = d.Kpad // eb
+        sms = torch.cuda.get_device_properties(d.device).multi_processor_count
+        if chunk_blocks is None:
+            chunk_blocks = pipeline_chunks(nblk, sms)
+        elif isinstance(chunk_blocks, int):
+            cb = max(1, min(chunk_blocks, nblk))
+            chunk_blocks = [min(cb, nblk - b) for b in range(0, nblk, cb)]
+        assert sum(chunk_blocks) == nblk and min(chunk_blocks) > 0
+        edges = np.concatenate([[0], np.cumsum(chunk_blocks)])
+        self.blocks = [(int(a), int(b)) for a, b in zip(edges[:-1], edges[1:])]
+        K = d.K
+        self.elems = [(min(b0 * eb, K), min(b1 * eb, K)) for b0, b1 in self.blocks]
+        nc = len(self.blocks)
+        # chunk range of the face neighbours of each chunk
+        nbr = d.nbr[:, :K].cpu().numpy()
+        owner = np.searchsorted(edges, np.arange(K) // eb, side="right") - 1
+        self.lo, self.hi = np.arange(nc), np.arange(nc)
+        for c, (k0, k1) in enumerate(self.elems):
+            nb = nbr[:, k0:k1]
+            nb = nb[nb >= 0]
+            if nb.size:
+                oc = owner[nb]
+                self.lo[c], self.hi[c] = min(c, int(oc.min())), max(c, int(oc.max()))
+        self.schedule = wavefront_schedule(self.lo, self.hi)
+        fld = d.fld
+        self.rows_in = torch.empty((fld, K, d.ref.Np), dtype=d.dtype, device=d.device)
+        self.rows_out = torch.empty_like(self.rows_in)
+        self.bufs = [d.empty_fields(), self.stepper.other]
+        # the tcgen05 stage writes the row layout itself in the last stage.  Reading
+        # it in the first stage works too (layout 1) but the neighbour gather from
+        # rows of Np values costs more than the conversion kernel
+        # (scripts/rows_stage_time.py), so the input is converted on the copy stream
+        self.direct = bool(direct) and getattr(d, "fused_kind", -1) == 2
+        self.h2d, self.d2h = torch.cuda.Stream(d.device), torch.cuda.Stream(d.device)
+        self.ev_in = [torch.cuda.Event() for _ in range(nc)]
+        self.ev_out = [torch.cuda.Event() for _ in range(nc)]
+
+    @staticmethod
+    def accepts(disc, state):
+        """Pinned host torch tensors of the device dtype, (K, Np) each, on a
+        single-rank fused discretization."""
+        d = disc.dev
+        if d.fused is None or d.halo is not None:
+            return False
+        return all(isinstance(a, torch.Tensor) and not a.is_cuda and a.is_pinned() and a.dtype == d.dtype
+                   and a.is_contiguous() and tuple(a.shape) == (d.K, d.ref.Np) for a in state.fields())
+
+    def step(self, state, dt):
+        import ctypes
+        disc, d = self.disc, self.disc.dev
+        fl = disc.flux
+        s = ctypes.byref(d.struct)
+        cur = torch.cuda.current_stream(d.device)
+        sp = lambda st: ctypes.c_void_p(st.cuda_stream)
+        host_in = state.fields()
+        out = torch.empty((d.fld, d.K, d.ref.Np), dtype=d.dtype, pin_memory=True)
+        self.h2d.wait_stream(cur)
+        self.d2h.wait_stream(cur)
+        direct = self.direct
+        with torch.cuda.stream(self.h2d):
+            for c, (k0, k1) in enumerate(self.elems):
+                for f in range(d.fld):
+                    self.rows_in[f, k0:k1].copy_(host_in[f][k0:k1], non_blocking=True)
+                _native.call("wadg_rows_to_fields", s, _vp(self.rows_in), k0, k1, _vp(self.bufs[0]), sp(self.h2d))
+                self.ev_in[c].record(self.h2d)
+        waited = -1
+        res = self.stepper.res
+        for st, c in self.schedule:
+            if st == 1 and self.hi[c] > waited:
+                waited = int(self.hi[c])
+                cur.wait_event(self.ev_in[waited])
+            b0, b1 = self.blocks[c]
+            qi, qo = self.bufs[(st - 1) % 2], self.bufs[st % 2]
+            if direct and st == 5:           # the last stage writes the row layout
+                _native.call("wadg_stage_fused_rows", s, _vp(qi), _vp(self.rows_out), _vp(res), fl.tau_p,
+                             fl.tau_u, LSRK4A[st - 1], LSRK4B[st - 1], dt, b0, b1, 2, sp(cur))
+            else:
+                _native.call("wadg_stage_fused", s, _vp(qi), _vp(qo), _vp(res), fl.tau_p, fl.tau_u,
+                             LSRK4A[st - 1], LSRK4B[st - 1], dt, b0, b1, sp(cur))
+            if st == 5:
+                self.ev_out[c].record(cur)
+        with torch.cuda.stream(self.d2h):
+            for c, (k0, k1) in enumerate(self.elems):
+                self.d2h.wait_event(self.ev_out[c])
+                if not direct:
+                    _native.call("wadg_fields_to_rows", s, _vp(self.bufs[1]), k0, k1, _vp(self.rows_out),
+                                 sp(self.d2h))
+                for f in range(d.fld):
+                    out[f, k0:k1].copy_(self.rows_out[f, k0:k1], non_blocking=True)
+        cur.wait_stream(self.h2d)
+        cur.wait_stream(self.d2h)
+        self.d2h.synchronize()
+        return FieldState.from_fields(list(out.unbind(0)), state.t + dt)
+
+
 def lsrk_step(state, dt, rhs_fn):
     """One five-stage low-storage RK4 step (R/.../solver.py:348-363)."""
     if isinstance(rhs_fn, _BoundRHS):
         disc = rhs_fn.disc
         _check_state(state, disc)
+        if HostPipeline.accepts(disc, state):
+            if getattr(disc, "_pipeline", None) is None:
+                disc._pipeline = HostPipeline(disc)
+            return disc._pipeline.step(state, dt)
         Q = disc.to_device(state)
         Q = DeviceStepper(disc).step(Q, dt)
         return disc.from_device(Q, state, state.t + dt)

@@ -1,0 +1,133 @@
+"""Pipelined host-state LSRK step (solver.HostPipeline): the wavefront launch
+order on CPU, and on the GPU bitwise agreement with the device-resident
+stepper (the same per-element arithmetic on block ranges)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1608_03836_b200 import meshgen, solver
+from paper_1608_03836_b200.solver import FieldState, Formulation, SolverConfig, wavefront_schedule
+
+
+def _simulate(order, lo, hi, n_stages=5):
+    """Replay an in-order launch list and check every read-after-write and
+    write-after-read dependency of the ping-pong sweep."""
+    nc = len(lo)
+    done = {}                                   # (stage, chunk) -> launch position
+    for pos, (s, c) in enumerate(order):
+        assert (s, c) not in done
+        if s > 1:
+            for c2 in range(lo[c], hi[c] + 1):  # inputs: stage s-1 of the chunks c reads
+                assert done.get((s - 1, c2), 10**9) < pos
+            for c2 in range(nc):                # overwritten input: readers of c at stage s-1
+                if lo[c2] <= c <= hi[c2]:
+                    assert done.get((s - 1, c2), 10**9) < pos
+        if s > 1:
+            assert done[(s - 1, c)] < pos
+        done[(s, c)] = pos
+    assert len(done) == n_stages * nc
+
+
+@pytest.mark.parametrize("nc,span", [(1, 0), (2, 1), (7, 1), (16, 1), (12, 2), (9, 3)])
+def test_wavefront_schedule_respects_dependencies(nc, span):
+    lo = [max(0, c - span) for c in range(nc)]
+    hi = [min(nc - 1, c + span) for c in range(nc)]
+    order = wavefront_schedule(lo, hi)
+    _simulate(order, lo, hi)
+    # stage 5 of chunk 0 finishes well before the sweep ends when there is room
+    if nc >= 8 and span == 1:
+        first5 = order.index((5, 0))
+        assert first5 < len(order) // 2
+
+
+def test_wavefront_schedule_irregular_ranges():
+    rng = np.random.default_rng(3)
+    nc = 10
+    lo = [max(0, c - int(rng.integers(0, 3))) for c in range(nc)]
+    hi = [min(nc - 1, c + int(rng.integers(0, 3))) for c in range(nc)]
+    _simulate(wavefront_schedule(lo, hi), lo, hi)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("direct", [True, False])
+@pytest.mark.parametrize("dtype,N", [("float32", 4), ("float32", 2), ("float64", 3)])
+def test_host_pipeline_bitwise_device_stepper(dtype, N, direct):
+    mesh = meshgen.warped_cube_tet_mesh(6, N)
+    c2 = lambda x, y, z: 1 + 0.5 * np.sin(2 * np.pi * x) * np.cos(2 * np.pi * z)
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype=dtype)
+    disc = solver.Discretization(mesh, cfg, solver.MediumField(c2))
+    d = disc.dev
+    assert d.fused is not None
+    g = torch.Generator().manual_seed(11)
+    tdt = d.dtype
+    host = [torch.randn((mesh.K, disc.ref.Np), generator=g, dtype=torch.float64).to(tdt).pin_memory()
+            for _ in range(4)]
+    st = FieldState.from_fields(host)
+    pipe = solver.HostPipeline(disc, chunk_blocks=2, direct=direct)
+    assert len(pipe.blocks) > 3
+    assert pipe.direct == (direct and dtype == "float32")
+    assert solver.HostPipeline.accepts(disc, st)
+    ref = solver.DeviceStepper(disc, fused=True)
+    Q = disc.to_device(st)
+    dt = 1e-3
+    a = st
+    for _ in range(3):
+        a = pipe.step(a, dt)
+        Q = ref.step(Q, dt)
+    b = disc.from_device(Q, st, 0.0)
+    for x, y in zip(a.fields(), b.fields()):
+        assert x.is_pinned()
+        assert torch.equal(x, y)
+    assert abs(a.t - 3 * dt) < 1e-15
+    # the public entry point routes pinned host states through the pipeline
+    c = solver.lsrk_step(st, dt, disc.rhs)
+    assert disc._pipeline is not pipe
+    assert getattr(disc, "_pipeline", None) is not None
+    Q1 = solver.DeviceStepper(disc, fused=True).step(disc.to_device(st), dt)
+    for x, y in zip(c.fields(), disc.from_device(Q1, st, 0.0).fields()):
+        assert torch.equal(x, y)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("layout", [1, 2])
+def test_stage_fused_rows_matches_field_layout(layout):
+    """wadg_stage_fused_rows with Q_in (1) or Q_out (2) in the FieldState row
+    layout is bitwise the field-layout stage; K is not a multiple of the
+    128-element tile, so the last tile is partly padding."""
+    import ctypes
+    from paper_1608_03836_b200 import _native
+    mesh = meshgen.warped_cube_tet_mesh(5, 3)
+    assert mesh.K % 128
+    disc = solver.Discretization(mesh, SolverConfig(N=3, formulation=Formulation.StrongWeak, dtype="float32"))
+    d = disc.dev
+    if getattr(d, "fused_kind", -1) != 2:
+        pytest.skip("row layouts need the tcgen05 stage")
+    K, Np = d.K, disc.ref.Np
+    g = torch.Generator(device="cuda").manual_seed(5)
+    rows = torch.randn((4, K, Np), generator=g, device="cuda")
+    Q = d.empty_fields()
+    Q[:, :, :K] = rows.transpose(1, 2)
+    res0 = torch.randn(d.empty_fields().shape, generator=g, device="cuda")
+    res0[:, :, K:] = 0
+    s = ctypes.byref(d.struct)
+    vp = lambda t: ctypes.c_void_p(t.data_ptr())
+    sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    fl = disc.flux
+    ra, rb = res0.clone(), res0.clone()
+    out_a = d.empty_fields()
+    _native.call("wadg_stage_fused", s, vp(Q), vp(out_a), vp(ra), fl.tau_p, fl.tau_u, 0.3, 0.7, 1e-3, 0, -1, sp)
+    if layout == 1:
+        out_b = d.empty_fields()
+        _native.call("wadg_stage_fused_rows", s, vp(rows), vp(out_b), vp(rb), fl.tau_p, fl.tau_u, 0.3, 0.7, 1e-3,
+                     0, -1, 1, sp)
+        assert torch.equal(out_a[:, :, :K], out_b[:, :, :K])
+    else:
+        out_b = torch.full((4, K, Np), float("nan"), device="cuda")
+        _native.call("wadg_stage_fused_rows", s, vp(Q), vp(out_b), vp(rb), fl.tau_p, fl.tau_u, 0.3, 0.7, 1e-3,
+                     0, -1, 2, sp)
+        assert torch.equal(out_a[:, :, :K].transpose(1, 2), out_b)
+    assert torch.equal(ra[:, :, :K], rb[:, :, :K])
+    with pytest.raises(_native.NativeError):
+        _native.call("wadg_stage_fused_rows", s, vp(Q), vp(out_a), vp(rb), fl.tau_p, fl.tau_u, 0.3, 0.7, 1e-3,
+                     0, -1, 3, sp)
