@@ -40,6 +40,11 @@ namespace uk {
 // debug: fine-grained clocks of the tcgen05 stage (slots 8..31 of a 32-slot
 // per-CTA record in P.prof; phase marks use WADG_PROF_MARK as elsewhere)
 #define UMMA_MARK0(slot) UMMA_MARK(slot, threadIdx.x == 0)
+#ifdef WADG_MMA_TRACE   // debug build only: MMA-warp timeline marks in slots 6..29
+#define MMA_TRACE(slot) UMMA_MARK(slot, threadIdx.x == 16 * 32)
+#else
+#define MMA_TRACE(slot) do { } while (0)
+#endif
 #define UMMA_MARK(slot, cond)                                                                  \
     do {                                                                                       \
         if (P.prof && (cond)) P.prof[(size_t)blockIdx.x * 32 + (slot)] = clock64();            \
@@ -233,6 +238,11 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     const size_t blk = (size_t)(block0 + blockIdx.x);
     const size_t kblk = blk * ME;
     UMMA_MARK0(0);
+    if (P.prof && threadIdx.x == 0) {   // debug: SM id (slot 30), for per-SM gap analysis
+        uint32_t smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        P.prof[(size_t)blockIdx.x * 32 + 30] = smid;
+    }
 
     if (tid == 0) {
         for (int i = 0; i < 8; ++i) fused::mbar_init(&bar[i], 1);
@@ -416,8 +426,13 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         commit_w(&bar[7]);
         for (int ch = 0; ch < NCH; ++ch) {
             const bool more = ch + 1 < NCH;
+            const int tb = (ch == 2 || ch == 3) ? 6 + 8 * (ch - 2) : -1;
+#define VTR(k) do { if (tb >= 0) MMA_TRACE(tb + (k)); } while (0)
+            VTR(0);
             from_epilogue(B_P);              // gp(ch) in TMEM, dp(ch) consumed
+            VTR(1);
             op_wait(C::SL_PQ);
+            VTR(2);
             issue_v2p(ch);
             commit_w(&bar_v2[0]);
             if (more) {
@@ -425,8 +440,11 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 issue_v1p(ch + 1);
             }
             commit_w(&bar[0]);
+            VTR(3);
             from_epilogue(B_U);              // F(ch) in TMEM, U(ch) consumed
+            VTR(4);
             op_wait(C::SL_DTW);
+            VTR(5);
             issue_v2u(ch);
             commit_w(&bar_v2[1]);
             if (more && (ch & 1)) {          // next chunk pair (ch + 1, ch + 2)
@@ -437,11 +455,14 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             // refills: the -Pq / D_a(ch) tiles are free once V2p(ch) (issued after V1p(ch))
             // is done, the DTW / Vq(ch) tiles once V2u(ch) is
             wait_k(&bar_v2[0], ++nv2p);
+            VTR(6);
             if (more) op_load(C::SL_PQ, sPq, ops + C::O_PQ + (size_t)(ch + 1) * C::OPPQ, C::OPPQ * 4);
             if (ch + 2 < NCH)
                 op_load(C::SL_DA + (ch & 1), sDa + (ch & 1) * C::OPDA, ops + C::O_DA + (size_t)(ch + 2) * C::OPDA,
                         C::OPDA * 4);
             wait_k(&bar_v2[1], ++nv2u);
+            VTR(7);
+#undef VTR
             if (more) op_load(C::SL_DTW, sDTW, ops + C::O_DTW + (size_t)(ch + 1) * C::OPDTW, C::OPDTW * 4);
             if (!(ch & 1) && ch + 2 < NCH)   // pair ch/2 consumed (V1u issued before V2u(ch)): next pair
                 op_load(C::SL_VQ, sVq, ops + C::O_VQ + (size_t)(ch / 2 + 1) * C::OPVQ, C::OPVQ * 4);
@@ -470,8 +491,12 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         };
         for (int step = 0; step < NSTEP; ++step) {
             const int hh = step % NFH;
+            if (step == 3) MMA_TRACE(22);
+            if (step == 4) MMA_TRACE(28);
             if (hh == 0) from_epilogue(B_S0);   // this face's own / exterior nodes written
+            if (step == 4) MMA_TRACE(29);
             if (step > 0) from_epilogue(B_S2);  // traces(step-1) read out of TMEM
+            if (step == 3) MMA_TRACE(23);
             const uint32_t vih = su32(sVfi + hh * C::OPVFI), vil = vih + C::OPVFI * 2;
             const uint32_t id = idesc_tf32(128, 16);
 #pragma unroll 1
@@ -492,13 +517,17 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     }
             }
             commit_w(&bar[0]);
+            if (step == 3) MMA_TRACE(24);
             if (step >= 2) {                 // lift(step-2) done: its -Pf buffer takes step
                 wait_k(&bar[7], ++nB, 4000 + step);
                 op_load(step & 1, sPf(step & 1), ops + C::O_PF + (size_t)step * C::OPPF, C::OPPF * 4);
             }
+            if (step == 3) MMA_TRACE(25);
             if (step > 0) {
                 from_epilogue(B_S1);         // flux of step-1 written
+                if (step == 3) MMA_TRACE(26);
                 issue_lift(step - 1);
+                if (step == 3) MMA_TRACE(27);
             }
         }
         // An mbarrier parity wait is only unambiguous while at most one completion is

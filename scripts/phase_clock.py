@@ -61,6 +61,21 @@ def main():
     out = {"K": mesh.K, "N": args.order, "dtype": args.dtype, "elems_per_block": kb,
            "cycles_per_cta_median": float(tot),
            "phases": {p: {"cycles": float(c), "share": float(c / tot)} for p, c in zip(phases, med)}}
+    if d.fused_kind == 2:          # per-SM occupancy: gaps between consecutive CTAs on one SM
+        raw = buf.view(nblk, stride).cpu().numpy()
+        t0, t1, sm = raw[:, 0].astype(np.float64), raw[:, 5].astype(np.float64), raw[:, 30]
+        gaps, busy, span = [], 0.0, 0.0
+        for s_ in np.unique(sm):
+            i = np.where(sm == s_)[0]
+            i = i[np.argsort(t0[i])]
+            gaps += list(t0[i][1:] - t1[i][:-1])
+            busy += float(np.sum(t1[i] - t0[i]))
+            span += float(t1[i][-1] - t0[i][0])
+        out["inter_cta_gap_cycles_median"] = float(np.median(gaps)) if gaps else None
+        out["inter_cta_gap_cycles_p90"] = float(np.percentile(gaps, 90)) if gaps else None
+        out["sm_busy_fraction"] = busy / span
+        out["ctas_per_sm"] = nblk / len(np.unique(sm))
+        out["cta_cycles_mean"] = float(np.mean(t1 - t0))
     print(json.dumps(out))
 
 
