@@ -1105,10 +1105,32 @@ __global__ void __launch_bounds__(256) k_fma_peak(const T *__restrict__ in, T *_
     for (int i = 0; i < 16; ++i) s += a[i];
     if (s == (T)12345.678) out[threadIdx.x] = s;
 }
+// packed fp32 (FFMA2): 16 independent float2 chains, 4 flops per chain per iteration
+__global__ void __launch_bounds__(256) k_ffma2_peak(const float *__restrict__ in, float *__restrict__ out, int iters) {
+    float2 a[16];
+    const float2 b = make_float2(in[threadIdx.x & 7], in[(threadIdx.x + 1) & 7]);
+    const float2 c = make_float2(in[8 + (threadIdx.x & 7)], in[8 + ((threadIdx.x + 3) & 7)]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = make_float2(in[16 + i] + threadIdx.x, in[32 + i] - threadIdx.x);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) a[i] = __ffma2_rn(a[i], b, c);
+    }
+    float s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+    if (s == 12345.678f) out[threadIdx.x] = s;
+}
 }  // namespace wadg
 
+// dtype WADG_F64 / WADG_F32 (FFMA / DFMA, 2 * 16 * iters flops per thread) or 2 =
+// packed fp32 FFMA2 (4 * 16 * iters flops per thread)
 extern "C" int wadg_microbench_fma(int dtype, int blocks, int iters, const void *in, void *out, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == 2) {
+        wadg::k_ffma2_peak<<<blocks, 256, 0, st>>>((const float *)in, (float *)out, iters);
+        return check_launch("wadg_microbench_fma");
+    }
     if (dtype == WADG_F64)
         wadg::k_fma_peak<double><<<blocks, 256, 0, st>>>((const double *)in, (double *)out, iters);
     else

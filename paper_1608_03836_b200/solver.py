@@ -469,12 +469,24 @@ class DeviceStepper:
         import ctypes
         d = self.disc.dev
         fl = self.disc.flux
+        exch = getattr(self.disc, "exchange", None)      # slab of a multi-rank run (parallel.py)
+        if exch is not None:
+            exch.start(Q)                                # pack + post this stage's halo traces
         if self.fused:
             out = self.other
-            _native.call("wadg_stage_fused", ctypes.byref(d.struct), _vp(Q), _vp(out), _vp(self.res),
-                         fl.tau_p, fl.tau_u, a, b, dt, 0, -1, _stream())
+            if exch is not None:
+                exch.fused_stage(Q, out, self.res, fl.tau_p, fl.tau_u, a, b, dt, _stream())
+            else:
+                _native.call("wadg_stage_fused", ctypes.byref(d.struct), _vp(Q), _vp(out), _vp(self.res),
+                             fl.tau_p, fl.tau_u, a, b, dt, 0, -1, _stream())
             self.other = Q
             return out
+        if exch is not None:
+            _native.call("wadg_volume", ctypes.byref(d.struct), _vp(Q), _vp(self.rhs), _stream())
+            exch.surface(Q, self.rhs, fl.tau_p, fl.tau_u, _stream())
+            _native.call("wadg_update_lsrk", ctypes.byref(d.struct), _vp(self.rhs), _vp(self.res), _vp(Q),
+                         a, b, dt, _stream())
+            return Q
         _native.call("wadg_stage", ctypes.byref(d.struct), _vp(Q), _vp(self.res), _vp(self.rhs),
                      fl.tau_p, fl.tau_u, a, b, dt, _stream())
         return Q
@@ -600,7 +612,7 @@ class HostPipeline:
         """Pinned host torch tensors of the device dtype, (K, Np) each, on a
         single-rank fused discretization."""
         d = disc.dev
-        if d.fused is None or d.halo is not None:
+        if d.fused is None or d.halo is not None or getattr(disc, "exchange", None) is not None:
             return False
         return all(isinstance(a, torch.Tensor) and not a.is_cuda and a.is_pinned() and a.dtype == d.dtype
                    and a.is_contiguous() and tuple(a.shape) == (d.K, d.ref.Np) for a in state.fields())

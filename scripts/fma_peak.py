@@ -16,7 +16,7 @@ __graft_entry__.build()
 from paper_1608_03836_b200 import _native  # noqa: E402
 
 
-def measure(dtype_code, torch_dtype, iters=20000, blocks=148 * 8):
+def measure(dtype_code, torch_dtype, iters=20000, blocks=148 * 8, flops_per_fma=2.0):
     inp = torch.rand(64, dtype=torch_dtype, device="cuda")
     out = torch.empty(256, dtype=torch_dtype, device="cuda")
     sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -29,11 +29,12 @@ def measure(dtype_code, torch_dtype, iters=20000, blocks=148 * 8):
     e1.record()
     torch.cuda.synchronize()
     s = e0.elapsed_time(e1) * 1e-3
-    return 2.0 * 16 * iters * 256 * blocks / s / 1e12
+    return flops_per_fma * 16 * iters * 256 * blocks / s / 1e12
 
 
 if __name__ == "__main__":
     print(json.dumps({"fp32_fma_tflops": measure(_native.WADG_F32, torch.float32),
+                      "fp32_ffma2_tflops": measure(2, torch.float32, flops_per_fma=4.0),
                       "fp64_fma_tflops": measure(_native.WADG_F64, torch.float64)}))
 
 

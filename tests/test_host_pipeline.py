@@ -131,3 +131,52 @@ def test_stage_fused_rows_matches_field_layout(layout):
     with pytest.raises(_native.NativeError):
         _native.call("wadg_stage_fused_rows", s, vp(Q), vp(out_a), vp(rb), fl.tau_p, fl.tau_u, 0.3, 0.7, 1e-3,
                      0, -1, 3, sp)
+
+
+class _RecordingExchange:
+    """Stands in for parallel.HaloExchange on a single domain (no halo
+    slots): records the calls DeviceStepper makes and runs the full range."""
+
+    def __init__(self, disc):
+        self.disc, self.calls = disc, []
+
+    def start(self, Q):
+        self.calls.append("start")
+
+    def fused_stage(self, Qin, Qout, res, tau_p, tau_u, a, b, dt, sp):
+        import ctypes
+        from paper_1608_03836_b200 import _native
+        self.calls.append("fused")
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())
+        _native.call("wadg_stage_fused", ctypes.byref(self.disc.dev.struct), vp(Qin), vp(Qout), vp(res),
+                     tau_p, tau_u, a, b, dt, 0, -1, sp)
+
+    def surface(self, Q, rhs, tau_p, tau_u, sp):
+        import ctypes
+        from paper_1608_03836_b200 import _native
+        self.calls.append("surface")
+        vp = lambda t: ctypes.c_void_p(t.data_ptr())
+        _native.call("wadg_surface", ctypes.byref(self.disc.dev.struct), vp(Q), vp(rhs), tau_p, tau_u,
+                     1, 0, -1, sp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fused", [True, False])
+def test_device_stepper_routes_stages_through_the_slab_exchange(fused):
+    """A slab discretization (disc.exchange set by parallel.slab_discretization)
+    must post its halo every stage: DeviceStepper, and so lsrk_step on a slab,
+    goes through exchange.start + exchange.fused_stage / surface, with results
+    identical to the single-domain stage."""
+    mesh = meshgen.warped_cube_tet_mesh(4, 3)
+    cfg = SolverConfig(N=3, formulation=Formulation.StrongWeak, dtype="float32")
+    disc = solver.Discretization(mesh, cfg)
+    g = torch.Generator().manual_seed(2)
+    st = FieldState.from_fields([torch.randn((mesh.K, disc.ref.Np), generator=g) for _ in range(4)])
+    Q0 = disc.to_device(st)
+    want = solver.DeviceStepper(disc, fused=fused).step(Q0.clone(), 1e-3)
+    disc.exchange = _RecordingExchange(disc)
+    got = solver.DeviceStepper(disc, fused=fused).step(Q0.clone(), 1e-3)
+    assert torch.equal(got[:, :, :mesh.K], want[:, :, :mesh.K])
+    assert disc.exchange.calls == ["start", "fused" if fused else "surface"] * 5
+    pinned = FieldState.from_fields([a.pin_memory() for a in st.fields()])
+    assert not solver.HostPipeline.accepts(disc, pinned)      # slabs step through the exchange
