@@ -977,17 +977,35 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         // res = a res + dt Minv(rhs); Q_out = Q_in + b res   (field c = sub)
         {
             const int c = sub;
+            // 16 nodes per pass: the old res values are all loaded before the first
+            // store (one load latency per pass instead of one per node)
 #pragma unroll
-            for (int j0 = 0; j0 < NPK; j0 += 8) {
-                float v[8];
-                ld8(tl + RACC + NPN * c + j0, v);
+            for (int h0 = 0; h0 < NPK; h0 += 16) {
+                float rv[16], v[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int j = h0 + i;
+                    rv[i] = (a_rk != 0.f && j < NP) ? __ldg(res + (size_t)(c * NP + j) * S + kblk + e) : 0.f;
+                }
+                {
+                    float v8[8];
+                    ld8(tl + RACC + NPN * c + h0, v8);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = v8[i];
+                }
+                if (h0 + 8 < NPK) {
+                    float v8[8];
+                    ld8(tl + RACC + NPN * c + h0 + 8, v8);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[8 + i] = v8[i];
+                }
                 wait_ld();
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int j = j0 + i;
+                for (int i = 0; i < 16; ++i) {
+                    const int j = h0 + i;
                     if (j < NP) {
                         const size_t o = (size_t)(c * NP + j) * S + kblk + e;
-                        const float r = (a_rk == 0.f) ? dt * v[i] : a_rk * res[o] + dt * v[i];
+                        const float r = (a_rk == 0.f) ? dt * v[i] : a_rk * rv[i] + dt * v[i];
                         res[o] = r;
                         const uint32_t so = c * ME * NPK + kmaj_off<NPK>(e, j) / 4;
                         const float q = sQ[so] + b_rk * r;
