@@ -664,21 +664,25 @@ WADG_KUNROLL
         if (tile < C::TILES_B) {
             const int e0 = (tile % C::EG2) * TE2, j0 = (tile / C::EG2) * TJ;
 #pragma unroll
-            for (int c = 0; c < FLD; ++c)
+            for (int c = 0; c < FLD; ++c) {
+                // the field's old res values are all loaded before its first store
+                T rold[TJ][TE2];
+#pragma unroll
+                for (int u = 0; u < TJ; ++u) {
+                    const int j = j0 + u;
+#pragma unroll
+                    for (int t = 0; t < TE2; ++t)
+                        rold[u][t] = (a_rk != T(0) && j < NP) ? __ldg(res + (size_t)(c * NP + j) * S + kblk + e0 + t)
+                                                             : T(0);
+                }
 #pragma unroll
                 for (int u = 0; u < TJ; ++u) {
                     const int j = j0 + u;
                     if (j < NP) {
                         const size_t o = (size_t)(c * NP + j) * S + kblk + e0;
                         T r[TE2], q[TE2], qi[TE2];
-                        if (a_rk == T(0)) {
 #pragma unroll
-                            for (int t = 0; t < TE2; ++t) r[t] = dt * acc[sl][c][t][u];
-                        } else {
-                            ldv<T, TE2>(r, res + o);
-#pragma unroll
-                            for (int t = 0; t < TE2; ++t) r[t] = a_rk * r[t] + dt * acc[sl][c][t][u];
-                        }
+                        for (int t = 0; t < TE2; ++t) r[t] = a_rk * rold[u][t] + dt * acc[sl][c][t][u];
                         ldv<T, TE2>(qi, sQ + (c * NPP + j) * KB + e0);
 #pragma unroll
                         for (int t = 0; t < TE2; ++t) q[t] = qi[t] + b_rk * r[t];
@@ -686,6 +690,7 @@ WADG_KUNROLL
                         stv<T, TE2>(Qout + o, q);
                     }
                 }
+            }
         }
     }
     __syncthreads();
