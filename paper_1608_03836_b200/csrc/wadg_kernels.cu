@@ -377,20 +377,37 @@ k_update(const Prob<T> P, const T *__restrict__ rhs, T *__restrict__ out, T *__r
         }
         __syncthreads();
     }
+    if (MODE == 0) {
+#pragma unroll
+        for (int r = 0; r < RJ; ++r) {
+            const int j = g + r * NG;
+            if (j < Np) {
+#pragma unroll
+                for (int c = 0; c < FLD; ++c) out[(size_t)(c * Np + j) * S + k] = acc[c][r];
+            }
+        }
+        return;
+    }
+    // LSRK: the old res / Q values of one node row (all fields) are loaded
+    // before its stores (the stores could alias the loads, so the compiler
+    // would otherwise serialise one load-store round trip per value)
 #pragma unroll
     for (int r = 0; r < RJ; ++r) {
         const int j = g + r * NG;
         if (j < Np) {
+            T ro[FLD], qo[FLD];
 #pragma unroll
             for (int c = 0; c < FLD; ++c) {
                 const size_t o = (size_t)(c * Np + j) * S + k;
-                if (MODE == 0) {
-                    out[o] = acc[c][r];
-                } else {
-                    const T rr = (a == T(0)) ? dt * acc[c][r] : a * out[o] + dt * acc[c][r];
-                    out[o] = rr;
-                    Qo[o] = Qo[o] + b * rr;
-                }
+                ro[c] = (a != T(0)) ? out[o] : T(0);
+                qo[c] = Qo[o];
+            }
+#pragma unroll
+            for (int c = 0; c < FLD; ++c) {
+                const size_t o = (size_t)(c * Np + j) * S + k;
+                const T rr = a * ro[c] + dt * acc[c][r];
+                out[o] = rr;
+                Qo[o] = qo[c] + b * rr;
             }
         }
     }
