@@ -517,6 +517,25 @@ def pipeline_chunks(nblk, sms, wave_chunk=3):
     return head + body + tail
 
 
+def chunk_neighbour_ranges(nbr, blocks, eb):
+    """For element chunks given as fused-block ranges ``blocks`` (eb elements
+    per block), the lowest and highest chunk holding a face neighbour of each
+    chunk, itself included.  ``nbr`` is the (Nf, K) neighbour table (< 0 =
+    boundary or halo)."""
+    K = nbr.shape[1]
+    edges = np.array([b0 for b0, _ in blocks] + [blocks[-1][1]])
+    owner = np.searchsorted(edges, np.arange(K) // eb, side="right") - 1
+    nc = len(blocks)
+    lo, hi = np.arange(nc), np.arange(nc)
+    for c, (b0, b1) in enumerate(blocks):
+        nb = nbr[:, min(b0 * eb, K):min(b1 * eb, K)]
+        nb = nb[nb >= 0]
+        if nb.size:
+            oc = owner[nb]
+            lo[c], hi[c] = min(c, int(oc.min())), max(c, int(oc.max()))
+    return lo, hi
+
+
 def wavefront_schedule(lo, hi, n_stages=5):
     """Launch order of (stage, chunk) pairs for a chunked multi-stage sweep on
     one in-order stream.  Chunk c reads the chunks lo[c]..hi[c] of the
@@ -583,16 +602,7 @@ class HostPipeline:
         K = d.K
         self.elems = [(min(b0 * eb, K), min(b1 * eb, K)) for b0, b1 in self.blocks]
         nc = len(self.blocks)
-        # chunk range of the face neighbours of each chunk
-        nbr = d.nbr[:, :K].cpu().numpy()
-        owner = np.searchsorted(edges, np.arange(K) // eb, side="right") - 1
-        self.lo, self.hi = np.arange(nc), np.arange(nc)
-        for c, (k0, k1) in enumerate(self.elems):
-            nb = nbr[:, k0:k1]
-            nb = nb[nb >= 0]
-            if nb.size:
-                oc = owner[nb]
-                self.lo[c], self.hi[c] = min(c, int(oc.min())), max(c, int(oc.max()))
+        self.lo, self.hi = chunk_neighbour_ranges(d.nbr[:, :K].cpu().numpy(), self.blocks, eb)
         self.schedule = wavefront_schedule(self.lo, self.hi)
         fld = d.fld
         self.rows_in = torch.empty((fld, K, d.ref.Np), dtype=d.dtype, device=d.device)

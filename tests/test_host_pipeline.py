@@ -7,7 +7,8 @@ import pytest
 import torch
 
 from paper_1608_03836_b200 import meshgen, solver
-from paper_1608_03836_b200.solver import FieldState, Formulation, SolverConfig, wavefront_schedule
+from paper_1608_03836_b200.solver import (FieldState, Formulation, SolverConfig, chunk_neighbour_ranges,
+                                          pipeline_chunks, wavefront_schedule)
 
 
 def _simulate(order, lo, hi, n_stages=5):
@@ -47,6 +48,39 @@ def test_wavefront_schedule_irregular_ranges():
     lo = [max(0, c - int(rng.integers(0, 3))) for c in range(nc)]
     hi = [min(nc - 1, c + int(rng.integers(0, 3))) for c in range(nc)]
     _simulate(wavefront_schedule(lo, hi), lo, hi)
+
+
+@pytest.mark.parametrize("n,nblk_chunk", [(8, 2), (8, 5), (12, 7)])
+def test_schedule_on_type_ordered_warped_cube(n, nblk_chunk):
+    """The pipeline's chunk neighbour ranges on a real z-ordered tet mesh:
+    neighbours reach at most one z layer, and the wavefront order over the
+    chunks respects every dependency of the ping-pong sweep."""
+    from paper_1608_03836_b200 import device, refelem
+    mesh = meshgen.warped_cube_tet_mesh(n, 1)
+    n_or = len(refelem.orientation_permutations(mesh.shape))
+    nbr, _ = device.neighbour_tables(mesh, n_or)
+    eb = 128
+    nblk = -(-mesh.K // eb)
+    blocks = [(b, min(b + nblk_chunk, nblk)) for b in range(0, nblk, nblk_chunk)]
+    lo, hi = chunk_neighbour_ranges(nbr, blocks, eb)
+    layer_blocks = 6 * n * n / eb                        # one z layer of the type-ordered mesh
+    span = int(np.ceil(layer_blocks / nblk_chunk)) + 1
+    assert all(0 <= c - lo[c] <= span and 0 <= hi[c] - c <= span for c in range(len(blocks)))
+    # a neighbour outside [lo, hi] would break the schedule: check against the table
+    owner = np.minimum(np.arange(mesh.K) // (eb * nblk_chunk), len(blocks) - 1)
+    for f in range(4):
+        m = nbr[f] >= 0
+        oc, ok = owner[nbr[f][m]], owner[np.arange(mesh.K)[m]]
+        assert np.all(lo[ok] <= oc) and np.all(oc <= hi[ok])
+    _simulate(wavefront_schedule(lo, hi), lo, hi)
+
+
+def test_pipeline_chunks_cover_whole_waves():
+    for nblk, sms in [(12288, 148), (1536, 148), (100, 148), (5000, 132)]:
+        c = pipeline_chunks(nblk, sms)
+        assert sum(c) == nblk and min(c) > 0
+        # whole waves everywhere except one chunk that takes the remainder
+        assert sum(1 for x in c if x % sms) <= 1
 
 
 @pytest.mark.gpu
