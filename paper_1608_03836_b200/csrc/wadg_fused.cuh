@@ -53,9 +53,9 @@ struct Cfg {
     static constexpr int NFQ = (N + 1) * (N + 1);
     static constexpr int NF = 4, FLD = 4;
     static constexpr int KB = F32 ? (N <= 5 ? 64 : 32) : (N == 1 ? 64 : (N <= 5 ? 32 : 16));
-    static constexpr int QC0 = F32 ? (N <= 4 ? 64 : 32) : (N <= 3 ? 64 : (N <= 5 ? 32 : 16));
+    static constexpr int QC0 = F32 ? (N <= 4 ? 64 : 32) : (N <= 2 ? 64 : (N <= 5 ? 32 : 16));
     static constexpr int QC = QC0 < rup(NQ, 8) ? QC0 : rup(NQ, 8);   // never wider than Nq
-    static constexpr int MINB = N == 1 ? 3 : ((!F32 && N == 2) ? 2 : 1);   // low order: several CTAs / SM
+    static constexpr int MINB = N == 1 ? 3 : ((!F32 && (N == 2 || N == 3)) ? 2 : 1);   // low order: several CTAs / SM
     static constexpr int NCH = cdiv(NQ, QC);
     // phase A (interp-to-quadrature GEMMs): TE elements x TQ quad points
     // low orders use 1-element tiles so that every phase keeps most of the 256
