@@ -52,27 +52,27 @@ struct Cfg {
     static constexpr int NFP = nfp_tri(N);
     static constexpr int NFQ = (N + 1) * (N + 1);
     static constexpr int NF = 4, FLD = 4;
-    static constexpr int KB = F32 ? (N <= 5 ? 64 : 32) : (N == 1 ? 64 : (N <= 5 ? 32 : 16));
+    static constexpr int KB = F32 ? (N <= 4 ? 64 : 32) : (N == 1 ? 64 : (N <= 5 ? 32 : 16));
     static constexpr int QC0 = F32 ? (N <= 4 ? 64 : 32) : (N <= 2 ? 64 : (N <= 5 ? 32 : 16));
     static constexpr int QC = QC0 < rup(NQ, 8) ? QC0 : rup(NQ, 8);   // never wider than Nq
-    static constexpr int MINB = N == 1 ? 3 : ((!F32 && (N == 2 || N == 3)) ? 2 : 1);   // low order: several CTAs / SM
+    static constexpr int MINB = N == 1 ? 3 : (((!F32 && (N == 2 || N == 3)) || (F32 && N == 5)) ? 2 : 1);   // low order: several CTAs / SM
     static constexpr int NCH = cdiv(NQ, QC);
     // phase A (interp-to-quadrature GEMMs): TE elements x TQ quad points
     // low orders use 1-element tiles so that every phase keeps most of the 256
     // threads busy (at N = 1 a CTA has only 64 x 4 nodes / quadrature points)
-    static constexpr int TE = N == 1 ? 1 : (F32 ? (QC == 64 ? 4 : 2) : 2);
+    static constexpr int TE = (N == 1 || (F32 && N == 5)) ? 1 : (F32 ? (QC == 64 ? 4 : 2) : 2);
     static constexpr int TQ = N == 1 ? 2 : (F32 ? 4 : (QC == 64 ? 4 : (QC == 32 ? 2 : 1)));
     static constexpr int TILES_A = (KB / TE) * (QC / TQ);
     // phase B (projection GEMMs): TE2 elements x TJ nodes, all 4 fields
     // (TE2, TJ) chosen per order so that most of the 256 threads own a tile
-    static constexpr int TE2 = N == 1 ? 1 : (F32 ? ((N == 2 || N == 3) ? 2 : 4) : (N == 2 ? 1 : 2));
+    static constexpr int TE2 = N == 1 ? 1 : (F32 ? ((N == 2 || N == 3 || N == 5) ? 2 : 4) : (N == 2 ? 1 : 2));
     static constexpr int TJ = N == 1 ? 1 : ((N == 4 || N == 6) ? 3 : ((N == 2 || (!F32 && N == 3)) ? 2 : 4));
     static constexpr int EG2 = KB / TE2;
     static constexpr int TILES_B = EG2 * (NPP / TJ);
     static constexpr int SLOTS = cdiv(TILES_B, NTF);
     // face-trace interpolation tiles: TFQ face points x TEF elements
     static constexpr int TFQ = N == 1 ? 1 : 2;
-    static constexpr int TEF = N == 1 ? 1 : (F32 ? 4 : ((N == 2 || N == 3) ? 1 : 2));
+    static constexpr int TEF = N == 1 ? 1 : (F32 ? (N == 5 ? 2 : 4) : ((N == 2 || N == 3) ? 1 : 2));
     static constexpr int NFQP = rup(NFQ, TFQ);
     static constexpr int TILES_F = (KB / TEF) * (NFQP / TFQ);
     static constexpr int SLOTS_F = cdiv(TILES_F, NTF);
