@@ -214,3 +214,28 @@ def test_device_stepper_routes_stages_through_the_slab_exchange(fused):
     assert disc.exchange.calls == ["start", "fused" if fused else "surface"] * 5
     pinned = FieldState.from_fields([a.pin_memory() for a in st.fields()])
     assert not solver.HostPipeline.accepts(disc, pinned)      # slabs step through the exchange
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["tet_fused_f64", "tet_fused_f32", "tri_split_f64"])
+def test_graphed_steps_bitwise_eager(case):
+    """DeviceStepper.step_graphed (captured CUDA graph, replayed) gives the
+    eager step's result bit for bit, across the ping-pong buffer alternation."""
+    if case.startswith("tet"):
+        mesh, N = meshgen.warped_cube_tet_mesh(3, 3), 3
+    else:
+        mesh, N = meshgen.warped_triangle_mesh(4, 3), 3
+    dtype = "float32" if case.endswith("f32") else "float64"
+    disc = solver.Discretization(mesh, SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype=dtype))
+    g = torch.Generator().manual_seed(4)
+    st = FieldState.from_fields([torch.randn((mesh.K, disc.ref.Np), generator=g, dtype=torch.float64)
+                                 for _ in range(mesh.dim + 1)])
+    a, b = solver.DeviceStepper(disc), solver.DeviceStepper(disc)
+    Qa, Qb = disc.to_device(st), disc.to_device(st)
+    Qa = a.step(Qa, 1e-3)                  # warm the kernels before any capture
+    Qb = b.step(Qb, 1e-3)
+    for _ in range(4):
+        Qa = a.step(Qa, 1e-3)
+        Qb = b.step_graphed(Qb, 1e-3)
+    torch.cuda.synchronize()
+    assert torch.equal(Qa[:, :, :mesh.K], Qb[:, :, :mesh.K])
