@@ -588,8 +588,9 @@ class HostPipeline:
 
     The state is split into chunks of whole fused-stage blocks (a multiple of
     the SM count by default).  Three streams overlap the work:
-      * a copy stream moves chunk c host -> device and converts it to the field
-        layout (wadg_rows_to_fields);
+      * a copy stream moves chunk c host -> device, and a conversion stream
+        turns it into the field layout (wadg_rows_to_fields) once it lands, so
+        the copy engine never waits behind a kernel;
       * the current stream runs the five stage kernels on block ranges in a
         wavefront order;
       * a second copy stream converts each chunk back (wadg_fields_to_rows) and
@@ -638,7 +639,11 @@ class HostPipeline:
         # rows of Np values costs more than the conversion kernel
         # (scripts/rows_stage_time.py), so the input is converted on the copy stream
         self.direct = bool(direct) and getattr(d, "fused_kind", -1) == 2
+        self.trace = None                     # debug: list -> per-launch timing events
+        self.lookahead = 8                    # chunks of copy-in queued beyond the next stage-1 needs
         self.h2d, self.d2h = torch.cuda.Stream(d.device), torch.cuda.Stream(d.device)
+        self.pack = torch.cuda.Stream(d.device)
+        self.ev_copied = [torch.cuda.Event() for _ in range(nc)]
         self.ev_in = [torch.cuda.Event() for _ in range(nc)]
         self.ev_out = [torch.cuda.Event() for _ in range(nc)]
 
@@ -664,18 +669,37 @@ class HostPipeline:
         self.h2d.wait_stream(cur)
         self.d2h.wait_stream(cur)
         direct = self.direct
-        with torch.cuda.stream(self.h2d):
-            for c, (k0, k1) in enumerate(self.elems):
-                for f in range(d.fld):
-                    self.rows_in[f, k0:k1].copy_(host_in[f][k0:k1], non_blocking=True)
-                _native.call("wadg_rows_to_fields", s, _vp(self.rows_in), k0, k1, _vp(self.bufs[0]), sp(self.h2d))
-                self.ev_in[c].record(self.h2d)
+        self.pack.wait_stream(cur)
+        nc = len(self.elems)
+        queued = [-1]                        # last chunk whose copy-in is enqueued
+
+        def enqueue_input(upto):             # copy engine first, conversion on its own stream
+            while queued[0] < upto:
+                c = queued[0] + 1
+                k0, k1 = self.elems[c]
+                with torch.cuda.stream(self.h2d):
+                    for f in range(d.fld):
+                        self.rows_in[f, k0:k1].copy_(host_in[f][k0:k1], non_blocking=True)
+                    self.ev_copied[c].record(self.h2d)
+                with torch.cuda.stream(self.pack):
+                    self.pack.wait_event(self.ev_copied[c])
+                    _native.call("wadg_rows_to_fields", s, _vp(self.rows_in), k0, k1, _vp(self.bufs[0]),
+                                 sp(self.pack))
+                    self.ev_in[c].record(self.pack)
+                queued[0] = c
+
+        # Host enqueue order follows the device order: a chunk's copy-in goes out
+        # just ahead of the first stage that needs it, and its copy-out right behind
+        # its last stage, so the first stage launch is queued after a few chunks of
+        # copies rather than after all of them
         waited = -1
         res = self.stepper.res
         for st, c in self.schedule:
-            if st == 1 and self.hi[c] > waited:
-                waited = int(self.hi[c])
-                cur.wait_event(self.ev_in[waited])
+            if st == 1:
+                enqueue_input(min(nc - 1, int(self.hi[c]) + self.lookahead))
+                if self.hi[c] > waited:
+                    waited = int(self.hi[c])
+                    cur.wait_event(self.ev_in[waited])
             b0, b1 = self.blocks[c]
             qi, qo = self.bufs[(st - 1) % 2], self.bufs[st % 2]
             if direct and st == 5:           # the last stage writes the row layout
@@ -684,17 +708,23 @@ class HostPipeline:
             else:
                 _native.call("wadg_stage_fused", s, _vp(qi), _vp(qo), _vp(res), fl.tau_p, fl.tau_u,
                              LSRK4A[st - 1], LSRK4B[st - 1], dt, b0, b1, sp(cur))
+            if self.trace is not None:       # debug: per-launch end times on the compute stream
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(cur)
+                self.trace.append((st, c, ev))
             if st == 5:
                 self.ev_out[c].record(cur)
-        with torch.cuda.stream(self.d2h):
-            for c, (k0, k1) in enumerate(self.elems):
-                self.d2h.wait_event(self.ev_out[c])
-                if not direct:
-                    _native.call("wadg_fields_to_rows", s, _vp(self.bufs[1]), k0, k1, _vp(self.rows_out),
-                                 sp(self.d2h))
-                for f in range(d.fld):
-                    out[f, k0:k1].copy_(self.rows_out[f, k0:k1], non_blocking=True)
+                k0, k1 = self.elems[c]
+                with torch.cuda.stream(self.d2h):
+                    self.d2h.wait_event(self.ev_out[c])
+                    if not direct:
+                        _native.call("wadg_fields_to_rows", s, _vp(self.bufs[1]), k0, k1, _vp(self.rows_out),
+                                     sp(self.d2h))
+                    for f in range(d.fld):
+                        out[f, k0:k1].copy_(self.rows_out[f, k0:k1], non_blocking=True)
+        enqueue_input(nc - 1)
         cur.wait_stream(self.h2d)
+        cur.wait_stream(self.pack)
         cur.wait_stream(self.d2h)
         self.d2h.synchronize()
         return FieldState.from_fields(list(out.unbind(0)), state.t + dt)

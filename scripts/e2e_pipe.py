@@ -71,6 +71,10 @@ for a in args:
     pipe = solver.HostPipeline(disc, chunk_blocks=cb)
     r = {"chunk_blocks": a, "chunks": len(pipe.blocks), "span": int(max(pipe.hi - range(len(pipe.hi))))}
     r["e2e_ms"] = timed(lambda: pipe.step(st, dt))
+    for la in (1, 2, 8, 64):
+        pipe.lookahead = la
+        r[f"e2e_ms_lookahead{la}"] = timed(lambda: pipe.step(st, dt))
+    pipe.lookahead = 8
     # the same launch order without copies
     import ctypes
     s = ctypes.byref(d.struct)
@@ -82,6 +86,23 @@ for a in args:
                          ctypes.c_void_p(pipe.bufs[stg % 2].data_ptr()), ctypes.c_void_p(pipe.stepper.res.data_ptr()),
                          disc.flux.tau_p, disc.flux.tau_u, solver.LSRK4A[stg - 1], solver.LSRK4B[stg - 1], dt, b0, b1, cur())
     r["chunked_sweep_ms"] = timed(sweep)
+    # the same sweep while unrelated H2D and D2H copies of the state run on two
+    # other streams: how much do the copies slow the kernels down?
+    big_d = torch.empty((4, K, Np), dtype=torch.float32, device="cuda")
+    big_h = torch.empty((4, K, Np), dtype=torch.float32).pin_memory()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    def sweep_with_copies():
+        cur = torch.cuda.current_stream()
+        s1.wait_stream(cur); s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            for f in range(4):
+                big_d[f].copy_(host[f], non_blocking=True)
+        with torch.cuda.stream(s2):
+            big_h.copy_(pipe.rows_out, non_blocking=True)
+        sweep()
+        cur.wait_stream(s1); cur.wait_stream(s2)
+    r["chunked_sweep_with_concurrent_copies_ms"] = timed(sweep_with_copies)
+    del big_d, big_h
     print(json.dumps(r), flush=True)
     del pipe
     torch.cuda.empty_cache()
@@ -134,3 +155,25 @@ for name, kw in (("all", {}), ("no_copies", dict(copy_in=False, copy_out=False))
                  ("no_copy_in", dict(copy_in=False, pack=False)),
                  ("copies_only", dict(compute=False))):
     print(json.dumps({"variant": name, "ms": timed(lambda: variant(**kw))}), flush=True)
+
+
+# per-launch timeline of one pipelined step (compute stream): gaps between launches
+pipe = solver.HostPipeline(disc)
+for _ in range(2):
+    pipe.step(st, dt)
+torch.cuda.synchronize()
+start = torch.cuda.Event(enable_timing=True)
+pipe.trace = []
+start.record()
+pipe.step(st, dt)
+torch.cuda.synchronize()
+ends = [(s_, c_, start.elapsed_time(e)) for s_, c_, e in pipe.trace]
+ms_chunk = {}
+prev = 0.0
+gaps = []
+for s_, c_, t in ends:
+    gaps.append((s_, c_, round(t - prev, 3)))
+    prev = t
+print(json.dumps({"timeline_first_20 (stage, chunk, ms since previous end)": gaps[:20],
+                  "last_end_ms": round(ends[-1][2], 3), "n_launches": len(ends),
+                  "largest_10": sorted(gaps, key=lambda g: -g[2])[:10]}), flush=True)
