@@ -64,6 +64,15 @@ args = sys.argv[1:] or ["auto", str(3 * sms), str(2 * sms)]
 for a in args:
     if a == "auto":
         cb = None
+    elif a.startswith("r"):      # ramped head: 1, 1, 1, 2 waves, then 3-wave chunks
+        nblk = d.Kpad // d.fused
+        head = [sms, sms, sms, 2 * sms]
+        tail = [2 * sms, sms, sms, sms]
+        mid = nblk - sum(head) - sum(tail)
+        body = [3 * sms] * (mid // (3 * sms))
+        if mid - sum(body):
+            body.append(mid - sum(body))
+        cb = head + body + tail
     elif a.startswith("w"):
         cb = solver.pipeline_chunks(d.Kpad // d.fused, sms, int(a[1:]))
     else:
