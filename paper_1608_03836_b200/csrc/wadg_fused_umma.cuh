@@ -238,6 +238,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     const size_t blk = (size_t)(block0 + blockIdx.x);
     const size_t kblk = blk * ME;
     UMMA_MARK0(0);
+    asm volatile("griddepcontrol.launch_dependents;");   // the next stage may start its prologue
     if (P.prof && threadIdx.x == 0) {   // debug: SM id (slot 30), for per-SM gap analysis
         uint32_t smid;
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -253,6 +254,11 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     for (int r = tid; r < NF * 6 * NFP; r += C::NTH) sExt[r] = __ldg(P.ext_node + r);
     for (int r = tid; r < NF * NFP; r += C::NTH) sFmask[r] = __ldg(P.fmask + r);
     for (int r = tid; r < 6 * NFP; r += C::NTH) sPerm[r] = __ldg(P.fperm + r);
+    // Programmatic dependent launch: everything above touches only static data,
+    // so it overlaps the previous stage kernel's tail; the fields, res and halo
+    // written by that kernel are read (and Qout / res written) only after this
+    // wait.  Without the launch attribute the wait is a no-op.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // neighbour tables of all faces (consumed in the surface phase)
     int nbr[NF], ncode[NF];
     if (!mma_warp) {

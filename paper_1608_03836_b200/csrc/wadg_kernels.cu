@@ -848,9 +848,23 @@ static int launch_umma_lay(const wadg_problem *Pc, const void *Qin, void *Qout, 
         if (e != cudaSuccess) return fail(cudaGetErrorString(e));
         attr_set = true;
     }
-    uk::k_stage_umma<N, LAY><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin,
-                                                             (float *)Qout, (float *)res, (float)tp, (float)tu,
-                                                             (float)a, (float)b, (float)dt, b0);
+    // programmatic dependent launch: consecutive stage kernels on a stream overlap
+    // the next one's prologue with this one's tail (the kernel waits on
+    // griddepcontrol.wait before touching data the previous kernel wrote)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(b1 - b0);
+    cfg.blockDim = dim3(C::NTH);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, uk::k_stage_umma<N, LAY>, make_fprob<float>(*Pc), (const float *)Qin,
+                                       (float *)Qout, (float *)res, (float)tp, (float)tu, (float)a, (float)b,
+                                       (float)dt, b0);
+    if (e != cudaSuccess) return fail(cudaGetErrorString(e));
     return check_launch("wadg_stage_fused(umma)");
 }
 
