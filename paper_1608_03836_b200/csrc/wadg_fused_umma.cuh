@@ -678,20 +678,27 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             const int code = f == 0 ? ncode[0] : f == 1 ? ncode[1] : f == 2 ? ncode[2] : ncode[3];
             const int c = sub;
             float *dst = sStage + (size_t)c * NFP * ME + e;
+            // one loop per case (the case is fixed per element and face); the rare
+            // boundary and halo cases stay rolled to keep the kernel's code small
+            if (nb >= 0) {
 #pragma unroll
-            for (int i = 0; i < NFP; ++i) {
-                if (nb >= 0) {
+                for (int i = 0; i < NFP; ++i) {
                     if constexpr (LAY & 1)
                         fused::cp_async_elem(dst + i * ME, Qin + ((size_t)c * P.K + nb) * NP + sExt[code * NFP + i]);
                     else
                         fused::cp_async_elem(dst + i * ME, Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
-                } else if (nb == -1) {   // mirror BC (solver.py:214-217): p+ = -p-, u+ = u-
+                }
+            } else if (nb == -1) {       // mirror BC (solver.py:214-217): p+ = -p-, u+ = u-
+#pragma unroll 1
+                for (int i = 0; i < NFP; ++i) {
                     const float m = sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i]) / 4];
                     dst[i * ME] = c == 0 ? -m : m;
-                } else {
+                }
+            } else {
+#pragma unroll 1
+                for (int i = 0; i < NFP; ++i)
                     fused::cp_async_elem(dst + i * ME,
                                          P.halo + ((size_t)(-nb - 2) * 4 + c) * NFP + sPerm[(code % P.nor) * NFP + i]);
-                }
             }
             fused::cp_async_commit();
         };
