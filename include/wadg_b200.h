@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define WADG_ABI_VERSION 5
+#define WADG_ABI_VERSION 6
 #define WADG_ELEMS_PER_BLOCK 32
 
 enum { WADG_F64 = 0, WADG_F32 = 1 };
@@ -101,6 +101,14 @@ typedef struct wadg_problem {
     const void *fgeo_il;
     const void *wu_il;
     const void *wp_il;    /* NULL when wp is NULL */
+    /* tcgen05 stage: per element mean update weight, [2][Kpad]: row 0 the mean
+     * of 1/J, row 1 the mean of c^2/J over the update points.  When not NULL,
+     * wu_il / wp_il hold the deviations w - wbar and the stage forms the WADG
+     * update as wbar R + Pu((w - wbar) Vu R) (exact, since Pu Vu = I); the
+     * tensor core then accumulates only the small deviation term, which keeps
+     * its round-toward-zero accumulation error small.  NULL: wu_il / wp_il
+     * hold the full weights.                                               */
+    const void *wbar;
     /* ExactCurvedMass comparator (R/.../solver.py:156-167, 302-306): when minv_p
      * is not NULL, wadg_mass_inverse / wadg_update_lsrk / wadg_stage apply the
      * stored dense per-element operators A_k = M_k^-1 Mhat (M_k the J/c^2- and

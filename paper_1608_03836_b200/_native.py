@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 WADG_F64, WADG_F32 = 0, 1
 WADG_STRONG, WADG_STRONG_WEAK = 0, 1
 ELEMS_PER_BLOCK = 32
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
@@ -35,7 +35,7 @@ class WadgProblem(ctypes.Structure):
         ("halo", _vp), ("n_halo", _i32),
         ("Ne", _i32), ("Ve", _vp), ("we", _vp), ("ewp", _vp), ("ewu", _vp), ("e_recip", _i32),
         ("order", _i32), ("opVA", _vp), ("opVB", _vp), ("opU1", _vp), ("opU2", _vp), ("liftT", _vp),
-        ("geo_il", _vp), ("fgeo_il", _vp), ("wu_il", _vp), ("wp_il", _vp),
+        ("geo_il", _vp), ("fgeo_il", _vp), ("wu_il", _vp), ("wp_il", _vp), ("wbar", _vp),
         ("minv_p", _vp), ("minv_u", _vp),
     ]
 

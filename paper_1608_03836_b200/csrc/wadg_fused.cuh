@@ -232,6 +232,7 @@ struct FProb {
     int nor;
     long long *prof;   // optional: per-CTA clock64 at phase boundaries (debug)
     const T *geo_il, *fgeo_il, *wu_il, *wp_il;   // block-interleaved copies (tcgen05 stage)
+    const T *wbar;                               // tcgen05 stage: [2][Kpad] mean update weights (or NULL)
 };
 
 #define WADG_PROF_MARK(slot)                                                          \

@@ -70,9 +70,8 @@ struct CfgU {
     // operator tile images (floats, hi image then lo image)
     // volume tiles per quadrature chunk: D_a (rows a*16 + q), Vq (rows q), DTW_a (3 blocks of
     // rows j, K = q), -Pq (rows j, K = q)
-    // Vq tiles cover two chunks (32 rows): U_i is computed for a chunk pair at once (N = 32)
-    static constexpr int NPAIR = cdiv(NCH, 2);
-    static constexpr int OPDA = 2 * 48 * NPK, OPVQ = 2 * 32 * NPK, OPDTW = 2 * 3 * NPN * QC, OPPQ = 2 * NPN * QC;
+    // Vq tiles per chunk (16 rows), double buffered
+    static constexpr int OPDA = 2 * 48 * NPK, OPVQ = 2 * 16 * NPK, OPDTW = 2 * 3 * NPN * QC, OPPQ = 2 * NPN * QC;
     static constexpr int OPVF = 2 * 16 * NPK;               // rows: face points of one half
     static constexpr int OPVFI = 2 * 16 * NFPK;
     static constexpr int OPPF = 2 * NPN * 16;               // rows j, K = face points
@@ -82,7 +81,7 @@ struct CfgU {
     // offsets (floats) of the packed operator buffer
     static constexpr size_t O_DA = 0;
     static constexpr size_t O_VQ = O_DA + (size_t)NCH * OPDA;
-    static constexpr size_t O_DTW = O_VQ + (size_t)NPAIR * OPVQ;
+    static constexpr size_t O_DTW = O_VQ + (size_t)NCH * OPVQ;
     static constexpr size_t O_PQ = O_DTW + (size_t)NCH * OPDTW;
     static constexpr size_t O_VFI = O_PQ + (size_t)NCH * OPPQ;         // [half] Vfi
     static constexpr size_t O_PF = O_VFI + (size_t)NFH * OPVFI;         // [f][half] -Pf
@@ -93,7 +92,7 @@ struct CfgU {
     static constexpr size_t MISC = 2304;
     static_assert(128 + 4 * (NF * 6 * NFP + NF * NFP + 6 * NFP) <= MISC, "index tables exceed MISC");
     static constexpr size_t SQF = (size_t)FLD * ME * NPK;              // floats of one field set
-    static constexpr size_t S_VOL = (size_t)(2 * OPDA + OPVQ + OPDTW + OPPQ) * 4;
+    static constexpr size_t S_VOL = (size_t)(2 * OPDA + 2 * OPVQ + OPDTW + OPPQ) * 4;
     static constexpr size_t S_EXT = (size_t)FLD * ME * NFPK * 4;      // one K-major face-node operand
     static constexpr size_t S_UPD = (size_t)2 * (OPU1 + OPU2) * 4;
     static constexpr size_t S_OPS = fused::maxz(S_VOL, S_UPD);
@@ -104,7 +103,8 @@ struct CfgU {
     static constexpr size_t SMEM = MISC + SQF * 4 + S_UNION;
     // TMEM columns
     static constexpr uint32_t RACC = 0, SCR = 4 * NPN;
-    static_assert(SCR + 336 <= 512 && SCR + 192 + 4 * NPK <= 512 && SCR + 320 <= 512, "TMEM budget");
+    static_assert(SCR + 288 + NPN <= 512 && SCR + 192 + 4 * NPK <= 512 && SCR + 320 + (NPN < 32 ? NPN : 32) <= 512,
+                  "TMEM budget");
     // op-tile barrier slots (bar[1 + slot]) in the volume phase; the surface and update
     // phases use slots 0 and 1
     static constexpr int SL_DA = 0, SL_VQ = 2, SL_PQ = 4, SL_DTW = 5;
@@ -156,7 +156,7 @@ __device__ __forceinline__ void st_split8(uint32_t t_hi, uint32_t t_lo, const fl
     float hi[8], lo[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        hi[i] = umma::tf32_hi(v[i]);
+        hi[i] = umma::tf32_split_hi(v[i]);
         lo[i] = v[i] - hi[i];
     }
     umma::st8(t_hi, hi);
@@ -167,7 +167,7 @@ __device__ __forceinline__ void st_split4(uint32_t t_hi, uint32_t t_lo, const fl
     float hi[4], lo[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        hi[i] = umma::tf32_hi(v[i]);
+        hi[i] = umma::tf32_split_hi(v[i]);
         lo[i] = v[i] - hi[i];
     }
     umma::st4(t_hi, hi);
@@ -211,7 +211,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     constexpr uint32_t RACC = C::RACC, SCR = C::SCR;
     constexpr uint32_t FQB = ME * NPK * 4;              // bytes of one field in sQ / sQlo
     constexpr int NB = C::NTH;                          // named-barrier thread count
-    enum { B_P = 1, B_U = 2, B_S0 = 3, B_S1 = 4, B_R = 5, B_Z0 = 6, B_Z1 = 7, B_S2 = 8 };
+    enum { B_P = 1, B_U = 2, B_S0 = 3, B_S1 = 4, B_R = 5, B_Z0 = 6, B_Z1 = 7, B_S2 = 8, B_E = 9 };
 
     extern __shared__ __align__(1024) unsigned char smem[];
     // mbarriers: [0] MMA group A (volume p chain, face traces, update U1), [7] MMA
@@ -320,11 +320,17 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     // ---- shared-memory regions and TMEM columns per phase ------------------
     // volume
     float *sDa = sOp;                                   // [2][OPDA]
-    float *sVq = sDa + 2 * C::OPDA;                     // [OPVQ] (one chunk pair)
-    float *sPq = sVq + C::OPVQ;                         // [OPPQ]
+    auto sVq = [&](int b) { return sDa + 2 * C::OPDA + b * C::OPVQ; };   // [2][OPVQ]
+    float *sPq = sDa + 2 * C::OPDA + 2 * C::OPVQ;       // [OPPQ]
     float *sDTW = sPq + C::OPPQ;                        // [OPDTW]
-    // U of a chunk pair: field i at UO + 32 i, chunk ch at + 16 (ch & 1)
-    const uint32_t DPO = SCR, UO = SCR + 48, GPH = SCR + 144, GPL = SCR + 192, FH = SCR + 240, FL = SCR + 288;
+    // U of a chunk: field i at UO + 16 i.  RPC: the split-TF32 correction terms
+    // (A_lo B_hi, A_hi B_lo) of the R_p volume accumulation, kept apart from the
+    // main terms in RACC: the tensor core's fp32 accumulation truncates toward
+    // zero at the accumulator's ulp, so the small corrections are not added into
+    // the large running R_p (half the truncations there); folded into R_p by the
+    // epilogue at the end of the volume
+    const uint32_t DPO = SCR, UO = SCR + 48, GPH = SCR + 96, GPL = SCR + 144, FH = SCR + 192, FL = SCR + 240,
+                   RPC = SCR + 288;
     // surface (over the sQlo + ops union): exterior node hi / lo and own node lo
     // parts (K-major operands), resident Vfi tiles, two -Pf tiles, neighbour-node
     // staging; TMEM: traces at the 16 points of a face half (own, exterior), the
@@ -333,7 +339,10 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     float *sVfi = sQlo + 3 * C::S_EXT / 4;
     auto sPf = [&](int b) { return sVfi + NFH * C::OPVFI + b * C::OPPF; };
     float *sStage = sVfi + NFH * C::OPVFI + 2 * C::OPPF;
-    const uint32_t OWN = SCR, EXT = SCR + 64, GH = SCR + 128, GL = SCR + 192, OWNH = SCR + 256;
+    // RPCS: the split-TF32 correction terms of the R_p lifts (nodes 0 .. RPW-1; the
+    // rest, if any, go into RACC), folded into R_p after the last lift (like RPC)
+    constexpr int RPW = NPN < 32 ? NPN : 32;
+    const uint32_t OWN = SCR, EXT = SCR + 64, GH = SCR + 128, GL = SCR + 192, OWNH = SCR + 256, RPCS = SCR + 320;
     // update: two chains, one per field pair (0: p, u1; 1: u2, u3).  R of pair 0
     // (hi, lo) in the sQlo region, R of pair 1 (hi, lo) in TMEM; per chain z and
     // omega z (hi, lo) in TMEM; two {Vu, Pu} tile buffers
@@ -378,8 +387,8 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                              desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
             }
         };
-        auto issue_v1u = [&]() {                       // U_i for the chunk pair in sVq
-            const uint32_t bh = su32(sVq), bl = bh + C::OPVQ * 2, id = idesc_tf32(128, 32);
+        auto issue_v1u = [&](int ch) {                 // U_i of chunk ch (Vq tile in buffer ch & 1)
+            const uint32_t bh = su32(sVq(ch & 1)), bl = bh + C::OPVQ * 2, id = idesc_tf32(128, 16);
 #pragma unroll 1
             for (int ks = 0; ks < NPK / 8; ++ks) {
                 const uint32_t o = ks * 256;
@@ -387,7 +396,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 for (int t = 0; t < 3; ++t)
 #pragma unroll
                     for (int i = 0; i < 3; ++i)
-                        mma_ss_w(tm + UO + 32 * i, desc_k((t == 0 ? aQlo : aQ) + (1 + i) * FQB + o, 128, SBO_Q),
+                        mma_ss_w(tm + UO + 16 * i, desc_k((t == 0 ? aQlo : aQ) + (1 + i) * FQB + o, 128, SBO_Q),
                                  desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
             }
         };
@@ -404,7 +413,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                                  (ch > 0 || ks > 0 || t > 0) ? 1u : 0u);
             }
         };
-        auto issue_v2u = [&](int ch) {   // R_p += sum_a DTW_a F_a
+        auto issue_v2u = [&](int ch) {   // R_p += sum_a DTW_a F_a: main terms -> RACC, corrections -> RPC
             constexpr uint32_t BLK = NPN * QC * 4;
             const uint32_t bh = su32(sDTW), bl = bh + C::OPDTW * 2, id = idesc_tf32(128, NPN);
 #pragma unroll 1
@@ -413,22 +422,25 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 for (int t = 0; t < 3; ++t)
 #pragma unroll
                     for (int a = 0; a < 3; ++a)
-                        mma_ts_w(tm + RACC, tm + (t == 0 ? FL : FH) + 16 * a + 8 * ks,
+                        mma_ts_w(t < 2 ? tm + RPC : tm + RACC, tm + (t == 0 ? FL : FH) + 16 * a + 8 * ks,
                                  desc_k((t == 1 ? bl : bh) + a * BLK + ks * 256, 128, SBO_16), id,
-                                 (ch > 0 || ks > 0 || t > 0 || a > 0) ? 1u : 0u);
+                                 (ch > 0 || ks > 0 || a > 0 || t == 1) ? 1u : 0u);
             }
         };
         op_load(C::SL_DA, sDa, ops + C::O_DA, C::OPDA * 4);
-        op_load(C::SL_VQ, sVq, ops + C::O_VQ, C::OPVQ * 4);
+        op_load(C::SL_VQ, sVq(0), ops + C::O_VQ, C::OPVQ * 4);
         op_load(C::SL_PQ, sPq, ops + C::O_PQ, C::OPPQ * 4);
         op_load(C::SL_DTW, sDTW, ops + C::O_DTW, C::OPDTW * 4);
-        if (NCH > 1) op_load(C::SL_DA + 1, sDa + C::OPDA, ops + C::O_DA + C::OPDA, C::OPDA * 4);
+        if (NCH > 1) {
+            op_load(C::SL_DA + 1, sDa + C::OPDA, ops + C::O_DA + C::OPDA, C::OPDA * 4);
+            op_load(C::SL_VQ + 1, sVq(1), ops + C::O_VQ + C::OPVQ, C::OPVQ * 4);
+        }
         __syncwarp();
         op_wait(C::SL_DA);
         issue_v1p(0);
         commit_w(&bar[0]);
         op_wait(C::SL_VQ);
-        issue_v1u();                         // chunks 0, 1
+        issue_v1u(0);
         commit_w(&bar[7]);
         for (int ch = 0; ch < NCH; ++ch) {
             const bool more = ch + 1 < NCH;
@@ -453,13 +465,13 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             VTR(5);
             issue_v2u(ch);
             commit_w(&bar_v2[1]);
-            if (more && (ch & 1)) {          // next chunk pair (ch + 1, ch + 2)
-                op_wait(C::SL_VQ);
-                issue_v1u();
+            if (more) {
+                op_wait(C::SL_VQ + ((ch + 1) & 1));
+                issue_v1u(ch + 1);
             }
             commit_w(&bar[7]);
             // refills: the -Pq / D_a(ch) tiles are free once V2p(ch) (issued after V1p(ch))
-            // is done, the DTW / Vq(ch) tiles once V2u(ch) is
+            // is done, the DTW / Vq(ch) tiles once V2u(ch) (issued after V1u(ch)) is
             wait_k(&bar_v2[0], ++nv2p);
             VTR(6);
             if (more) op_load(C::SL_PQ, sPq, ops + C::O_PQ + (size_t)(ch + 1) * C::OPPQ, C::OPPQ * 4);
@@ -470,8 +482,8 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             VTR(7);
 #undef VTR
             if (more) op_load(C::SL_DTW, sDTW, ops + C::O_DTW + (size_t)(ch + 1) * C::OPDTW, C::OPDTW * 4);
-            if (!(ch & 1) && ch + 2 < NCH)   // pair ch/2 consumed (V1u issued before V2u(ch)): next pair
-                op_load(C::SL_VQ, sVq, ops + C::O_VQ + (size_t)(ch / 2 + 1) * C::OPVQ, C::OPVQ * 4);
+            if (ch + 2 < NCH)
+                op_load(C::SL_VQ + (ch & 1), sVq(ch & 1), ops + C::O_VQ + (size_t)(ch + 2) * C::OPVQ, C::OPVQ * 4);
         }
         nB = NCH + 1;                        // group-B completions so far (V1u(0), per-chunk u commits)
         // ---- surface: per (face, half) step s: traces(s) (group A) are issued as
@@ -485,14 +497,22 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         auto issue_lift = [&](int st) {
             op_wait(st & 1);
             const uint32_t pfh = su32(sPf(st & 1)), pfl = pfh + C::OPPF * 2, idl = idesc_tf32(128, NPN);
+            const uint32_t idc = idesc_tf32(128, RPW), idr = idesc_tf32(128, NPN > RPW ? NPN - RPW : 8);
 #pragma unroll 1
             for (int ks = 0; ks < 2; ++ks)
 #pragma unroll
                 for (int t = 0; t < 3; ++t)
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        mma_ts_w(tm + RACC + NPN * c, tm + (t == 0 ? GL : GH) + 16 * c + 8 * ks,
-                                 desc_k((t == 1 ? pfl : pfh) + ks * 256, 128, SBO_16), idl, 1u);
+                    for (int c = 0; c < 4; ++c) {
+                        const uint32_t a = tm + (t == 0 ? GL : GH) + 16 * c + 8 * ks, b = (t == 1 ? pfl : pfh) + ks * 256;
+                        if (c == 0 && t < 2) {   // R_p corrections
+                            mma_ts_w(tm + RPCS, a, desc_k(b, 128, SBO_16), idc, (st > 0 || ks > 0 || t > 0) ? 1u : 0u);
+                            if constexpr (NPN > RPW)
+                                mma_ts_w(tm + RACC + RPW, a, desc_k(b + (RPW / 8) * SBO_16, 128, SBO_16), idr, 1u);
+                        } else {
+                            mma_ts_w(tm + RACC + NPN * c, a, desc_k(b, 128, SBO_16), idl, 1u);
+                        }
+                    }
             commit_w(&bar[7]);
         };
         for (int step = 0; step < NSTEP; ++step) {
@@ -654,7 +674,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             {
                 float U[3][4];
 #pragma unroll
-                for (int i = 0; i < 3; ++i) ld4(tl + UO + 32 * i + 16 * (ch & 1) + 4 * sub, U[i]);
+                for (int i = 0; i < 3; ++i) ld4(tl + UO + 16 * i + 4 * sub, U[i]);
                 wait_ld();
 #pragma unroll
                 for (int m = 0; m < 3; ++m) {
@@ -671,6 +691,18 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         }
         wait_A();                            // V2p of the last chunk
         wait_B();                            // V2u of the last chunk
+        // fold the R_p correction terms into R_p (fp32, round to nearest): node groups
+        // of 8 split between the four sub-groups of an element
+        for (int g = sub; g < NPN / 8; g += 4) {
+            float r[8], q[8];
+            ld8(tl + RACC + 8 * g, r);
+            ld8(tl + RPC + 8 * g, q);
+            wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] += q[i];
+            st8(tl + RACC + 8 * g, r);
+        }
+        wait_st();                           // handed to the MMA warp with the first face's operands
         UMMA_MARK0(2);
         // ---- surface ----
         auto gather = [&](int f) {   // neighbour face nodes of face f, field sub -> sStage [c][i][128]
@@ -729,9 +761,9 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                     const bool in = i0 + i < NFP;
                     const float x = in ? xs[(i0 + i) * ME] : 0.f;
                     const float y = in ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i0 + i]) / 4] : 0.f;
-                    ph[i] = tf32_hi(x);
+                    ph[i] = tf32_split_hi(x);
                     pl[i] = x - ph[i];
-                    qh[i] = tf32_hi(y);
+                    qh[i] = tf32_split_hi(y);
                     ql[i] = y - qh[i];
                 }
                 const uint32_t o = c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4;
@@ -817,9 +849,9 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                             const bool in = i0 + i < NFP;
                             const float x = in ? xs[(i0 + i) * ME] : 0.f;
                             const float y = in ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i0 + i]) / 4] : 0.f;
-                            ph[i] = tf32_hi(x);
+                            ph[i] = tf32_split_hi(x);
                             pl[i] = x - ph[i];
-                            qh[i] = tf32_hi(y);
+                            qh[i] = tf32_split_hi(y);
                             ql[i] = y - qh[i];
                         }
                         const uint32_t o = c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4;
@@ -873,6 +905,19 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             }
         }
         wait_B();                            // last lift: R complete
+        for (int g = sub; g < RPW / 8; g += 4) {   // fold the R_p lift corrections into R_p
+            float r[8], q[8];
+            ld8(tl + RACC + 8 * g, r);
+            ld8(tl + RPCS + 8 * g, q);
+            wait_ld();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] += q[i];
+            st8(tl + RACC + 8 * g, r);
+        }
+        wait_st();
+        fence_before();
+        nb_sync(B_E, NB - 32);               // epilogue warps only: R_p complete before it is read
+        fence_after();
         UMMA_MARK0(3);
         // ---- update ----
         // thread (e, sub): field lf = sub & 1 of each pair, points 8 (sub >> 1) .. +7 of a chunk
@@ -901,7 +946,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 wait_ld();
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    hi[i] = tf32_hi(v[i]);
+                    hi[i] = tf32_split_hi(v[i]);
                     lo[i] = v[i] - hi[i];
                 }
 #pragma unroll
@@ -914,7 +959,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 wait_ld();
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    hi[i] = tf32_hi(v[i]);
+                    hi[i] = tf32_split_hi(v[i]);
                     lo[i] = v[i] - hi[i];
                 }
                 st8(tl + RA1 + NPK * lf + j0, hi);
@@ -990,29 +1035,46 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         // res = a res + dt Minv(rhs); Q_out = Q_in + b res   (field c = sub)
         {
             const int c = sub;
+            // WADG update = wbar R + (tensor-core deviation term in RACC); the
+            // pre-update R of pair 0 is in shared memory (hi, lo), of pair 1 in TMEM
+            const float wb = P.wbar ? __ldg(P.wbar + (size_t)(c == 0 ? 1 : 0) * S + kblk + e) : 0.f;
             // 16 nodes per pass: the old res values are all loaded before the first
             // store (one load latency per pass instead of one per node)
 #pragma unroll
             for (int h0 = 0; h0 < NPK; h0 += 16) {
-                float rv[16], v[16];
+                float rv[16], v[16] = {}, rh[16] = {}, rl[16] = {};
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int j = h0 + i;
                     rv[i] = (a_rk != 0.f && j < NP) ? __ldg(res + (size_t)(c * NP + j) * S + kblk + e) : 0.f;
                 }
-                {
-                    float v8[8];
-                    ld8(tl + RACC + NPN * c + h0, v8);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) v[i] = v8[i];
-                }
-                if (h0 + 8 < NPK) {
-                    float v8[8];
-                    ld8(tl + RACC + NPN * c + h0 + 8, v8);
+                for (int hh = 0; hh < 16; hh += 8) {
+                    if (h0 + hh < NPK) {
+                        float v8[8];
+                        ld8(tl + RACC + NPN * c + h0 + hh, v8);
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) v[8 + i] = v8[i];
+                        for (int i = 0; i < 8; ++i) v[hh + i] = v8[i];
+                        if (c >= 2) {
+                            ld8(tl + RA1 + NPK * (c - 2) + h0 + hh, v8);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) rh[hh + i] = v8[i];
+                            ld8(tl + RA1 + 2 * NPK + NPK * (c - 2) + h0 + hh, v8);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) rl[hh + i] = v8[i];
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const uint32_t o = kmaj_off<NPK>(e, h0 + hh + i) / 4;
+                                rh[hh + i] = sA[c * ME * NPK + o];
+                                rl[hh + i] = sA[(2 + c) * ME * NPK + o];
+                            }
+                        }
+                    }
                 }
                 wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = fmaf(wb, rh[i] + rl[i], v[i]);
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int j = h0 + i;

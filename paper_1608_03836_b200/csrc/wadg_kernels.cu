@@ -735,6 +735,7 @@ static fused::FProb<T> make_fprob(const wadg_problem &p) {
     q.prof = g_prof;
     q.geo_il = (const T *)p.geo_il; q.fgeo_il = (const T *)p.fgeo_il;
     q.wu_il = (const T *)p.wu_il; q.wp_il = (const T *)p.wp_il;
+    q.wbar = (const T *)p.wbar;
     return q;
 }
 

@@ -182,6 +182,11 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t *bar, uint32_t phase,
 // TF32 split: x = hi + lo exactly, hi = x with the low 13 mantissa bits cleared
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 __device__ __forceinline__ float tf32_lo(float x) { return x - tf32_hi(x); }
+// hi part of an explicit split (the operand is stored as hi and lo): rounded to
+// the nearest tf32 (ties away), so the dropped lo*lo term has no sign bias
+__device__ __forceinline__ float tf32_split_hi(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
 
 // byte offset of (row, k) in a K-major no-swizzle tile with LBO = 128 and
 // SBO = 128 * (KT / 4) (core matrices of one 8-row group contiguous along K)

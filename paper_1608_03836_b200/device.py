@@ -17,6 +17,8 @@ straight from the map nodes, so million-element meshes never materialise
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -82,11 +84,16 @@ def interleave_blocks(x, npad, blk=128):
     return out
 
 
-def tf32_split(a):
-    """fp32 x = hi + lo exactly, hi = x with the low 13 mantissa bits cleared
-    (the tensor core's TF32 view of x)."""
+def tf32_split(a, mode=None):
+    """fp32 x = hi + lo exactly, hi a tf32 value: x rounded to the nearest
+    tf32 (ties away, "rn", default) or with the low 13 mantissa bits cleared
+    ("trunc", the tensor core's own view of a raw fp32 operand)."""
+    mode = mode or os.environ.get("WADG_TF32_SPLIT", "rn")
     x = np.ascontiguousarray(a, dtype=np.float32)
-    hi = (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    bits = x.view(np.uint32)
+    if mode == "rn":
+        bits = bits + np.uint32(0x1000)
+    hi = (bits & np.uint32(0xFFFFE000)).view(np.float32)
     return hi, (x - hi).astype(np.float32)
 
 
@@ -108,7 +115,7 @@ def split_images(*blocks):
 
 def umma_operator_images(ref, ru, cfg):
     """All reference operators of the tcgen05 fused stage (csrc/wadg_fused_umma.cuh,
-    CfgU offsets): per volume chunk D_a, DTW_a, -Pq and per chunk pair Vq; Vfi per
+    CfgU offsets): per volume chunk D_a, Vq, DTW_a, -Pq; Vfi per
     16-point half of the face rule; -Pf per face and half; update chunks Vu, Pu."""
     NP, NQ = ref.Np, ref.Nq
     QC, NCH, NPK, NPN, NFPK, NFH = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"], cfg["nfq8"]
@@ -127,8 +134,8 @@ def umma_operator_images(ref, ru, cfg):
     parts = []
     for ch in range(NCH):                   # D_a: rows a*16 + qq
         parts.append(split_images(np.vstack([rows(D, ch * QC, QC, NPK) for D in ref.Dq])))
-    for pr in range(-(-NCH // 2)):          # Vq: rows qq of a chunk pair (2 QC quadrature points)
-        parts.append(split_images(rows(ref.Vq, pr * 2 * QC, 2 * QC, NPK)))
+    for ch in range(NCH):                   # Vq: rows qq of a chunk
+        parts.append(split_images(rows(ref.Vq, ch * QC, QC, NPK)))
     for ch in range(NCH):                   # DTW_a: 3 blocks of (NPN rows j) x (QC columns q)
         parts.append(split_images(*[rows(M.T, ch * QC, QC, NPN).T for M in DTW]))
     for ch in range(NCH):                   # -Pq: (NPN rows j) x (QC columns q)
@@ -324,11 +331,24 @@ class DeviceProblem:
             fg = self.fgeo.view(self.dim + 1, ref.n_faces, ref.nfq, self.Kpad)
             self.fgeo_il = interleave_blocks(fg.reshape((self.dim + 1) * ref.n_faces, ref.nfq, self.Kpad),
                                              nfh * 16, kb)
-            self.wu_il = interleave_blocks(self.wu.unsqueeze(0), nchu * 16, kb)
-            self.wp_il = interleave_blocks(self.wp.unsqueeze(0), nchu * 16, kb) if self.wp is not None else None
+            # update weights as per-element means wbar plus deviations (wbar in
+            # [2][Kpad], include/wadg_b200.h); WADG_WBAR=0 keeps the full weights
+            wu, wp = self.wu, self.wp
+            self.wbar = None
+            if os.environ.get("WADG_WBAR", "1") != "0":
+                nq = ru.Nq
+                wbu = self.wu[:nq].double().mean(0)
+                wbp = self.wp[:nq].double().mean(0) if self.wp is not None else self.c2 * wbu
+                self.wbar = torch.stack([wbu, wbp]).to(self.dtype).contiguous()
+                wu = self.wu - self.wbar[0]
+                wp = self.wp - self.wbar[1] if self.wp is not None else None
+            self.wu_il = interleave_blocks(wu.unsqueeze(0), nchu * 16, kb)
+            self.wp_il = interleave_blocks(wp.unsqueeze(0), nchu * 16, kb) if wp is not None else None
+            del wu, wp
             s = self.struct
             s.geo_il, s.fgeo_il, s.wu_il = self.geo_il.data_ptr(), self.fgeo_il.data_ptr(), self.wu_il.data_ptr()
             s.wp_il = self.wp_il.data_ptr() if self.wp_il is not None else None
+            s.wbar = self.wbar.data_ptr() if self.wbar is not None else None
             self.fused_kind = 2
             self.struct.order = N
             return kb

@@ -1,0 +1,167 @@
+"""Parity at the BASELINE step counts (north_star: relative L2 of (p, u)
+after the stated number of steps <= 1e-11 in fp64 and <= 1e-5 in fp32),
+the default kernels (tcgen05 stage for fp32 N = 2..4, CUDA-core fused stage
+otherwise) against the fp64 oracle (oracle/wadg_oracle.py) on meshes of
+several 128-element tiles, so cross-tile neighbour gathers are checked
+against the oracle and not against the product.
+
+* config-4 physics: N = 4, heterogeneous c^2 = 1 + 0.5 sin 2 pi x sin 2 pi y
+  sin 2 pi z, Gaussian pulse, 100 steps, 8^3 x 6 tets (24 tiles), fp32 and fp64;
+* config-5 physics: N = 5, c^2 = 1, Gaussian pulse, 100 steps, 6^3 x 6 tets;
+* config-3 physics: N = 1..7, Gaussian pulse, 50 steps, 4^3 x 6 tets (3
+  tiles), fp32 and fp64;
+* the full config-4 mesh (K = 1,572,864): one LSRK stage (a != 0) of the
+  tcgen05 kernel checked element by element against the oracle on a sample
+  of tets, each with its face neighbours (a stage is local to that patch).
+
+dt = 0.5 h / (N+1)^2, h = 2/n.  Both sides start from the
+same projected state (the oracle's projection), so the comparison covers
+exactly the time stepping; the projection itself is compared separately.
+The measured errors are printed in pytest's terminal summary.
+"""
+
+import functools
+
+import numpy as np
+import pytest
+import torch
+
+import wadg_oracle as O
+from conftest import record_parity, submesh
+from paper_1608_03836_b200 import meshgen, solver
+from paper_1608_03836_b200.solver import FieldState, Formulation, SolverConfig
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"float64": 1e-11, "float32": 1e-5}
+
+
+def c2_het(x, y, z):
+    return 1.0 + 0.5 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y) * np.sin(2 * np.pi * z)
+
+
+def gaussian(x, y, z):
+    p = np.exp(-25.0 * (x * x + y * y + z * z))
+    return p, 0 * p, 0 * p, 0 * p
+
+
+def rel(got, want):
+    num = sum(float(np.sum((np.asarray(a, dtype=np.float64) - b) ** 2)) for a, b in zip(got, want))
+    den = sum(float(np.sum(b ** 2)) for b in want)
+    return np.sqrt(num / den)
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_run(n, N, het, steps):
+    """(mesh, initial oracle state, final oracle state, dt); cached so the
+    fp32 and fp64 cases share one oracle trajectory."""
+    mesh = meshgen.warped_cube_tet_mesh(n, N)
+    c2 = c2_het if het else 1.0
+    od = O.OracleDiscretization(mesh, N, True, c2=c2)
+    st0 = O.project_initial_condition(mesh, N, gaussian)
+    dt = 0.5 * (2.0 / n) / (N + 1) ** 2
+    st = st0
+    for _ in range(steps):
+        st = O.lsrk_step(st, dt, lambda y: O.rhs_full(y, od))
+    return mesh, st0, st, dt
+
+
+def device_run(mesh, N, het, dtype, st0, dt, steps):
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype=dtype)
+    medium = solver.MediumField(c2_het if het else 1.0)
+    disc = solver.Discretization(mesh, cfg, medium)
+    Q = disc.to_device(FieldState.from_fields(st0.fields()))
+    stepper = solver.DeviceStepper(disc)
+    for _ in range(steps):
+        Q = stepper.step(Q, dt)
+    out = disc.from_device(Q, FieldState.from_fields(st0.fields()), steps * dt)
+    return disc, [np.asarray(a) for a in out.fields()]
+
+
+def _check(name, n, N, het, dtype, steps):
+    mesh, st0, want, dt = oracle_run(n, N, het, steps)
+    disc, got = device_run(mesh, N, het, dtype, st0, dt, steps)
+    err = rel(got, want.fields())
+    change = rel(st0.fields(), want.fields())
+    record_parity(f"{name} K={mesh.K} N={N} {dtype} {steps} steps kernel={disc.dev.fused_kind}", err, TOL[dtype])
+    assert change > 1e-2, "the state should evolve over the run"
+    assert err < TOL[dtype], (name, N, dtype, err)
+    return disc
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_config4_physics_100_steps(dtype):
+    disc = _check("config-4 physics", 8, 4, True, dtype, 100)
+    if dtype == "float32":
+        assert disc.dev.fused_kind == 2          # the tcgen05 stage of the headline
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_config5_physics_100_steps(dtype):
+    _check("config-5 physics", 6, 5, False, dtype, 100)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7])
+def test_config3_physics_50_steps(N, dtype):
+    _check("config-3 physics", 4, N, False, dtype, 50)
+
+
+def test_projection_matches_oracle():
+    mesh = meshgen.warped_cube_tet_mesh(4, 4)
+    cfg = SolverConfig(N=4, formulation=Formulation.StrongWeak)
+    got = solver.project_initial_condition(mesh, cfg, gaussian)
+    want = O.project_initial_condition(mesh, 4, gaussian)
+    err = rel(got.fields()[:1], want.fields()[:1])
+    record_parity("Gaussian projection K=384 N=4", err, 1e-12)
+    assert err < 1e-12
+    assert all(np.max(np.abs(a)) == 0 for a in got.fields()[1:])
+
+
+# ---------------------------------------------------------------------------
+# full config-4 size: sampled element-local parity of one tcgen05 stage
+
+def test_full_size_stage_sampled_against_oracle():
+    """K = 1,572,864 (BASELINE config 4), N = 4, fp32, heterogeneous c^2:
+    one stage res' = a res + dt M^-1 rhs(Q), Q' = Q + b res' of the tcgen05
+    kernel, on random Q and res, compared with the oracle for 512 sampled
+    elements (boundary, interior and every tile position), each from its
+    one-neighbour patch.  Tolerance: the fp32 bar per element patch."""
+    N, n = 4, 64
+    mesh = meshgen.warped_cube_tet_mesh(n, N)
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype="float32")
+    disc = solver.Discretization(mesh, cfg, solver.MediumField(c2_het))
+    assert mesh.K == 1572864 and disc.dev.fused_kind == 2
+    d = disc.dev
+    g = torch.Generator(device="cuda").manual_seed(77)
+    Q = torch.randn(d.empty_fields().shape, generator=g, device="cuda", dtype=torch.float32)
+    res = torch.randn(Q.shape, generator=g, device="cuda", dtype=torch.float32)
+    Q[:, :, mesh.K:] = 0
+    res[:, :, mesh.K:] = 0
+    stepper = solver.DeviceStepper(disc)
+    stepper.res.copy_(res)
+    a, b, dt = solver.LSRK4A[2], solver.LSRK4B[2], 0.5 * mesh.h / 25
+    Qout = stepper.stage(Q, a, b, dt)
+    rng = np.random.default_rng(5)
+    blocks = rng.choice(mesh.K // 128, 64, replace=False)
+    elems = np.unique(np.concatenate([(blocks[:, None] * 128 + rng.choice(128, 8, replace=False)[None, :]).ravel(),
+                                      [0, 127, 128, mesh.K - 1]]))
+    sub, patch, loc = submesh(mesh, elems)
+    host = lambda X: [X[i, :, :mesh.K][:, torch.as_tensor(patch, device="cuda")].T.double().cpu().numpy()
+                      for i in range(4)]
+    Qp, Rp = host(Q), host(res)
+    od = O.OracleDiscretization(sub, N, True, c2=c2_het)
+    r = O.rhs_full(O.State(Qp[0], Qp[1:]), od).fields()
+    want_res = [a * x + dt * y for x, y in zip(Rp, r)]
+    want_Q = [q + b * x for q, x in zip(Qp, want_res)]
+    got_res, got_Q = host(stepper.res), host(Qout)
+    e_res = rel([x[loc] for x in got_res], [x[loc] for x in want_res])
+    e_Q = rel([x[loc] for x in got_Q], [x[loc] for x in want_Q])
+    # the rhs part alone (res' - a res = dt rhs), the hardest-hit quantity in fp32
+    e_rhs = rel([(x - a * y)[loc] for x, y in zip(got_res, Rp)], [dt * y[loc] for y in r])
+    record_parity(f"config-4 full size K={mesh.K} stage, {len(elems)} sampled tets: res", e_res, 1e-5)
+    record_parity(f"config-4 full size K={mesh.K} stage, {len(elems)} sampled tets: Q", e_Q, 1e-5)
+    record_parity(f"config-4 full size K={mesh.K} stage, {len(elems)} sampled tets: dt*rhs", e_rhs, 1e-5)
+    assert e_res < 1e-5 and e_Q < 1e-5 and e_rhs < 1e-5
+    del disc, d, Q, res, Qout, stepper
+    torch.cuda.empty_cache()

@@ -95,6 +95,39 @@ def test_energy_rate_equals_face_jump_dissipation(rng, curved):
     assert dE < 0
 
 
+def test_energy_rate_identity_curved_tets_sufficient_quadrature(rng):
+    """R/pkg/tests/test_solver.py:80-105 on curved tets, split by what is
+    exact.  With the strong-form sufficiency rules (volume 2N + 2N_geo - 3,
+    face 2N + 2N_geo - 2):
+    * tau = 0: the central-flux terms telescope exactly although the two
+      sides of a face integrate at different collapsed-rule points, because
+      p u.(n sJ) is a polynomial the face rule integrates exactly on both
+      sides (n sJ is the polynomial Nanson area vector): dE/dt = 0 to rounding;
+    * tau > 0: the penalty terms carry sJ = |n sJ| and n = (n sJ)/sJ, which are
+      not polynomials on curved faces, so the identity holds to the face
+      rule's accuracy (1e-6 measured; 1e-3 with the default 2N+1 rule)."""
+    N = 3
+    mesh = meshgen.warped_cube_tet_mesh(2, 2)
+    vdeg, fdeg = O.quadrature_degrees(N, mesh.N_geo, TET, False)
+    od0 = O.OracleDiscretization(mesh, N, True, 0.0, 0.0, vol_deg=vdeg, face_deg=fdeg)
+    st = rand_state(od0, rng, mesh.K)
+    scale = sum(float(np.abs(a).sum()) for a in st.fields())
+    assert abs(energy_rate(st, od0)) < 1e-14 * scale
+    tau_p, tau_u = 0.7, 1.3
+    od = O.OracleDiscretization(mesh, N, True, tau_p, tau_u, vol_deg=vdeg, face_deg=fdeg)
+    dE = energy_rate(st, od)
+    bc = od.bc_mask
+    pM, pP = od.face_traces(st.p)
+    uM, uP = zip(*[od.face_traces(a) for a in st.u])
+    pP = np.where(bc, -pM, pP)
+    uP = [np.where(bc, a, b) for a, b in zip(uM, uP)]
+    n = od.geo.nq
+    dun = sum((uP[i] - uM[i]) * n[i] for i in range(3))
+    quad = np.sum(od.ref.wfq[None, :] * od.geo.Jfq * (tau_p * (pP - pM) ** 2 + tau_u * dun ** 2))
+    assert dE == pytest.approx(-0.25 * quad, rel=1e-5)
+    assert dE < 0
+
+
 def test_wadg_exact_on_affine_elements(rng):
     """J constant per element: Pq diag(1/J) Vq r == r / J (the exact mass
     inverse), for both fields (c^2 = 1)."""
@@ -189,3 +222,22 @@ def test_wadg_and_exact_mass_errors_agree_on_curved_tets():
         W = od.ref.wq[None, :] * od.geo.Jq
         errs.append(np.sqrt(np.sum(W * (od.interp(st.p) - pex) ** 2)))
     assert 0.99 <= errs[0] / errs[1] <= 1.01
+
+
+def test_submesh_patch_reproduces_element_rhs(rng):
+    """The helper behind the full-size sampled GPU parity test: the oracle
+    RHS of an element computed on its one-neighbour patch equals the RHS on
+    the whole mesh (heterogeneous medium, curved tets)."""
+    from conftest import submesh
+    c2 = lambda x, y, z: 1 + 0.5 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y) * np.sin(2 * np.pi * z)
+    mesh = meshgen.warped_cube_tet_mesh(4, 2)
+    od = O.OracleDiscretization(mesh, 2, True, 0.7, 1.3, c2=c2)
+    st = rand_state(od, rng, mesh.K)
+    full = O.rhs_full(st, od).fields()
+    elems = np.array([0, 7, 100, 200, mesh.K - 1])
+    sub, patch, loc = submesh(mesh, elems)
+    assert sub.K < mesh.K
+    osub = O.OracleDiscretization(sub, 2, True, 0.7, 1.3, c2=c2)
+    part = O.rhs_full(O.State(st.p[patch], [a[patch] for a in st.u]), osub).fields()
+    for x, y in zip(part, full):
+        assert np.max(np.abs(x[loc] - y[elems])) < 1e-12 * np.abs(y).max()

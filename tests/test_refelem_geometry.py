@@ -185,3 +185,62 @@ def test_mesh_json_round_trip(tmp_path):
     assert m2.shape is TET and m2.K == mesh.K
     assert np.array_equal(m2.face_orientation, mesh.face_orientation)
     assert np.max(np.abs(m2.elem_map_nodes - mesh.elem_map_nodes)) == 0
+
+
+@pytest.mark.parametrize("N,N_geo", [(2, 2), (3, 2), (3, 3), (4, 4)])
+def test_discrete_divergence_theorem_curved_tets(N, N_geo, rng):
+    """R/pkg/tests/test_geometry.py:116-137 transplanted to curved tets under
+    the 3D sufficiency rules (volume 2N + 2N_geo - 3, face 2N + 2N_geo - 2):
+    the volume quadrature of J div u equals the face quadrature of u.n sJ for
+    random u in (P^N)^3, to 1e-10.  This pins the cofactor metric terms, the
+    Nanson normals, sJ, the collapsed tet / triangle rules and the face
+    parametrisation of the shared 3D setup independently of the solver."""
+    import wadg_oracle as O
+    mesh = meshgen.warped_cube_tet_mesh(2, N_geo)
+    vdeg, fdeg = O.quadrature_degrees(N, N_geo, TET, False)
+    ref = refelem.build_reference_element(N, TET, vdeg, fdeg)
+    g = geometry.compute_geometric_data(mesh, ref)
+    u = [rng.standard_normal((mesh.K, ref.Np)) for _ in range(3)]
+    divJ = sum((u[i] @ ref.Dq[a].T) * (g.Gq[a, i] * g.Jq) for a in range(3) for i in range(3))
+    vol = divJ @ ref.wq
+    un = sum((u[i] @ ref.Vfq.T) * g.nq[i] for i in range(3))
+    surf = (un * g.Jfq) @ ref.wfq
+    assert np.max(np.abs(vol - surf)) < 1e-10
+    # the warp is genuinely curved: with N_geo = 4 the default 2N+1 rules are below
+    # the face degree N + 2 N_geo - 2 of u.n sJ, and the identity fails
+    if N_geo >= 4:
+        ref_lo = refelem.build_reference_element(N, TET, 2 * N + 1, 2 * N + 1)
+        g_lo = geometry.compute_geometric_data(mesh, ref_lo)
+        divJ = sum((u[i] @ ref_lo.Dq[a].T) * (g_lo.Gq[a, i] * g_lo.Jq) for a in range(3) for i in range(3))
+        un = sum((u[i] @ ref_lo.Vfq.T) * g_lo.nq[i] for i in range(3))
+        assert np.max(np.abs(divJ @ ref_lo.wq - (un * g_lo.Jfq) @ ref_lo.wfq)) > 1e-8
+
+
+def test_tet_operators_exact_on_polynomials():
+    """Reference tet operators against closed forms: Vq interpolates, Dq
+    differentiates and Pq projects every monomial of total degree <= N exactly;
+    the volume rule integrates r^a s^b t^c exactly up to its degree."""
+    from math import factorial
+    N = 4
+    ref = refelem.build_reference_element(N, TET)
+    r, s, t = ref.nodes.T
+    rq, sq, tq = ref.volume_quad.points.T
+    for a in range(N + 1):
+        for b in range(N + 1 - a):
+            for c in range(N + 1 - a - b):
+                f = r ** a * s ** b * t ** c
+                fq = rq ** a * sq ** b * tq ** c
+                assert np.max(np.abs(ref.Vq @ f - fq)) < 1e-12
+                d = [a * rq ** max(a - 1, 0) * sq ** b * tq ** c, b * rq ** a * sq ** max(b - 1, 0) * tq ** c,
+                     c * rq ** a * sq ** b * tq ** max(c - 1, 0)]
+                for k in range(3):
+                    assert np.max(np.abs(ref.Dq[k] @ f - d[k])) < 1e-10
+                assert np.max(np.abs(ref.Pq @ fq - f)) < 1e-11
+    # exact integral over the bi-unit tet {r,s,t >= -1, r+s+t <= -1} of (1+r)^a (1+s)^b (1+t)^c
+    # = 2^(a+b+c+3) a! b! c! / (a+b+c+3)!
+    for a, b, c in [(0, 0, 0), (2, 1, 0), (3, 3, 3), (5, 2, 2)]:
+        if a + b + c > 2 * N + 1:
+            continue
+        exact = 2.0 ** (a + b + c + 3) * factorial(a) * factorial(b) * factorial(c) / factorial(a + b + c + 3)
+        got = ref.wq @ ((1 + rq) ** a * (1 + sq) ** b * (1 + tq) ** c)
+        assert got == pytest.approx(exact, rel=1e-13)
