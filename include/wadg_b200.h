@@ -86,6 +86,7 @@ typedef struct wadg_problem {
      * operators repacked into quadrature chunks of QC points (see
      * wadg_fused_config), NPP = Np rounded up to 4, zero padded:          */
     int32_t order;
+    int32_t fused_kind;   /* kernel the operators below are packed for: 0 CUDA cores, 2 tcgen05 */
     const void *opVA;     /* D_r, D_s, D_t, Vq at (q, j)   (layout: wadg_fused_config) */
     const void *opVB;     /* DTW_r, DTW_s, DTW_t, Pq at (j, q)                         */
     const void *opU1;     /* Vu                                                        */

@@ -34,7 +34,7 @@ class WadgProblem(ctypes.Structure):
         ("nbr", _vp), ("ncode", _vp),
         ("halo", _vp), ("n_halo", _i32),
         ("Ne", _i32), ("Ve", _vp), ("we", _vp), ("ewp", _vp), ("ewu", _vp), ("e_recip", _i32),
-        ("order", _i32), ("opVA", _vp), ("opVB", _vp), ("opU1", _vp), ("opU2", _vp), ("liftT", _vp),
+        ("order", _i32), ("fused_kind", _i32), ("opVA", _vp), ("opVB", _vp), ("opU1", _vp), ("opU2", _vp), ("liftT", _vp),
         ("geo_il", _vp), ("fgeo_il", _vp), ("wu_il", _vp), ("wp_il", _vp), ("wbar", _vp),
         ("minv_p", _vp), ("minv_u", _vp),
     ]

@@ -26,8 +26,6 @@
 namespace wadg {
 }
 #include "wadg_fused.cuh"
-#include "wadg_mma.cuh"
-#include "wadg_fused_tc.cuh"
 #include "wadg_umma.cuh"
 #include "wadg_fused_umma.cuh"
 
@@ -739,7 +737,20 @@ static fused::FProb<T> make_fprob(const wadg_problem &p) {
     return q;
 }
 
-static int g_fused_variant = -1;   // debug override: 0 CUDA-core, 1 mma.sync, 2 tcgen05, -1 default
+static int g_fused_variant = -1;   // debug override of the packing choice: 0 CUDA-core, 2 tcgen05, -1 default
+
+// cudaFuncSetAttribute (max dynamic shared memory) is per device: one flag per
+// (kernel instantiation, device)
+static bool attr_once(bool (&done)[64], const void *fn, size_t smem) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+    if (!done[dev]) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return false;
+        done[dev] = true;
+    }
+    return true;
+}
 
 // tcgen05 (TMEM / TMA) fused stage: fp32, orders whose 128-element tile fits
 template <typename T, int N>
@@ -755,21 +766,6 @@ static bool use_umma() {
     if (!umma_available<T, N>()) return false;
     if (g_fused_variant >= 0) return g_fused_variant == 2;
     return true;
-}
-
-// tensor-core (split-TF32 mma.sync) fused stage: fp32, orders with a 64-element tile
-template <typename T, int N>
-static constexpr bool tc_available() {
-    return sizeof(T) == 4 && N >= 2 && N <= 4;
-}
-
-// default per order, from B200 A/B timings: the
-// tensor-core kernel wins at N = 2 and 4, the CUDA-core kernel at N = 3
-template <typename T, int N>
-static bool use_tc() {
-    if (!tc_available<T, N>()) return false;
-    if (g_fused_variant >= 0) return g_fused_variant == 1;
-    return N != 3;
 }
 
 // info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),
@@ -788,15 +784,6 @@ static int fused_cfg(int32_t *info, int64_t *smem) {
             done = true;
         }
     }
-    if constexpr (tc_available<T, N>()) {
-        if (!done && use_tc<T, N>()) {
-            using C = tc::CfgTC<N>;
-            const int32_t w[8] = {1, C::KB, C::QC, C::NCH, C::NPP, C::QCS, C::NJS, C::NFQ8};
-            for (int i = 0; i < 8; ++i) v[i] = w[i];
-            sm = C::SMEM;
-            done = true;
-        }
-    }
     if (!done) {
         using C = fused::Cfg<T, N>;
         const int32_t w[8] = {0, C::KB, C::QC, C::NCH, C::NPP, C::QC, C::NPP, C::NFQ};
@@ -807,28 +794,6 @@ static int fused_cfg(int32_t *info, int64_t *smem) {
         for (int i = 0; i < 8; ++i) info[i] = v[i];
     if (smem) *smem = (int64_t)sm;
     return sm <= 227 * 1024 ? 0 : 1;
-}
-
-template <int N>
-static int fused_launch_tc(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
-                           double tu, double a, double b, double dt, int b0, int b1, cudaStream_t st) {
-    using C = tc::CfgTC<N>;
-    if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
-    const int nblk = Pc->Kpad / C::KB;
-    if (b1 < 0 || b1 > nblk) b1 = nblk;
-    if (b0 < 0) b0 = 0;
-    if (b1 <= b0) return 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(tc::k_stage_fused_tc<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)C::SMEM);
-        if (e != cudaSuccess) return fail(cudaGetErrorString(e));
-        attr_set = true;
-    }
-    tc::k_stage_fused_tc<N><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin,
-                                                           (float *)Qout, (float *)res, (float)tp, (float)tu,
-                                                           (float)a, (float)b, (float)dt, b0);
-    return check_launch("wadg_stage_fused(tc)");
 }
 
 template <int N, int LAY>
@@ -842,13 +807,9 @@ static int launch_umma_lay(const wadg_problem *Pc, const void *Qin, void *Qout, 
     if (b1 < 0 || b1 > nblk) b1 = nblk;
     if (b0 < 0) b0 = 0;
     if (b1 <= b0) return 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(uk::k_stage_umma<N, LAY>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-        if (e != cudaSuccess) return fail(cudaGetErrorString(e));
-        attr_set = true;
-    }
+    static bool attr_set[64] = {};
+    if (!attr_once(attr_set, (const void *)uk::k_stage_umma<N, LAY>, C::SMEM))
+        return fail("cudaFuncSetAttribute failed for the tcgen05 stage");
     // programmatic dependent launch: consecutive stage kernels on a stream overlap
     // the next one's prologue with this one's tail (the kernel waits on
     // griddepcontrol.wait before touching data the previous kernel wrote)
@@ -883,13 +844,15 @@ static int fused_launch_umma(const wadg_problem *Pc, const void *Qin, void *Qout
 template <typename T, int N>
 static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
                         double tu, double a, double b, double dt, int b0, int b1, int lay, cudaStream_t st) {
-    if constexpr (umma_available<T, N>()) {
-        if (use_umma<T, N>()) return fused_launch_umma<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, lay, st);
+    // dispatch on the kernel kind the operators were packed for (P->fused_kind),
+    // not on the current packing preference
+    if (Pc->fused_kind == 2) {
+        if constexpr (umma_available<T, N>())
+            return fused_launch_umma<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, lay, st);
+        return fail("operators packed for the tcgen05 stage, which is not compiled for this dtype / order");
     }
+    if (Pc->fused_kind != 0) return fail("unknown fused_kind");
     if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
-    if constexpr (tc_available<T, N>()) {
-        if (use_tc<T, N>()) return fused_launch_tc<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
-    }
     using C = fused::Cfg<T, N>;
     if (C::SMEM > 227 * 1024) return fail("fused stage does not fit shared memory for this order");
     if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
@@ -897,13 +860,9 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
     if (b1 < 0 || b1 > nblk) b1 = nblk;
     if (b0 < 0) b0 = 0;
     if (b1 <= b0) return 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(fused::k_stage_fused<T, N>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-        if (e != cudaSuccess) return fail(cudaGetErrorString(e));
-        attr_set = true;
-    }
+    static bool attr_set[64] = {};
+    if (!attr_once(attr_set, (const void *)fused::k_stage_fused<T, N>, C::SMEM))
+        return fail("cudaFuncSetAttribute failed for the fused stage");
     fused::k_stage_fused<T, N><<<b1 - b0, fused::NTF, C::SMEM, st>>>(
         make_fprob<T>(*Pc), (const T *)Qin, (T *)Qout, (T *)res, (T)tp, (T)tu, (T)a, (T)b, (T)dt, b0);
     return check_launch("wadg_stage_fused");
@@ -1075,7 +1034,7 @@ int wadg_debug_set_phase_clock_buffer(void *buf) {
 }
 
 int wadg_debug_set_fused_variant(int variant) {
-    if (variant < -1 || variant > 2) return fail("variant must be -1, 0, 1 or 2");
+    if (variant != -1 && variant != 0 && variant != 2) return fail("variant must be -1, 0 or 2");
     g_fused_variant = variant;
     return 0;
 }
@@ -1201,32 +1160,6 @@ __global__ void __launch_bounds__(256) k_mma_tf32_peak(const float *__restrict__
 extern "C" int wadg_microbench_mma_tf32(int blocks, int iters, const void *in, void *out, void *stream) {
     wadg::k_mma_tf32_peak<<<blocks, 256, 0, (cudaStream_t)stream>>>((const float *)in, (float *)out, iters);
     return check_launch("wadg_microbench_mma_tf32");
-}
-
-// Debug: one warp, C(16 x 8) = A(16 x K) B(K x 8) with 3xTF32 mma.sync; A given
-// column-major (A[k*16 + r]), B row-major (B[k*8 + n]), K a multiple of 8.
-namespace wadg {
-__global__ void k_mma_test(const float *A, const float *B, float *C, int K) {
-    const int lane = threadIdx.x;
-    float c[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int k0 = 0; k0 < K; k0 += 8) {
-        mma::AFrag a;
-        mma::BFrag b;
-        mma::load_a_colmajor(a, A + k0 * 16, 16, lane);
-        mma::load_b_rowmajor(b, B + k0 * 8, 8, lane);
-        mma::mma3(c, a, b);
-    }
-    const int g = lane >> 2, t = lane & 3;
-    C[g * 8 + 2 * t] = c[0];
-    C[g * 8 + 2 * t + 1] = c[1];
-    C[(g + 8) * 8 + 2 * t] = c[2];
-    C[(g + 8) * 8 + 2 * t + 1] = c[3];
-}
-}  // namespace wadg
-
-extern "C" int wadg_debug_mma_test(const void *A, const void *B, void *C, int K, void *stream) {
-    wadg::k_mma_test<<<1, 32, 0, (cudaStream_t)stream>>>((const float *)A, (const float *)B, (float *)C, K);
-    return check_launch("wadg_debug_mma_test");
 }
 
 // Debug / validation of the tcgen05 primitives (wadg_umma.cuh): one CTA of 128

@@ -23,6 +23,7 @@ import numpy as np
 import torch
 
 from . import _native, geometry, refelem
+from .errors import ConfigError
 
 PAD = 128
 CHUNK = 1 << 16
@@ -82,6 +83,29 @@ def interleave_blocks(x, npad, blk=128):
     out = xp.view(rows, npad // 4, 4, Kp // blk, blk).permute(3, 0, 1, 4, 2).contiguous()
     del xp
     return out
+
+
+def medium_on_device(c2, xq, shape):
+    """c^2 at the points xq (torch tensors on the device), as a float64 tensor
+    of ``shape``.  A callable is evaluated on the device tensors (torch
+    expressions stay on the GPU); a numpy-only callable falls back to a host
+    evaluation of the same points.  Non-positive or non-finite values raise
+    ConfigError, like the reference's MediumField (R/.../solver.py:62-63)."""
+    dev = xq[0].device
+    if not callable(c2):
+        v = torch.full(shape, float(c2), dtype=torch.float64, device=dev)
+    else:
+        try:
+            v = c2(*xq)
+            if not isinstance(v, torch.Tensor):
+                raise TypeError("numpy result")
+            v = v.to(device=dev, dtype=torch.float64).expand(shape)
+        except (TypeError, RuntimeError, AttributeError):
+            xyz = [a.cpu().numpy() for a in xq]
+            v = torch.as_tensor(np.array(np.broadcast_to(np.asarray(c2(*xyz), dtype=float), shape)), device=dev)
+    if not bool(torch.all(torch.isfinite(v) & (v > 0))):
+        raise ConfigError("wavespeed squared must be positive")
+    return v
 
 
 def tf32_split(a, mode=None):
@@ -241,11 +265,7 @@ class DeviceProblem:
             Ju = gu["J"]
             self.wu[:, c0:c1] = (1.0 / Ju).T.to(dt)
             if self.variable_c2:
-                xyz = [a.cpu().numpy() for a in gu["xq"]]
-                cv = np.array(np.broadcast_to(np.asarray(c2(*xyz), dtype=float), Ju.shape))
-                if np.any(cv <= 0) or not np.all(np.isfinite(cv)):
-                    raise ValueError("wavespeed squared must be positive")
-                self.wp[:, c0:c1] = (torch.as_tensor(cv, device=dev) / Ju).T.to(dt)
+                self.wp[:, c0:c1] = (medium_on_device(c2, gu["xq"], Ju.shape) / Ju).T.to(dt)
             del g, gu, X
         nbr, ncode = neighbour_tables(self.mesh, self.n_orient, self.k0, self.k1, self.halo)
         self.nbr = torch.full((ref.n_faces, Kp), -1, dtype=torch.int32, device=dev)
@@ -279,11 +299,7 @@ class DeviceProblem:
                                            dtype=np.float64), device=dev)
             g = geometry.geometric_factors(X, mm, k_offset=self.k0 + c0)
             J = g["J"]
-            if callable(c2):
-                xyz = [a.cpu().numpy() for a in g["xq"]]
-                cv = torch.as_tensor(np.array(np.broadcast_to(np.asarray(c2(*xyz), dtype=float), J.shape)), device=dev)
-            else:
-                cv = float(c2)
+            cv = medium_on_device(c2, g["xq"], J.shape)
             for w, dst in ((J / cv, self.minv_p), (J, self.minv_u)):
                 M = torch.einsum("kq,qi,qj->kij", w * wq, Vq, Vq)
                 M = 0.5 * (M + M.transpose(1, 2))
@@ -351,46 +367,31 @@ class DeviceProblem:
             s.wbar = self.wbar.data_ptr() if self.wbar is not None else None
             self.fused_kind = 2
             self.struct.order = N
+            self.struct.fused_kind = 2
             return kb
-        if cfg["kind"] == 0:                    # CUDA-core kernel layouts
-            NPP = roundup(NP, 4)
-            NQP = nch * qc
-            A = np.zeros((NQP, NPP, 4))
-            A[:NQ, :NP] = np.stack(list(ref.Dq) + [ref.Vq], axis=-1)
-            opVA = A.reshape(nch, qc, NPP, 4).transpose(0, 2, 1, 3)
-            B = np.zeros((NPP, NQP, 4))
-            B[:NP, :NQ] = np.stack(DTW + [ref.Pq], axis=-1)
-            opVB = B.reshape(NPP, nch, qc, 4).transpose(1, 2, 0, 3)
-            U1 = np.zeros((NQP, NPP))
-            U1[:NQ, :NP] = ru.Vq
-            opU1 = U1.reshape(nch, qc, NPP).transpose(0, 2, 1)
-            U2 = np.zeros((NPP, NQP))
-            U2[:NP, :NQ] = ru.Pq
-            opU2 = U2.reshape(NPP, nch, qc).transpose(1, 2, 0)
-            L = np.zeros((nf * nfq, NPP))
-            L[:, :NP] = ref.Pfq.T
-        else:                                   # tensor-core kernel layouts (padded strides)
-            NPP, QCS, NJS, NFQ8 = cfg["npp"], cfg["qcs"], cfg["njs"], cfg["nfq8"]
-            opVA = np.zeros((nch, 4, NPP, QCS))
-            opVB = np.zeros((nch, 4, qc, NJS))
-            opU1 = np.zeros((nch, NPP, QCS))
-            opU2 = np.zeros((nch, qc, NJS))
-            ops_q = list(ref.Dq) + [ref.Vq]              # (NQ, NP) each
-            ops_j = DTW + [ref.Pq]                       # (NP, NQ) each
-            for ch in range(nch):
-                q0, q1 = ch * qc, min(NQ, (ch + 1) * qc)
-                for m in range(4):
-                    opVA[ch, m, :NP, :q1 - q0] = ops_q[m][q0:q1].T
-                    opVB[ch, m, :q1 - q0, :NP] = ops_j[m][:, q0:q1].T
-                opU1[ch, :NP, :q1 - q0] = ru.Vq[q0:q1].T
-                opU2[ch, :q1 - q0, :NP] = ru.Pq[:, q0:q1].T
-            L = np.zeros((nf, NFQ8, NJS))
-            L[:, :nfq, :NP] = ref.Pfq.T.reshape(nf, nfq, NP)
+        # CUDA-core kernel layouts (kind 0)
+        NPP = roundup(NP, 4)
+        NQP = nch * qc
+        A = np.zeros((NQP, NPP, 4))
+        A[:NQ, :NP] = np.stack(list(ref.Dq) + [ref.Vq], axis=-1)
+        opVA = A.reshape(nch, qc, NPP, 4).transpose(0, 2, 1, 3)
+        B = np.zeros((NPP, NQP, 4))
+        B[:NP, :NQ] = np.stack(DTW + [ref.Pq], axis=-1)
+        opVB = B.reshape(NPP, nch, qc, 4).transpose(1, 2, 0, 3)
+        U1 = np.zeros((NQP, NPP))
+        U1[:NQ, :NP] = ru.Vq
+        opU1 = U1.reshape(nch, qc, NPP).transpose(0, 2, 1)
+        U2 = np.zeros((NPP, NQP))
+        U2[:NP, :NQ] = ru.Pq
+        opU2 = U2.reshape(NPP, nch, qc).transpose(1, 2, 0)
+        L = np.zeros((nf * nfq, NPP))
+        L[:, :NP] = ref.Pfq.T
         for name, arr in (("opVA", opVA), ("opVB", opVB), ("opU1", opU1), ("opU2", opU2), ("liftT", L)):
             self.ops[name] = self._t(arr)
             setattr(self.struct, name, self.ops[name].data_ptr())
-        self.fused_kind = cfg["kind"]
+        self.fused_kind = 0
         self.struct.order = N
+        self.struct.fused_kind = 0
         if self.Kpad % kb:
             return None
         return kb
@@ -410,12 +411,7 @@ class DeviceProblem:
                                            dtype=np.float64), device=dev)
             g = geometry.geometric_factors(X, mv, check=False)
             J = g["J"]
-            if callable(c2):
-                xyz = [a.cpu().numpy() for a in g["xq"]]
-                cv = torch.as_tensor(np.broadcast_to(np.asarray(c2(*xyz), dtype=float), J.shape),
-                                     device=dev)
-            else:
-                cv = float(c2)
+            cv = medium_on_device(c2, g["xq"], J.shape)
             self.ewp[:, c0:c1] = (J / cv).T.to(dt)
             self.ewu[:, c0:c1] = J.T.to(dt)
         self.ops["Ve"] = self._t(ref.Vq)

@@ -19,6 +19,7 @@ import json
 from dataclasses import dataclass, field
 
 import numpy as np
+import torch
 
 from . import refelem
 from .refelem import ElementShape
@@ -74,9 +75,18 @@ def build_connectivity(elem_vertices, shape):
     nf, nvf = fv.shape
     fverts = elem_vertices[:, fv]                                # (K, nf, nvf)
     keys = np.sort(fverts, axis=2).reshape(K * nf, nvf)
-    order = np.lexsort(keys.T[::-1])
-    sk = keys[order]
-    same = np.all(sk[1:] == sk[:-1], axis=1)
+    nbits = max(1, int(elem_vertices.max()).bit_length())
+    if nbits * nvf <= 62:       # one packed int64 key per face: a single sort instead of a lexsort
+        packed = np.zeros(K * nf, dtype=np.int64)
+        for c in range(nvf):
+            packed = (packed << nbits) | keys[:, c]
+        order = np.argsort(packed, kind="stable")
+        sp = packed[order]
+        same = sp[1:] == sp[:-1]
+    else:
+        order = np.lexsort(keys.T[::-1])
+        sk = keys[order]
+        same = np.all(sk[1:] == sk[:-1], axis=1)
     if np.any(same[1:] & same[:-1]):
         raise ValueError("non-manifold mesh: a face is shared by more than two elements")
     conn = np.full((K * nf, 2), -1, dtype=np.int64)
@@ -110,10 +120,13 @@ def build_connectivity(elem_vertices, shape):
 
 def _simplex_map_nodes(shape, N_geo, corner_xyz):
     """Affine placement of the reference node set in each simplex.
-    corner_xyz: (K, dim+1, dim) physical vertices in reference-vertex order."""
+    corner_xyz: (K, dim+1, dim) physical vertices in reference-vertex order
+    (numpy, or a torch tensor for large meshes: one multi-threaded matmul)."""
     nodes = refelem.interpolation_nodes(shape, N_geo)
     lam_rest = 0.5 * (1.0 + nodes)                                # (Npg, dim)
     lam = np.concatenate([1.0 - lam_rest.sum(axis=1, keepdims=True), lam_rest], axis=1)
+    if isinstance(corner_xyz, torch.Tensor):
+        return torch.matmul(torch.from_numpy(lam).to(corner_xyz.dtype), corner_xyz)   # (K, Npg, dim)
     return np.einsum("nv,kvd->knd", lam, corner_xyz)
 
 
@@ -198,12 +211,14 @@ def _kuhn_local():
 
 def warp_cube(x, y, z, amp=0.1):
     """BASELINE configs 2-5 warp, read as cyclic permutations:
-    x += a cos(pi x/2) cos(3 pi y/2) cos(pi z/2), y and z cyclically."""
-    c = lambda v: np.cos(0.5 * np.pi * v)
-    c3 = lambda v: np.cos(1.5 * np.pi * v)
-    return (x + amp * c(x) * c3(y) * c(z),
-            y + amp * c(y) * c3(z) * c(x),
-            z + amp * c(z) * c3(x) * c(y))
+    x += a cos(pi x/2) cos(3 pi y/2) cos(pi z/2), y and z cyclically.
+    Works on numpy arrays or torch tensors; each cosine is evaluated once."""
+    cos = torch.cos if isinstance(x, torch.Tensor) else np.cos
+    cx, cy, cz = (cos(0.5 * np.pi * v) for v in (x, y, z))
+    c3x, c3y, c3z = (cos(1.5 * np.pi * v) for v in (x, y, z))
+    return (x + amp * cx * c3y * cz,
+            y + amp * cy * c3z * cx,
+            z + amp * cz * c3x * cy)
 
 
 def warped_cube_tet_mesh(n, N_geo, amp=0.1, nz=None, z_range=None, domain=(-1.0, 1.0)):
@@ -230,9 +245,11 @@ def warped_cube_tet_mesh(n, N_geo, amp=0.1, nz=None, z_range=None, domain=(-1.0,
     corners = corners.reshape(nz, n * n, 6, 4, 3).transpose(0, 2, 1, 3, 4).reshape(-1, 4, 3)
     vid = (corners[..., 2] * (n + 1) + corners[..., 1]) * (n + 1) + corners[..., 0]
     xyz = np.stack([gx[corners[..., 0]], gx[corners[..., 1]], gz[corners[..., 2]]], axis=-1)
-    X = _simplex_map_nodes(ElementShape.Tetrahedron, N_geo, xyz)
+    # torch (multi-threaded) for the node placement and the ~10^8 cosines of a 1.5M-tet mesh
+    X = _simplex_map_nodes(ElementShape.Tetrahedron, N_geo, torch.from_numpy(xyz))
     if amp != 0.0:
-        X = np.stack(warp_cube(X[..., 0], X[..., 1], X[..., 2], amp), axis=-1)
+        X = torch.stack(warp_cube(X[..., 0], X[..., 1], X[..., 2], amp), dim=-1)
+    X = X.numpy()
     conn, tags, orient = build_connectivity(vid, ElementShape.Tetrahedron)
     prov = {"kind": "warped-kuhn-cube", "n": n, "nz": nz, "N_geo": N_geo, "amp": amp,
             "z_range": [float(zlo), float(zhi)]}

@@ -28,16 +28,9 @@ import numpy as np
 import torch
 
 from . import _native, geometry, refelem
-from .device import DeviceProblem
+from .device import DeviceProblem, medium_on_device
+from .errors import BlowUp, ConfigError  # noqa: F401  (reference names)
 from .refelem import ElementShape
-
-
-class BlowUp(Exception):
-    """Discrete energy exceeded 1e6 x initial; the run is unstable."""
-
-
-class ConfigError(ValueError):
-    """Invalid solver configuration."""
 
 
 class Formulation(enum.Enum):
@@ -306,6 +299,24 @@ def _stream():
     return ctypes_ptr(torch.cuda.current_stream().cuda_stream)
 
 
+def _on_disc_device(fn):
+    """Run a compute entry point with the Discretization's device current, so
+    the launches, their stream (_stream) and the per-device kernel attributes
+    all refer to that device even when another device is current."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kw):
+        disc = next((a for a in args if isinstance(a, Discretization)), None)
+        if disc is None and args:
+            disc = getattr(args[0], "disc", None)
+        if disc is None or not torch.cuda.is_available():
+            return fn(*args, **kw)      # no device: the call itself raises (no CPU fallback)
+        with torch.cuda.device(disc.dev.device):
+            return fn(*args, **kw)
+    return wrapper
+
+
 def ctypes_ptr(v):
     import ctypes
     return ctypes.c_void_p(v)
@@ -321,6 +332,7 @@ def _check_state(state, disc):
         raise ValueError(f"state has {len(state.fields())} fields, mesh needs {disc.dim + 1}")
 
 
+@_on_disc_device
 def _volume_terms(state, disc, strong_weak):
     _check_state(state, disc)
     d = disc.dev
@@ -332,6 +344,7 @@ def _volume_terms(state, disc, strong_weak):
     return tuple(disc.from_device(out, state, state.t).fields())
 
 
+@_on_disc_device
 def _surface_terms(state, disc, strong_weak):
     _check_state(state, disc)
     d = disc.dev
@@ -344,6 +357,7 @@ def _surface_terms(state, disc, strong_weak):
     return tuple(disc.from_device(out, state, state.t).fields())
 
 
+@_on_disc_device
 def _rhs_pre(state, disc, strong_weak):
     import ctypes
     _check_state(state, disc)
@@ -371,6 +385,7 @@ def rhs_pre_mass(state, disc):
     return _rhs_pre(state, disc, disc.strong_weak)
 
 
+@_on_disc_device
 def apply_mass_inverse(rhs_pre, disc):
     """Mass inverse on a premultiplied RHS (R/.../solver.py:290-306): matrix-free
     WADG, or the stored dense inverses of the ExactCurvedMass comparator."""
@@ -383,6 +398,7 @@ def apply_mass_inverse(rhs_pre, disc):
     return disc.from_device(out, rhs_pre, rhs_pre.t)
 
 
+@_on_disc_device
 def rhs_full(state, disc):
     """apply_mass_inverse(rhs_pre_mass(state)) in one device pass."""
     import ctypes
@@ -410,6 +426,7 @@ class _BoundRHS:
         return rhs_full(state, self.disc)
 
 
+@_on_disc_device
 def energy(state, disc):
     """1/2 int (p^2/c^2 + |u|^2) by volume quadrature (R/.../solver.py:314-321)."""
     d = disc.dev
@@ -417,6 +434,7 @@ def energy(state, disc):
     return device_energy(disc, Q)
 
 
+@_on_disc_device
 def device_energy(disc, Q):
     import ctypes
     d = disc.dev
@@ -465,6 +483,7 @@ class DeviceStepper:
         self.rhs = None if self.fused else d.empty_fields()
         self.other = d.empty_fields() if self.fused else None
 
+    @_on_disc_device
     def stage(self, Q, a, b, dt):
         import ctypes
         d = self.disc.dev
@@ -496,6 +515,7 @@ class DeviceStepper:
             Q = self.stage(Q, a, b, dt)
         return Q
 
+    @_on_disc_device
     def step_graphed(self, Q, dt):
         """``step`` replayed from a CUDA graph.  The launches of one step are
         captured once per (input buffer, dt) and replayed, which removes the
@@ -657,6 +677,7 @@ class HostPipeline:
         return all(isinstance(a, torch.Tensor) and not a.is_cuda and a.is_pinned() and a.dtype == d.dtype
                    and a.is_contiguous() and tuple(a.shape) == (d.K, d.ref.Np) for a in state.fields())
 
+    @_on_disc_device
     def step(self, state, dt):
         import ctypes
         disc, d = self.disc, self.disc.dev
@@ -752,21 +773,21 @@ def _as_cuda(a, dtype=None):
 
 
 def _generic_lsrk_step(state, dt, rhs_fn):
-    """Arbitrary rhs_fn: the state lives on the GPU as torch tensors, rhs_fn
-    is evaluated on it, and every stage axpy runs in wadg_lsrk_axpy."""
+    """Arbitrary rhs_fn: the state and the LSRK register live on the GPU and
+    every stage axpy runs in wadg_lsrk_axpy.  rhs_fn sees the state in the
+    caller's container type: a numpy FieldState for a host numpy state (as the
+    reference's lsrk_step, R/.../solver.py:348-363, passes it), device tensors
+    for CUDA tensors."""
     import ctypes
     host = not isinstance(state.p, torch.Tensor)
-    ys = [_as_cuda(a) for a in state.fields()]
-    if host:
-        ys = [a.clone() for a in ys]
-    else:
-        ys = [a.clone() for a in ys]
+    ys = [_as_cuda(a).clone() for a in state.fields()]
     res = [torch.zeros_like(a) for a in ys]
     t0 = state.t
     y = FieldState.from_fields(ys, t0)
     for a, b, c in zip(LSRK4A, LSRK4B, LSRK4C):
         y.t = t0 + c * dt
-        dfs = rhs_fn(y).fields()
+        arg = FieldState.from_fields([x.cpu().numpy() for x in ys], y.t) if host else y
+        dfs = rhs_fn(arg).fields()
         for m, dm in enumerate(dfs):
             dm = _as_cuda(dm, ys[m].dtype)
             code = _native.WADG_F64 if ys[m].dtype == torch.float64 else _native.WADG_F32
@@ -829,8 +850,11 @@ def _projection_chunks(mesh, N, initial_fn, dev, k0=0, k1=None, chunk=None):
 def project_initial_condition(mesh, config, initial_fn, medium=MediumField()):
     """L2-project the initial fields with a mass-exact quadrature
     (R/.../solver.py:379-389).  Setup step: dense per-element solves in
-    element chunks (torch, on the GPU when present); returns host arrays."""
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    element chunks on the GPU; returns host arrays.  Needs CUDA like every
+    other compute entry point (no CPU fallback)."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("project_initial_condition needs a CUDA device (no CPU fallback)")
+    dev = "cuda"
     nf = mesh.shape.dim + 1
     out = [np.empty((mesh.K, refelem.basis_dimension(mesh.shape, config.N))) for _ in range(nf)]
     for c0, c1, cs in _projection_chunks(mesh, config.N, initial_fn, dev):
@@ -852,10 +876,49 @@ def project_initial_condition_device(disc, initial_fn):
 
 
 def global_l2_error(ref, geo, coeffs, exact_fn):
-    """sqrt(sum w J (u_h - u)^2) (R/.../operators.py:103-107)."""
+    """sqrt(sum w J (u_h - u)^2) (R/.../operators.py:103-107), host arrays."""
     uq = np.atleast_2d(coeffs) @ ref.Vq.T
     fq = exact_fn(*geo.xyzq)
     return float(np.sqrt(np.sum(ref.wq[None, :] * geo.Jq * (uq - fq) ** 2)))
+
+
+def _field_values(fn, xq, shape, dev):
+    """fn(*xq) as a float64 device tensor: torch expressions run on the device,
+    a numpy-only callable is evaluated on a host copy of the points."""
+    try:
+        v = fn(*xq)
+        if not isinstance(v, torch.Tensor):
+            raise TypeError("numpy result")
+        return v.to(device=dev, dtype=torch.float64).expand(shape)
+    except (TypeError, RuntimeError, AttributeError):
+        xyz = [a.cpu().numpy() for a in xq]
+        return torch.as_tensor(np.array(np.broadcast_to(np.asarray(fn(*xyz), dtype=float), shape)), device=dev)
+
+
+@_on_disc_device
+def device_l2_error(disc, Q, exact_fn, ref_err=None, chunk=1 << 15):
+    """global_l2_error of the pressure field resident on the device (field
+    layout Q[0], (Np, Kpad)): the error quadrature's geometry is rebuilt on
+    the device in element chunks and the sum reduced there; only the scalar
+    comes back to the host."""
+    d = disc.dev
+    mesh, N = disc.mesh, disc.config.N
+    if ref_err is None:
+        ref_err = refelem.build_reference_element(N, mesh.shape, volume_quad_degree=2 * N + 4,
+                                                  face_quad_degree=1)
+    mops = geometry.map_operators(mesh.shape, mesh.N_geo, ref_err).to(d.device)
+    Vq = torch.as_tensor(ref_err.Vq, dtype=torch.float64, device=d.device)
+    wq = torch.as_tensor(ref_err.wq, dtype=torch.float64, device=d.device)
+    total = torch.zeros((), dtype=torch.float64, device=d.device)
+    for c0 in range(0, d.K, chunk):
+        c1 = min(d.K, c0 + chunk)
+        X = torch.as_tensor(np.asarray(mesh.elem_map_nodes[d.k0 + c0:d.k0 + c1], dtype=np.float64),
+                            device=d.device)
+        g = geometry.geometric_factors(X, mops, check=False)
+        uq = Q[0, :, c0:c1].to(torch.float64).T @ Vq.T
+        f = _field_values(exact_fn, g["xq"], g["J"].shape, d.device)
+        total += torch.sum(wq[None, :] * g["J"] * (uq - f) ** 2)
+    return float(torch.sqrt(total))
 
 
 def run(mesh, config, initial_fn, T, medium=MediumField(), exact_p=None, n_outputs=10, dt=None):
@@ -872,21 +935,19 @@ def run(mesh, config, initial_fn, T, medium=MediumField(), exact_p=None, n_outpu
     stepper = DeviceStepper(disc)
     sample_ts = np.linspace(0.0, T, n_outputs + 1)
     diag = {"t": [], "energy": [], "l2_error_p": []}
-    ref_err = geo_err = None
+    ref_err = None
     if exact_p is not None:
         ref_err = refelem.build_reference_element(
             config.N, mesh.shape, volume_quad_degree=2 * config.N + 4, face_quad_degree=1)
-        geo_err = geometry.compute_geometric_data(mesh, ref_err)
     t = 0.0
 
     def record(t):
+        # energy and pressure error are device reductions; only scalars reach the host
         e = device_energy(disc, Q)
         diag["t"].append(t)
         diag["energy"].append(e)
         if exact_p is not None:
-            p = Q[0, :, :disc.dev.K].T.to(torch.float64).cpu().numpy()
-            diag["l2_error_p"].append(global_l2_error(
-                ref_err, geo_err, p, lambda *xyz: exact_p(*xyz, t)))
+            diag["l2_error_p"].append(device_l2_error(disc, Q, lambda *xyz: exact_p(*xyz, t), ref_err))
         return e
 
     e0 = record(t)

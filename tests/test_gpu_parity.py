@@ -104,6 +104,15 @@ def test_generic_rhs_fn_and_scalar_lsrk():
     want = O.lsrk_step(O.State(np.array([[1.0]]), [np.zeros((1, 1))] * 2), dt,
                        lambda s: O.State(lam * s.p, [0 * a for a in s.u]))
     assert out.p[0, 0] == pytest.approx(want.p[0, 0], abs=1e-15)
+    # a numpy-only callable (np.sin, ndarray @) gets a numpy FieldState, as in the reference
+    A = np.array([[0.3, -0.1], [0.2, 0.5]])
+    st2 = FieldState(np.array([[0.4, -0.2]]), np.array([[0.1, 0.3]]), np.zeros((1, 2)))
+    f = lambda s: FieldState(np.sin(s.p) @ A, s.u1 @ A.T, 0 * s.u2)
+    got = solver.lsrk_step(st2, 0.1, f)
+    want = O.lsrk_step(O.State(st2.p.copy(), [st2.u1.copy(), st2.u2.copy()]), 0.1,
+                       lambda s: O.State(np.sin(s.p) @ A, [s.u[0] @ A.T, 0 * s.u[1]]))
+    assert isinstance(got.p, np.ndarray)
+    assert rel(got.fields(), want.fields()) < 1e-14
     g, mesh, disc = golden_disc("tri_strong_het")
     st = FieldState(*gfields(g, "ic"))
     a = solver.lsrk_step(st, 1e-3, lambda s: solver.rhs_full(s, disc))
@@ -249,31 +258,34 @@ def test_two_slab_halo_path_is_bitwise_single_domain(dtype, fused, rng):
 
 @pytest.mark.parametrize("N", [2, 3, 4])
 def test_tensor_core_and_cuda_core_fused_kernels_agree(N, rng):
-    """fp32: the split-TF32 tcgen05 and mma.sync fused stages and the CUDA-core
-    FMA one give the same 2 steps to fp32 rounding, and all match the oracle."""
+    """fp32: the split-TF32 tcgen05 fused stage and the CUDA-core FMA one give
+    the same 2 steps to fp32 rounding, and both match the oracle.  The packing
+    choice is a debug switch; the launch follows what the operators were packed
+    for (wadg_problem.fused_kind), so flipping the switch after a
+    Discretization exists does not change which kernel it runs."""
     from paper_1608_03836_b200 import _native
     mesh = meshgen.warped_cube_tet_mesh(3, N)
     cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype="float32")
     fl = _state3(mesh.K, refelem_np(N), rng)
     outs = {}
     try:
-        for v in (0, 1, 2):
+        for v in (0, 2):
             _native.call("wadg_debug_set_fused_variant", v)
             disc = solver.Discretization(mesh, cfg)
-            assert disc.dev.fused_kind == v
+            assert disc.dev.fused_kind == v and disc.dev.struct.fused_kind == v
+            _native.call("wadg_debug_set_fused_variant", 2 - v)     # must not affect this disc
             st = FieldState.from_fields(fl)
             for _ in range(2):
                 st = solver.lsrk_step(st, 2e-3, disc.rhs)
             outs[v] = st.fields()
     finally:
         _native.call("wadg_debug_set_fused_variant", -1)
-    assert rel(outs[0], outs[1]) < 2e-6
     assert rel(outs[0], outs[2]) < 2e-6
     od = O.OracleDiscretization(mesh, N, True)
     ost = O.State(fl[0], fl[1:])
     for _ in range(2):
         ost = O.lsrk_step(ost, 2e-3, lambda y: O.rhs_full(y, od))
-    assert rel(outs[1], ost.fields()) < 1e-5
+    assert rel(outs[0], ost.fields()) < 1e-5
     assert rel(outs[2], ost.fields()) < 1e-5
 
 

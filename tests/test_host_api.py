@@ -21,6 +21,17 @@ def test_flux_params_validation():
 def test_nonpositive_wavespeed_rejected():
     with pytest.raises(ConfigError):
         solver.Discretization(meshgen.uniform_quad_mesh(2), SolverConfig(N=2), MediumField(-1.0))
+    # a callable medium is checked where it is evaluated (on the device's points),
+    # with the reference's ConfigError (R/pkg/src/wadg/solver.py:62-63)
+    from paper_1608_03836_b200.device import medium_on_device
+    x = torch.linspace(-1, 1, 7, dtype=torch.float64)
+    with pytest.raises(ConfigError):
+        medium_on_device(lambda x, y: x, (x, x), x.shape)
+    with pytest.raises(ConfigError):
+        medium_on_device(lambda x, y: np.cos(x) * np.nan, (x, x), x.shape)
+    v = medium_on_device(lambda x, y: 1.0 + x * x, (x, x), x.shape)        # torch expression
+    w = medium_on_device(lambda x, y: 1.0 + np.asarray(x) ** 2, (x, x), x.shape)
+    assert torch.equal(v, w)
 
 
 def test_insufficient_quadrature_rejected():
@@ -87,3 +98,5 @@ def test_no_cpu_fallback_without_cuda():
         solver.rhs_full(st, disc)
     with pytest.raises(RuntimeError, match="CUDA"):
         solver.lsrk_step(st, 1e-3, disc.rhs)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        solver.project_initial_condition(mesh, disc.config, lambda x, y, z: (0 * x,) * 4)
