@@ -95,11 +95,20 @@ def _runs(mask, value):
 
 class HaloExchange:
     """Per-stage halo exchange for one rank; ``start`` packs and posts the
-    NCCL send/recv, ``surface`` runs the halo-free blocks, waits, then the
-    halo blocks."""
+    NCCL send/recv, ``surface`` / ``fused_stage`` run the halo-free element
+    blocks on the current stream and the blocks that read halo slots on a
+    high-priority side stream that waits for the transfer, so those blocks
+    start as soon as their traces arrive and SMs free up, instead of after
+    the whole interior wave.  The current stream waits for the side stream
+    before the next kernel.
 
-    def __init__(self, disc, plan, group=None):
-        import torch.distributed as dist
+    ``dist`` is torch.distributed, or any object with the same P2POp /
+    isend / irecv / batch_isend_irecv interface (tests use a loopback one)."""
+
+    def __init__(self, disc, plan, group=None, dist=None):
+        import torch
+        if dist is None:
+            import torch.distributed as dist
         from . import _native
         self.dist, self.native = dist, _native
         self.disc, self.plan, self.group = disc, plan, group
@@ -111,6 +120,9 @@ class HaloExchange:
             fblk = halo_blocks(d, d.fused)
             self.free_runs_f = _runs(fblk, False)
             self.halo_runs_f = _runs(fblk, True)
+        with torch.cuda.device(d.device):
+            lo, hi = torch.cuda.Stream.priority_range()
+            self.side = torch.cuda.Stream(device=d.device, priority=min(lo, hi))
         self.reqs = []
 
     def start(self, Q):
@@ -129,36 +141,43 @@ class HaloExchange:
             ro += nr
         self.reqs = self.dist.batch_isend_irecv(ops) if ops else []
 
+    def _split_launch(self, free, halo, launch):
+        """launch(b0, b1, stream_ptr) over the free runs on the current stream,
+        then over the halo runs on the side stream after the transfer."""
+        import torch
+        main = torch.cuda.current_stream()
+        ready = torch.cuda.Event()
+        ready.record(main)                       # previous stage and this stage's pack are ordered
+        for b0, b1 in free:
+            launch(b0, b1, ctypes.c_void_p(main.cuda_stream))
+        with torch.cuda.stream(self.side):
+            self.side.wait_event(ready)
+            for r in self.reqs:                  # NCCL: the side stream waits for the transfer
+                r.wait()
+            for b0, b1 in halo:
+                launch(b0, b1, ctypes.c_void_p(self.side.cuda_stream))
+            done = torch.cuda.Event()
+            done.record(self.side)
+        main.wait_event(done)
+        self.reqs = []
+
     def surface(self, Q, rhs, tau_p, tau_u, sp):
         d = self.disc.dev
         vp = lambda t: ctypes.c_void_p(t.data_ptr())
-        for b0, b1 in self.free_runs:
-            self.native.call("wadg_surface", ctypes.byref(d.struct), vp(Q), vp(rhs), tau_p, tau_u,
-                             1, b0, b1, sp)
-        for r in self.reqs:
-            r.wait()
-        self.reqs = []
-        for b0, b1 in self.halo_runs:
-            self.native.call("wadg_surface", ctypes.byref(d.struct), vp(Q), vp(rhs), tau_p, tau_u,
-                             1, b0, b1, sp)
-
+        self._split_launch(self.free_runs, self.halo_runs, lambda b0, b1, st: self.native.call(
+            "wadg_surface", ctypes.byref(d.struct), vp(Q), vp(rhs), tau_p, tau_u, 1, b0, b1, st))
 
     def fused_stage(self, Qin, Qout, res, tau_p, tau_u, a, b, dt, sp):
         """Fused stage: interface-free element blocks while the halo is in
-        flight, then the blocks that read halo slots."""
+        flight, the blocks that read halo slots on the side stream."""
         d = self.disc.dev
         vp = lambda t: ctypes.c_void_p(t.data_ptr())
         args = (ctypes.byref(d.struct), vp(Qin), vp(Qout), vp(res), tau_p, tau_u, a, b, dt)
-        for b0, b1 in self.free_runs_f:
-            self.native.call("wadg_stage_fused", *args, b0, b1, sp)
-        for r in self.reqs:
-            r.wait()
-        self.reqs = []
-        for b0, b1 in self.halo_runs_f:
-            self.native.call("wadg_stage_fused", *args, b0, b1, sp)
+        self._split_launch(self.free_runs_f, self.halo_runs_f,
+                           lambda b0, b1, st: self.native.call("wadg_stage_fused", *args, b0, b1, st))
 
 
-def slab_discretization(mesh, config, medium, rank, world, n_layers, group=None):
+def slab_discretization(mesh, config, medium, rank, world, n_layers, group=None, dist=None):
     """Discretization of rank's z-slab with its halo exchange attached as
     ``disc.exchange``."""
     from .solver import Discretization
@@ -166,5 +185,5 @@ def slab_discretization(mesh, config, medium, rank, world, n_layers, group=None)
     plans = halo_plans(mesh, ranges)
     disc = Discretization(mesh, config, medium, k_range=ranges[rank], halo=plans[rank])
     disc.dev
-    disc.exchange = HaloExchange(disc, plans[rank], group)
+    disc.exchange = HaloExchange(disc, plans[rank], group, dist)
     return disc

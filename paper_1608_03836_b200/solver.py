@@ -484,12 +484,16 @@ class DeviceStepper:
         self.other = d.empty_fields() if self.fused else None
 
     @_on_disc_device
-    def stage(self, Q, a, b, dt):
+    def stage(self, Q, a, b, dt, started=False):
+        """One LSRK stage; for a slab (disc.exchange) the halo of Q is packed and
+        posted first, unless the caller did that already (started=True, e.g. a
+        driver of several slabs in one process posts every slab's halo before
+        running any stage)."""
         import ctypes
         d = self.disc.dev
         fl = self.disc.flux
         exch = getattr(self.disc, "exchange", None)      # slab of a multi-rank run (parallel.py)
-        if exch is not None:
+        if exch is not None and not started:
             exch.start(Q)                                # pack + post this stage's halo traces
         if self.fused:
             out = self.other

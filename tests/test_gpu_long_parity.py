@@ -121,30 +121,29 @@ def test_projection_matches_oracle():
 # ---------------------------------------------------------------------------
 # full config-4 size: sampled element-local parity of one tcgen05 stage
 
-def test_full_size_stage_sampled_against_oracle():
-    """K = 1,572,864 (BASELINE config 4), N = 4, fp32, heterogeneous c^2:
-    one stage res' = a res + dt M^-1 rhs(Q), Q' = Q + b res' of the tcgen05
-    kernel, on random Q and res, compared with the oracle for 512 sampled
-    elements (boundary, interior and every tile position), each from its
-    one-neighbour patch.  Tolerance: the fp32 bar per element patch."""
-    N, n = 4, 64
+def _sampled_stage_check(n, N, dtype, label, n_blocks=64, per_block=8):
+    """One LSRK stage res' = a res + dt M^-1 rhs(Q), Q' = Q + b res' (a != 0) of
+    the default fused kernel on random Q and res over the whole mesh, compared
+    with the oracle for sampled elements (every tile position, boundary and
+    interior), each evaluated on its one-neighbour patch."""
     mesh = meshgen.warped_cube_tet_mesh(n, N)
-    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype="float32")
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype=dtype)
     disc = solver.Discretization(mesh, cfg, solver.MediumField(c2_het))
-    assert mesh.K == 1572864 and disc.dev.fused_kind == 2
     d = disc.dev
+    tdt = torch.float32 if dtype == "float32" else torch.float64
     g = torch.Generator(device="cuda").manual_seed(77)
-    Q = torch.randn(d.empty_fields().shape, generator=g, device="cuda", dtype=torch.float32)
-    res = torch.randn(Q.shape, generator=g, device="cuda", dtype=torch.float32)
+    Q = torch.randn(d.empty_fields().shape, generator=g, device="cuda", dtype=tdt)
+    res = torch.randn(Q.shape, generator=g, device="cuda", dtype=tdt)
     Q[:, :, mesh.K:] = 0
     res[:, :, mesh.K:] = 0
     stepper = solver.DeviceStepper(disc)
+    assert stepper.fused
     stepper.res.copy_(res)
-    a, b, dt = solver.LSRK4A[2], solver.LSRK4B[2], 0.5 * mesh.h / 25
+    a, b, dt = solver.LSRK4A[2], solver.LSRK4B[2], 0.5 * mesh.h / (N + 1) ** 2
     Qout = stepper.stage(Q, a, b, dt)
     rng = np.random.default_rng(5)
-    blocks = rng.choice(mesh.K // 128, 64, replace=False)
-    elems = np.unique(np.concatenate([(blocks[:, None] * 128 + rng.choice(128, 8, replace=False)[None, :]).ravel(),
+    blocks = rng.choice(mesh.K // 128, n_blocks, replace=False)
+    elems = np.unique(np.concatenate([(blocks[:, None] * 128 + rng.choice(128, per_block, replace=False)[None, :]).ravel(),
                                       [0, 127, 128, mesh.K - 1]]))
     sub, patch, loc = submesh(mesh, elems)
     host = lambda X: [X[i, :, :mesh.K][:, torch.as_tensor(patch, device="cuda")].T.double().cpu().numpy()
@@ -157,11 +156,30 @@ def test_full_size_stage_sampled_against_oracle():
     got_res, got_Q = host(stepper.res), host(Qout)
     e_res = rel([x[loc] for x in got_res], [x[loc] for x in want_res])
     e_Q = rel([x[loc] for x in got_Q], [x[loc] for x in want_Q])
-    # the rhs part alone (res' - a res = dt rhs), the hardest-hit quantity in fp32
+    # the rhs part alone (res' - a res = dt rhs), the quantity most exposed to rounding
     e_rhs = rel([(x - a * y)[loc] for x, y in zip(got_res, Rp)], [dt * y[loc] for y in r])
-    record_parity(f"config-4 full size K={mesh.K} stage, {len(elems)} sampled tets: res", e_res, 1e-5)
-    record_parity(f"config-4 full size K={mesh.K} stage, {len(elems)} sampled tets: Q", e_Q, 1e-5)
-    record_parity(f"config-4 full size K={mesh.K} stage, {len(elems)} sampled tets: dt*rhs", e_rhs, 1e-5)
-    assert e_res < 1e-5 and e_Q < 1e-5 and e_rhs < 1e-5
+    tag = f"{label} K={mesh.K} N={N} {dtype} kernel={d.fused_kind}, one stage, {len(elems)} sampled tets"
+    record_parity(tag + ": res", e_res, TOL[dtype])
+    record_parity(tag + ": Q", e_Q, TOL[dtype])
+    record_parity(tag + ": dt*rhs", e_rhs, TOL[dtype])
+    kind = d.fused_kind
     del disc, d, Q, res, Qout, stepper
     torch.cuda.empty_cache()
+    assert e_res < TOL[dtype] and e_Q < TOL[dtype] and e_rhs < TOL[dtype]
+    return mesh.K, kind
+
+
+def test_full_size_stage_sampled_against_oracle():
+    """BASELINE config 4 at full size: K = 1,572,864, N = 4, fp32,
+    heterogeneous c^2, the tcgen05 stage."""
+    K, kind = _sampled_stage_check(64, 4, "float32", "config-4 full size")
+    assert K == 1572864 and kind == 2
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7])
+def test_million_tet_stage_sampled_against_oracle(N, dtype):
+    """north_star: fp64 and fp32 on a >= 1M-tet curvilinear mesh at N = 1..7
+    matching the oracle: 56^3 x 6 = 1,053,696 warped tets, heterogeneous c^2."""
+    K, _ = _sampled_stage_check(56, N, dtype, ">=1M tets", n_blocks=32, per_block=4)
+    assert K >= 1_000_000
