@@ -1162,6 +1162,32 @@ extern "C" int wadg_microbench_mma_tf32(int blocks, int iters, const void *in, v
     return check_launch("wadg_microbench_mma_tf32");
 }
 
+// mma.sync m8n8k4 FP64 (DMMA) throughput probe: 8 independent accumulators per warp
+namespace wadg {
+__global__ void __launch_bounds__(256) k_dmma_peak(const double *__restrict__ in, double *__restrict__ out, int iters) {
+    const double a = in[threadIdx.x & 7], b = in[8 + (threadIdx.x & 7)];
+    double c[8][2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k][0] = c[k][1] = 0.0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(c[k][0]), "+d"(c[k][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += c[k][0] + c[k][1];
+    if (s == 12345.678) out[threadIdx.x] = s;
+}
+}  // namespace wadg
+
+extern "C" int wadg_microbench_dmma(int blocks, int iters, const void *in, void *out, void *stream) {
+    wadg::k_dmma_peak<<<blocks, 256, 0, (cudaStream_t)stream>>>((const double *)in, (double *)out, iters);
+    return check_launch("wadg_microbench_dmma");
+}
+
 // Debug / validation of the tcgen05 primitives (wadg_umma.cuh): one CTA of 128
 // threads computes C (128 x N) = A (128 x K) B^T, A row-major (128 x K), B
 // row-major (N x K), with split-TF32 tcgen05.mma (A_lo B_hi + A_hi B_lo +
@@ -1324,4 +1350,13 @@ extern "C" int wadg_debug_umma_rate(void *out, int n, int count, int mode, void 
     cudaFuncSetAttribute(wadg::k_umma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     wadg::k_umma_rate<<<1, 128, smem, (cudaStream_t)stream>>>((long long *)out, n, count, mode);
     return check_launch("wadg_debug_umma_rate");
+}
+
+// Chip-wide tcgen05 kind::tf32 throughput: `blocks` CTAs each issue `count`
+// M=128, K=8 MMAs of width n (timed by the caller with CUDA events)
+extern "C" int wadg_microbench_umma(int blocks, int n, int count, int mode, void *out, void *stream) {
+    const size_t smem = 1024 + (128 * 8 + 256 * 8) * 4;
+    cudaFuncSetAttribute(wadg::k_umma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    wadg::k_umma_rate<<<blocks, 128, smem, (cudaStream_t)stream>>>((long long *)out, n, count, mode);
+    return check_launch("wadg_microbench_umma");
 }

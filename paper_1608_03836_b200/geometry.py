@@ -194,6 +194,8 @@ def geometric_factors(X, mops, check=True, k_offset=0):
 def compute_geometric_data(mesh, ref):
     """Host evaluation of the mapping metric (reference-compatible API,
     R/.../geometry.py:56-102).  Raises NonPositiveJacobian."""
+    if mesh.shape.dim == 2:
+        return _host_geometry_2d(mesh, ref)
     mops = map_operators(mesh.shape, mesh.N_geo, ref).to("cpu")
     X = torch.as_tensor(np.asarray(mesh.elem_map_nodes, dtype=np.float64))
     g = geometric_factors(X, mops)
@@ -210,3 +212,35 @@ def element_areas(geo):
 
 def element_perimeters(geo):
     return geo.Jfq @ geo.ref.wfq
+
+
+def _host_geometry_2d(mesh, ref):
+    """2D host metric with per-coordinate BLAS products (the reference's
+    matrix formulation, R/.../geometry.py:56-102), so the host diagnostics
+    (w_upd_p, geo, stable_dt) agree with the reference to rounding of the same
+    operations: J = x_r y_s - x_s y_r, (dr/dx) = [y_s, -x_s; -y_r, x_r] / J,
+    face normal (y', -x') / |.| along each face's CCW parameter."""
+    mo = map_operators(mesh.shape, mesh.N_geo, ref)
+    X = np.asarray(mesh.elem_map_nodes[:, :, 0], dtype=np.float64)
+    Y = np.asarray(mesh.elem_map_nodes[:, :, 1], dtype=np.float64)
+    Er, Es = mo.Eg
+    xq, yq = X @ mo.E.T, Y @ mo.E.T
+    xr, xs, yr, ys = X @ Er.T, X @ Es.T, Y @ Er.T, Y @ Es.T
+    J = xr * ys - xs * yr
+    if np.any(J <= 0):
+        k, q = np.argwhere(J <= 0)[0]
+        raise NonPositiveJacobian(int(k), int(q), float(J[k, q]))
+    G = np.stack([np.stack([ys / J, -xs / J]), np.stack([-yr / J, xr / J])])
+    Efr, Efs = mo.Efg
+    xf, yf = X @ mo.Ef.T, Y @ mo.Ef.T
+    xfr, xfs, yfr, yfs = X @ Efr.T, X @ Efs.T, Y @ Efr.T, Y @ Efs.T
+    tx, ty = np.empty_like(xf), np.empty_like(xf)
+    nfq = ref.nfq
+    for f in range(mesh.shape.n_faces):
+        dr, ds = mo.tangents[f][0]
+        sl = slice(f * nfq, (f + 1) * nfq)
+        tx[:, sl] = xfr[:, sl] * dr + xfs[:, sl] * ds
+        ty[:, sl] = yfr[:, sl] * dr + yfs[:, sl] * ds
+    sJ = np.hypot(tx, ty)
+    return GeometricData(ref=ref, xyzq=(xq, yq), Jq=J, Gq=G, xyzfq=(xf, yf), Jfq=sJ,
+                         nq=(ty / sJ, -tx / sJ))

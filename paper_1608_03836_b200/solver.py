@@ -969,3 +969,34 @@ def run(mesh, config, initial_fn, T, medium=MediumField(), exact_p=None, n_outpu
     state = disc.from_device(Q, state, t)
     diag = {k: np.asarray(v) for k, v in diag.items()}
     return state, diag
+
+
+# ---------------------------------------------------------------------------
+# Exact disk solution (R/pkg/src/wadg/solver.py:445-466): the standing pressure
+# mode of the unit disk with the Dirichlet mirror BC.  Host diagnostics for
+# run(..., exact_p=bessel_pressure); J0 / J1 from scipy.special (the reference
+# restates them as series / Hankel expansions, R/pkg/src/wadg/bessel.py).
+
+DISK_LAMBDA = 5.52007811028631     # second zero of J0 (R/pkg/src/wadg/bessel.py:18)
+
+
+def bessel_pressure(x, y, t, lam=DISK_LAMBDA):
+    """p = J0(lam r) cos(lam t)."""
+    from scipy.special import j0
+    return j0(lam * np.hypot(x, y)) * np.cos(lam * t)
+
+
+def bessel_velocity(x, y, t, lam=DISK_LAMBDA):
+    """u = J1(lam r) sin(lam t) r_hat."""
+    from scipy.special import j1
+    r = np.hypot(x, y)
+    mag = j1(lam * r) * np.sin(lam * t)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        cx = np.where(r > 0, x / np.where(r > 0, r, 1.0), 0.0)
+        cy = np.where(r > 0, y / np.where(r > 0, r, 1.0), 0.0)
+    return mag * cx, mag * cy
+
+
+def bessel_initial_condition(x, y):
+    p = bessel_pressure(x, y, 0.0)
+    return p, np.zeros_like(p), np.zeros_like(p)

@@ -11,6 +11,7 @@ dense per-element M_J^{-1} (solver.py:153-154 vs 166-167).
 """
 
 import argparse
+import gc
 import ctypes
 import json
 import os
@@ -87,6 +88,7 @@ def main():
             r["fp_frac"] = r["fp_TFLOPs"] / peaks[dtype]
             rows.append(r)
             print(json.dumps(r), flush=True)
+            gc.collect()                 # Discretization <-> disc.rhs is a reference cycle
             torch.cuda.empty_cache()
     print(json.dumps({"summary": "config3", "hbm_peak_GBs": hbm, "fma_peak_TFLOPs": peaks,
                       "n": args.n, "steps": args.steps}))
