@@ -28,6 +28,7 @@ namespace wadg {
 #include "wadg_fused.cuh"
 #include "wadg_umma.cuh"
 #include "wadg_fused_umma.cuh"
+#include "wadg_fused_dmma.cuh"
 
 namespace wadg {
 
@@ -737,7 +738,7 @@ static fused::FProb<T> make_fprob(const wadg_problem &p) {
     return q;
 }
 
-static int g_fused_variant = -1;   // debug override of the packing choice: 0 CUDA-core, 2 tcgen05, -1 default
+static int g_fused_variant = -1;   // debug override of the packing choice: 0 CUDA-core, 2 tcgen05, 3 DMMA, -1 default
 
 // cudaFuncSetAttribute (max dynamic shared memory) is per device: one flag per
 // (kernel instantiation, device)
@@ -768,6 +769,22 @@ static bool use_umma() {
     return true;
 }
 
+// DMMA (FP64 tensor core) fused stage: fp64, N = 2..5
+template <typename T, int N>
+static constexpr bool dmma_available() {
+    if constexpr (sizeof(T) == 8 && N >= 2 && N <= 5) return dk::CfgD<N>::SMEM <= 227 * 1024;
+    return false;
+}
+
+// default per order from B200 A/B timings: DMMA at N = 4, 5;
+// the DFMA tiles (two CTAs per SM) at N = 2, 3
+template <typename T, int N>
+static bool use_dmma() {
+    if (!dmma_available<T, N>()) return false;
+    if (g_fused_variant >= 0) return g_fused_variant == 3;
+    return N >= 4;
+}
+
 // info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),
 //            quad-chunk row stride, node row stride, padded face points}
 template <typename T, int N>
@@ -779,6 +796,15 @@ static int fused_cfg(int32_t *info, int64_t *smem) {
         if (use_umma<T, N>()) {
             using C = uk::CfgU<N>;
             const int32_t w[8] = {2, C::ME, C::QC, C::NCH, C::NPK, C::NPN, C::NFPK, C::NFH};
+            for (int i = 0; i < 8; ++i) v[i] = w[i];
+            sm = C::SMEM;
+            done = true;
+        }
+    }
+    if constexpr (dmma_available<T, N>()) {
+        if (!done && use_dmma<T, N>()) {
+            using C = dk::CfgD<N>;
+            const int32_t w[8] = {3, C::KB, C::QC, C::NCH, C::NPP, C::NFPK, C::NFQP, (int32_t)C::OP_TOTAL};
             for (int i = 0; i < 8; ++i) v[i] = w[i];
             sm = C::SMEM;
             done = true;
@@ -850,6 +876,24 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
         if constexpr (umma_available<T, N>())
             return fused_launch_umma<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, lay, st);
         return fail("operators packed for the tcgen05 stage, which is not compiled for this dtype / order");
+    }
+    if (Pc->fused_kind == 3) {
+        if constexpr (dmma_available<T, N>()) {
+            using C = dk::CfgD<N>;
+            if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
+            if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
+            const int nblk = Pc->Kpad / C::KB;
+            if (b1 < 0 || b1 > nblk) b1 = nblk;
+            if (b0 < 0) b0 = 0;
+            if (b1 <= b0) return 0;
+            static bool attr_set[64] = {};
+            if (!attr_once(attr_set, (const void *)dk::k_stage_dmma<N>, C::SMEM))
+                return fail("cudaFuncSetAttribute failed for the DMMA stage");
+            dk::k_stage_dmma<N><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<double>(*Pc), (const double *)Qin,
+                                                                (double *)Qout, (double *)res, tp, tu, a, b, dt, b0);
+            return check_launch("wadg_stage_fused(dmma)");
+        }
+        return fail("operators packed for the DMMA stage, which is not compiled for this dtype / order");
     }
     if (Pc->fused_kind != 0) return fail("unknown fused_kind");
     if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
@@ -1034,7 +1078,7 @@ int wadg_debug_set_phase_clock_buffer(void *buf) {
 }
 
 int wadg_debug_set_fused_variant(int variant) {
-    if (variant != -1 && variant != 0 && variant != 2) return fail("variant must be -1, 0 or 2");
+    if (variant != -1 && variant != 0 && variant != 2 && variant != 3) return fail("variant must be -1, 0, 2 or 3");
     g_fused_variant = variant;
     return 0;
 }

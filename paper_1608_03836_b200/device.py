@@ -178,6 +178,53 @@ def umma_operator_images(ref, ru, cfg):
     return out
 
 
+def frag_image(B, K, Nn):
+    """DMMA (mma.m8n8k4.f64) B-fragment image of B (k x n, zero padded to
+    K x Nn): [K/4][Nn/8][32], lane t holding B[4 ks + t % 4][8 nt + t // 4]
+    (csrc/wadg_fused_dmma.cuh)."""
+    Bp = np.zeros((K, Nn))
+    Bp[:B.shape[0], :B.shape[1]] = B
+    lane = np.arange(32)
+    ks, nt = np.arange(K // 4), np.arange(Nn // 8)
+    kk = 4 * ks[:, None, None] + (lane % 4)[None, None, :]
+    nn = 8 * nt[None, :, None] + (lane // 4)[None, None, :]
+    return Bp[kk, nn]
+
+
+def dmma_operator_images(ref, ru, cfg):
+    """All reference operators of the DMMA fused stage (csrc/wadg_fused_dmma.cuh,
+    CfgD offsets), in fragment order: per volume chunk D_r, D_s, D_t, Vq (k = node,
+    n = point) and DTW_r, DTW_s, DTW_t, -Pq (k = point, n = node); Vfi; -Pf per
+    face; per update chunk Vu and Pu."""
+    NP, NQ = ref.Np, ref.Nq
+    QC, NCH, NPP, NFPK, NFQP = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"]
+    nf, nfq = ref.n_faces, ref.nfq
+    DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
+
+    def cols(M, c0, n):                     # columns c0 .. c0+n of M (zero past the end)
+        out = np.zeros((M.shape[0], n))
+        c1 = min(M.shape[1], c0 + n)
+        if c1 > c0:
+            out[:, :c1 - c0] = M[:, c0:c1]
+        return out
+
+    parts = []
+    for ch in range(NCH):
+        parts += [frag_image(cols(Op.T, ch * QC, QC), NPP, QC) for Op in list(ref.Dq) + [ref.Vq]]
+    for ch in range(NCH):
+        parts += [frag_image(cols(Op, ch * QC, QC).T, QC, NPP) for Op in DTW + [-ref.Pq]]
+    parts.append(frag_image(ref.face_interp.T, NFPK, NFQP))
+    for f in range(nf):
+        parts.append(frag_image(-ref.Pfq[:, f * nfq:(f + 1) * nfq].T, NFQP, NPP))
+    for ch in range(NCH):
+        parts.append(frag_image(cols(ru.Vq.T, ch * QC, QC), NPP, QC))
+    for ch in range(NCH):
+        parts.append(frag_image(cols(ru.Pq, ch * QC, QC).T, QC, NPP))
+    out = np.concatenate([p.ravel() for p in parts])
+    assert out.size == cfg["nfq8"], (out.size, cfg["nfq8"])
+    return out
+
+
 class DeviceProblem:
     """All device arrays of one (mesh range, reference elements, medium) and
     the C struct pointing at them."""
@@ -368,6 +415,16 @@ class DeviceProblem:
             self.fused_kind = 2
             self.struct.order = N
             self.struct.fused_kind = 2
+            return kb
+        if cfg["kind"] == 3:                    # DMMA kernel: one buffer of fragment-order images
+            if self.Kpad % kb:
+                return None
+            self.ops["dmma"] = self._t(dmma_operator_images(ref, ru, cfg), torch.float64)
+            for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
+                setattr(self.struct, name, self.ops["dmma"].data_ptr())
+            self.fused_kind = 3
+            self.struct.order = N
+            self.struct.fused_kind = 3
             return kb
         # CUDA-core kernel layouts (kind 0)
         NPP = roundup(NP, 4)

@@ -14,7 +14,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=48)
 ap.add_argument("--orders", type=int, nargs="+", default=[2, 3, 4])
 ap.add_argument("--dtype", default="float32")
+ap.add_argument("--variant", type=int, default=-1, help="fused kernel: 0 CUDA cores, 2 tcgen05, 3 DMMA")
 args = ap.parse_args()
+if args.variant >= 0:
+    _native.call("wadg_debug_set_fused_variant", args.variant)
 for N in args.orders:
     mesh = meshgen.warped_cube_tet_mesh(args.n, N)
     disc = solver.Discretization(mesh, solver.SolverConfig(N=N, formulation=solver.Formulation.StrongWeak,
@@ -36,7 +39,7 @@ for N in args.orders:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    print(json.dumps({"N": N, "K": mesh.K, "ms": ms, "GDOF/s": 4 * mesh.K * disc.ref.Np / (ms * 1e-3) / 1e9}),
+    print(json.dumps({"N": N, "dtype": args.dtype, "kind": d.fused_kind, "K": mesh.K, "ms": ms, "GDOF/s": 4 * mesh.K * disc.ref.Np / (ms * 1e-3) / 1e9}),
           flush=True)
     del disc, d, A, B, res
     torch.cuda.empty_cache()

@@ -55,3 +55,43 @@ def test_interleave_blocks_layout():
     for b, r, q, e in [(0, 0, 0, 0), (1, 2, 12, 127), (0, 1, 7, 33), (1, 0, 5, 64)]:
         assert y[b, r, q // 4, e, q % 4] == x[r, q, b * 128 + e]
     assert torch.all(y[:, :, 3, :, 1:] == 0)          # points 13..15 are zero padding
+
+
+def test_dmma_fragment_images_reconstruct_operators():
+    """The DMMA stage's B-fragment images (device.dmma_operator_images): lane t
+    of [k step][n tile] holds B[4 ks + t % 4][8 nt + t // 4]; inverting that map
+    must give back each operator (csrc/wadg_fused_dmma.cuh offsets)."""
+    import numpy as np
+    from paper_1608_03836_b200 import _native, device, refelem
+    for N in (2, 4, 5):
+        cfg = _native.fused_config(_native.WADG_F64, N)
+        assert cfg["kind"] == 3
+        ref = refelem.build_reference_element(N, refelem.ElementShape.Tetrahedron)
+        img = device.dmma_operator_images(ref, ref, cfg)
+        QC, NCH, NPP, NFPK, NFQP = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"]
+
+        def unpack(flat, K, Nn):
+            a = flat.reshape(K // 4, Nn // 8, 32)
+            B = np.zeros((K, Nn))
+            for t in range(32):
+                B[(4 * np.arange(K // 4))[:, None] + t % 4, (8 * np.arange(Nn // 8))[None, :] + t // 4] = a[:, :, t]
+            return B
+        o, NP, NQ = 0, ref.Np, ref.Nq
+        sz = lambda K, Nn: K * Nn
+        # last chunk of D_s (volume image VA): B[k=j][n=q] = Ds[ch QC + q, j]
+        ch = NCH - 1
+        o_va = (ch * 4 + 1) * sz(NPP, QC)
+        B = unpack(img[o_va:o_va + sz(NPP, QC)], NPP, QC)
+        q1 = NQ - ch * QC
+        assert np.array_equal(B[:NP, :q1], ref.Dq[1][ch * QC:].T)
+        assert not B[:, q1:].any()
+        assert not B[NP:].any()
+        # -Pq of chunk 0 (VB image, op 3): B[k=q][n=j] = -Pq[j, q]
+        o_vb = NCH * 4 * sz(NPP, QC) + 3 * sz(QC, NPP)
+        B = unpack(img[o_vb:o_vb + sz(QC, NPP)], QC, NPP)
+        assert np.array_equal(B[:min(QC, NQ), :NP], -ref.Pq[:, :min(QC, NQ)].T)
+        # -Pf of face 2: B[k=fq][n=j] = -Pf[j, 2 nfq + fq]
+        o_l = NCH * 4 * sz(NPP, QC) + NCH * 4 * sz(QC, NPP) + sz(NFPK, NFQP) + 2 * sz(NFQP, NPP)
+        B = unpack(img[o_l:o_l + sz(NFQP, NPP)], NFQP, NPP)
+        nfq = ref.nfq
+        assert np.array_equal(B[:nfq, :NP], -ref.Pfq[:, 2 * nfq:3 * nfq].T)
