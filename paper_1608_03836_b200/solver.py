@@ -178,7 +178,12 @@ class Discretization:
         self._halo = halo
         self._dev = None
         self._host = {}
-        self.rhs = _BoundRHS(self)
+
+    @property
+    def rhs(self):
+        """rhs_full bound to this discretization (a fresh small object per access,
+        so the discretization holds no reference cycle through it)."""
+        return _BoundRHS(self)
 
     # -- device ------------------------------------------------------------------
     @property

@@ -90,3 +90,19 @@ def submesh(mesh, elems):
     sub = meshgen.CurvedMesh(mesh.shape, mesh.N_geo, mesh.elem_map_nodes[patch], c, tags, h=mesh.h,
                              face_orientation=ori)
     return sub, patch, index[elems]
+
+
+@pytest.fixture(autouse=True)
+def _release_device_memory():
+    """GPU tests build full-size (1.5M-tet) problems one after another: collect
+    the previous test's objects (a HostPipeline / HaloExchange refers back to its
+    Discretization) and return the cached blocks before the next test."""
+    yield
+    import gc
+    gc.collect()
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
+    except Exception:
+        pass

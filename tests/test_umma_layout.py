@@ -64,7 +64,11 @@ def test_dmma_fragment_images_reconstruct_operators():
     import numpy as np
     from paper_1608_03836_b200 import _native, device, refelem
     for N in (2, 4, 5):
-        cfg = _native.fused_config(_native.WADG_F64, N)
+        _native.call("wadg_debug_set_fused_variant", 3)
+        try:
+            cfg = _native.fused_config(_native.WADG_F64, N)
+        finally:
+            _native.call("wadg_debug_set_fused_variant", -1)
         assert cfg["kind"] == 3
         ref = refelem.build_reference_element(N, refelem.ElementShape.Tetrahedron)
         img = device.dmma_operator_images(ref, ref, cfg)
