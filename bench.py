@@ -204,6 +204,72 @@ def reference_2d_calibration(K1D=64, N=4, steps=2):
             "port_over_reference_speed": t_ref / t_port}
 
 
+def umma_issued_flops(N, Kpad):
+    """Tensor-core flops the tcgen05 stage issues per launch: every MMA of
+    csrc/wadg_fused_umma.cuh (M = 128, K = 8, split-TF32: 3 MMAs per product,
+    padded extents) times 2 * 128 * N_mma * 8."""
+    rup = lambda a, b: -(-a // b) * b
+    NP = (N + 1) * (N + 2) * (N + 3) // 6
+    NPK = NPN = rup(NP, 8)
+    NQ = (N + 1) ** 3
+    NCH = -(-NQ // 16)
+    NFPK = rup((N + 1) * (N + 2) // 2, 8)
+    NFH = -(-((N + 1) ** 2) // 16)
+    mac = lambda n: 128 * n * 8
+    per_chunk = (NPK // 8 * 3 * mac(48) + NPK // 8 * 9 * mac(16)      # D_a p, Vq u_i
+                 + 2 * 9 * mac(NPN) + 2 * 9 * mac(NPN))               # -Pq gp_i, DTW_a F_a
+    per_step = NFPK // 8 * 3 * 8 * mac(16) + 2 * 3 * 4 * mac(NPN)     # traces (own + ext), lifts
+    per_uchunk = NPK // 8 * 3 * 4 * mac(16) + 2 * 3 * 4 * mac(NPN)    # z = Vu R, R (+)= Pu omega z
+    per_tile = NCH * per_chunk + 4 * NFH * per_step + NCH * per_uchunk
+    return 2.0 * per_tile * (Kpad // 128)
+
+
+def dmma_issued_flops(N, Kpad):
+    """FP64 tensor-core flops the DMMA stage issues per launch (csrc/wadg_fused_dmma.cuh:
+    8 x 8 x 4 MMAs over padded extents)."""
+    rup = lambda a, b: -(-a // b) * b
+    NP = (N + 1) * (N + 2) * (N + 3) // 6
+    NPP, NQ = rup(NP, 8), (N + 1) ** 3
+    QC = 32 if N <= 4 else 16
+    NCH = -(-NQ // QC)
+    NFPK, NFQP = rup((N + 1) * (N + 2) // 2, 4), rup((N + 1) ** 2, 8)
+    fma = (NCH * QC * NPP * (6 + 6)          # volume: 6 products each way
+           + 4 * (NFQP * NFPK * 8 + NFQP * NPP * 4)   # traces (own + ext, 4 fields), lifts
+           + NCH * QC * NPP * (4 + 4))       # update z, R'
+    return 2.0 * fma * Kpad
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def reference_benchmark_rhs():
+    """The reference's own per-phase timer (R/pkg/src/wadg/analysis.py:238-266,
+    baseline/_ref, 2D only) on the warped triangles of config 1 at N = 4:
+    ns per DOF of volume / surface / update, median of 10."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "wadg")):
+        return {"unavailable": "baseline/_ref not installed"}
+    sys.path.insert(0, ref_dir)
+    try:
+        from wadg import analysis as ran, meshgen as rmg, refelem as rrf, solver as rsv
+        from paper_1608_03836_b200 import meshgen
+        m = meshgen.warped_triangle_mesh(64, 4)
+        rm = rmg.CurvedMesh2D(shape=rrf.ElementShape.Triangle, N_geo=m.N_geo, elem_map_nodes=m.elem_map_nodes,
+                              face_connectivity=m.face_connectivity, boundary_tags=m.boundary_tags, h=m.h)
+        rep = ran.benchmark_rhs(rm, rsv.SolverConfig(N=4, formulation=rsv.Formulation.StrongWeak), repetitions=10)
+        return {"mesh": f"warped triangles 64x64x2 = {m.K}, N=4, strong-weak", "ns_per_dof": rep}
+    except Exception as exc:                     # pragma: no cover
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -388,11 +454,38 @@ def main():
             hbm_peak = float(json.load(f)["hbm_gbs"])
         peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
     achieved = B[top] / (avg[top] * 1e-3) / 1e9
+    # compute side of the dominant kernel: flops the tensor / FP pipes are issued
+    # (padded MMA extents, the 3 split-TF32 MMAs per product counted) against the
+    # measured peaks (profiles/r02_measured_peaks.json), and the binding roof =
+    # the larger of the two lower-bound times
+    kind = getattr(d, "fused_kind", -1) if fused else -1
+    peaks_r02 = {"tcgen05_tf32": 1105.2, "dmma_f64": 37.1, "ffma": 71.8, "dfma": 34.1}
+    pk_path = os.path.join(ROOT, "profiles", "r02_measured_peaks.json")
+    if os.path.exists(pk_path):
+        with open(pk_path) as f:
+            tf = json.load(f)["tflops"]
+        peaks_r02 = {"tcgen05_tf32": tf["tcgen05_tf32_tflops_TS_N256"], "dmma_f64": tf["dmma_f64_tflops"],
+                     "ffma": tf["fp32_fma_tflops"], "dfma": tf["fp64_fma_tflops"]}
+    if kind == 2:
+        issued, cpeak, cname = umma_issued_flops(N, d.Kpad), peaks_r02["tcgen05_tf32"], "tcgen05 kind::tf32"
+    elif kind == 3:
+        issued, cpeak, cname = dmma_issued_flops(N, d.Kpad), peaks_r02["dmma_f64"], "DMMA f64"
+    else:
+        issued = FL[top]
+        cpeak, cname = (peaks_r02["ffma"], "FFMA") if cfg.dtype == "float32" else (peaks_r02["dfma"], "DFMA")
+    t_hbm = B[top] / (hbm_peak * 1e9)
+    t_cmp = issued / (cpeak * 1e12)
+    compute = {"pipe": cname, "issued_tflop_per_launch": issued / 1e12,
+               "achieved_tflops": issued / (avg[top] * 1e-3) / 1e12, "peak_tflops": cpeak,
+               "frac": issued / (avg[top] * 1e-3) / 1e12 / cpeak,
+               "lower_bound_ms": {"hbm": t_hbm * 1e3, "compute": t_cmp * 1e3}}
     # measured DRAM traffic per launch from the committed ncu --set full capture
     traffic = None
-    kname = {2: "umma"}.get(getattr(d, "fused_kind", 0), "fused")
-    tpath = os.path.join(ROOT, "profiles", f"r01_ncu_stage_{kname}_{'f32' if cfg.dtype == 'float32' else 'f64'}"
-                         f"_N{N}_{args.config}.json")
+    kname = {2: "umma", 3: "dmma"}.get(getattr(d, "fused_kind", 0), "fused")
+    tname = f"ncu_stage_{kname}_{'f32' if cfg.dtype == 'float32' else 'f64'}_N{N}_{args.config}.json"
+    tpath = os.path.join(ROOT, "profiles", "r02_" + tname)
+    if not os.path.exists(tpath):
+        tpath = os.path.join(ROOT, "profiles", "r01_" + tname)
     if fused and world == 1 and os.path.exists(tpath):
         with open(tpath) as f:
             nd = json.load(f)
@@ -463,9 +556,19 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, Ks, el = cpu_oracle_rate(args.config, 16, 3, args.order)
+        try:
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(1):
+                v1, _, el1 = cpu_oracle_rate(args.config, 12, 1, args.order)
+            one = {"value": v1, "sample": f"warped cube 12^3x6, 1 LSRK step, {el1:.1f} s, 1 BLAS thread"}
+        except Exception as exc:                  # pragma: no cover
+            one = {"unavailable": f"{type(exc).__name__}: {exc}"}
         cpu = {"value": v, "unit": "GDOF/s", "cores": os.cpu_count(), "kind": "port",
+               "cpu_model": cpu_model(),
                "sample": f"numpy oracle (fp64) on warped cube 16^3x6 = {Ks} tets, N={N}, "
-                         f"3 LSRK steps, {el:.1f} s"}
+                         f"3 LSRK steps, {el:.1f} s",
+               "one_thread": one,
+               "reference_benchmark_rhs_2d": reference_benchmark_rhs()}
 
     if rank == 0:
         Np2, Nqu = Np * Np, disc.ref_upd.Nq
@@ -479,17 +582,28 @@ def main():
             "config": {"workload": desc, "K": mesh.K, "N": N, "Np": Np, "formulation": "strong-weak",
                        "dt": dt, "l2": "inputs > L2 (fields+geometry ~GBs); no flush needed",
                        "parallelism": f"z-slabs x{world}", "setup_s": round(setup_s, 1)},
-            "roofline": {"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm_peak,
-                         "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
-                         "peak_source": peak_src, "algorithmic_bytes_per_launch": B[top],
-                         "fp_achieved_tflops": FL[top] / (avg[top] * 1e-3) / 1e12},
+            "roofline": ({"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm_peak,
+                          "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
+                          "peak_source": peak_src, "algorithmic_bytes_per_launch": B[top],
+                          "algorithmic_tflop_per_launch": FL[top] / 1e12,
+                          "bound_from": "larger lower-bound time of HBM bytes vs issued compute",
+                          "compute": compute}
+                         if t_hbm >= t_cmp else
+                         {"bound": "tensor" if kind in (2, 3) else "fp", "kernel": top,
+                          "achieved": compute["achieved_tflops"], "peak": cpeak, "unit": "TFLOP/s",
+                          "frac": compute["frac"], "traffic": traffic,
+                          "peak_source": "measured (profiles/r02_measured_peaks.json)",
+                          "hbm": {"achieved_gbs": achieved, "peak_gbs": hbm_peak, "frac": achieved / hbm_peak,
+                                  "algorithmic_bytes_per_launch": B[top]},
+                          "bound_from": "larger lower-bound time of HBM bytes vs issued compute",
+                          "compute": compute}),
             "kernels": kernels,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": (5 if fused else 15) * args.steps,
             "stage_kernel": "wadg_stage_fused" if fused else "wadg_volume+wadg_surface+wadg_update_lsrk",
-            "fused_kernel": ({0: "k_stage_fused (CUDA-core FMA)", 1: "k_stage_fused_tc (mma.sync split-TF32)",
-                              2: "k_stage_umma (tcgen05 split-TF32, TMEM)"}.get(getattr(d, "fused_kind", -1))
+            "fused_kernel": ({0: "k_stage_fused (CUDA-core FMA)", 2: "k_stage_umma (tcgen05 split-TF32, TMEM)",
+                              3: "k_stage_dmma (FP64 tensor cores, mma.sync m8n8k4)"}.get(getattr(d, "fused_kind", -1))
                              if fused else None),
             "clocks": clk,
             "storage_words_per_element": {"wadg_weights": 2 * Nqu, "dense_inverse": 2 * Np2,
