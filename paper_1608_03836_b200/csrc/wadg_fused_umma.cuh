@@ -71,7 +71,8 @@ struct CfgU {
     // volume tiles per quadrature chunk: D_a (rows a*16 + q), Vq (rows q), DTW_a (3 blocks of
     // rows j, K = q), -Pq (rows j, K = q)
     // Vq tiles per chunk (16 rows), double buffered
-    static constexpr int OPDA = 2 * 48 * NPK, OPVQ = 2 * 16 * NPK, OPDTW = 2 * 3 * NPN * QC, OPPQ = 2 * NPN * QC;
+    static constexpr int NPAIR = cdiv(NCH, 2);
+    static constexpr int OPDA = 2 * 48 * NPK, OPVQ = 2 * 32 * NPK, OPDTW = 2 * 3 * NPN * QC, OPPQ = 2 * NPN * QC;
     static constexpr int OPVF = 2 * 16 * NPK;               // rows: face points of one half
     static constexpr int OPVFI = 2 * 16 * NFPK;
     static constexpr int OPPF = 2 * NPN * 16;               // rows j, K = face points
@@ -81,7 +82,7 @@ struct CfgU {
     // offsets (floats) of the packed operator buffer
     static constexpr size_t O_DA = 0;
     static constexpr size_t O_VQ = O_DA + (size_t)NCH * OPDA;
-    static constexpr size_t O_DTW = O_VQ + (size_t)NCH * OPVQ;
+    static constexpr size_t O_DTW = O_VQ + (size_t)NPAIR * OPVQ;
     static constexpr size_t O_PQ = O_DTW + (size_t)NCH * OPDTW;
     static constexpr size_t O_VFI = O_PQ + (size_t)NCH * OPPQ;         // [half] Vfi
     static constexpr size_t O_PF = O_VFI + (size_t)NFH * OPVFI;         // [f][half] -Pf
@@ -92,7 +93,7 @@ struct CfgU {
     static constexpr size_t MISC = 2304;
     static_assert(128 + 4 * (NF * 6 * NFP + NF * NFP + 6 * NFP) <= MISC, "index tables exceed MISC");
     static constexpr size_t SQF = (size_t)FLD * ME * NPK;              // floats of one field set
-    static constexpr size_t S_VOL = (size_t)(2 * OPDA + 2 * OPVQ + OPDTW + OPPQ) * 4;
+    static constexpr size_t S_VOL = (size_t)(2 * OPDA + OPVQ + OPDTW + OPPQ) * 4;
     static constexpr size_t S_EXT = (size_t)FLD * ME * NFPK * 4;      // one K-major face-node operand
     static constexpr size_t S_UPD = (size_t)2 * (OPU1 + OPU2) * 4;
     static constexpr size_t S_OPS = fused::maxz(S_VOL, S_UPD);
@@ -320,17 +321,21 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     // ---- shared-memory regions and TMEM columns per phase ------------------
     // volume
     float *sDa = sOp;                                   // [2][OPDA]
-    auto sVq = [&](int b) { return sDa + 2 * C::OPDA + b * C::OPVQ; };   // [2][OPVQ]
-    float *sPq = sDa + 2 * C::OPDA + 2 * C::OPVQ;       // [OPPQ]
+    float *sVq = sDa + 2 * C::OPDA;                     // [OPVQ] (one chunk pair)
+    float *sPq = sVq + C::OPVQ;                         // [OPPQ]
     float *sDTW = sPq + C::OPPQ;                        // [OPDTW]
-    // U of a chunk: field i at UO + 16 i.  RPC: the split-TF32 correction terms
-    // (A_lo B_hi, A_hi B_lo) of the R_p volume accumulation, kept apart from the
-    // main terms in RACC: the tensor core's fp32 accumulation truncates toward
-    // zero at the accumulator's ulp, so the small corrections are not added into
-    // the large running R_p (half the truncations there); folded into R_p by the
-    // epilogue at the end of the volume
-    const uint32_t DPO = SCR, UO = SCR + 48, GPH = SCR + 96, GPL = SCR + 144, FH = SCR + 192, FL = SCR + 240,
-                   RPC = SCR + 288;
+    // U of a chunk pair: field i at UO + 32 i, chunk ch at + 16 (ch & 1).  dp_a is
+    // written into the gp hi columns (GPH) and the epilogue overwrites it with
+    // gp_hi in place (each thread reads its dp values before it writes); the
+    // next chunk's D_a p MMAs are issued after this chunk's -Pq gp ones, whose
+    // reads of GPH precede them in the tensor core's in-order execution.  RPC:
+    // the split-TF32 correction terms (A_lo B_hi, A_hi B_lo) of the R_p volume
+    // accumulation, kept apart from the main terms in RACC: the tensor core's
+    // fp32 accumulation truncates toward zero at the accumulator's ulp, so the
+    // small corrections are not added into the large running R_p (half the
+    // truncations there); folded into R_p by the epilogue at the end of the volume
+    const uint32_t UO = SCR, GPH = SCR + 96, GPL = SCR + 144, FH = SCR + 192, FL = SCR + 240, RPC = SCR + 288;
+    const uint32_t DPO = GPH;
     // surface (over the sQlo + ops union): exterior node hi / lo and own node lo
     // parts (K-major operands), resident Vfi tiles, two -Pf tiles, neighbour-node
     // staging; TMEM: traces at the 16 points of a face half (own, exterior), the
@@ -387,8 +392,8 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                              desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
             }
         };
-        auto issue_v1u = [&](int ch) {                 // U_i of chunk ch (Vq tile in buffer ch & 1)
-            const uint32_t bh = su32(sVq(ch & 1)), bl = bh + C::OPVQ * 2, id = idesc_tf32(128, 16);
+        auto issue_v1u = [&]() {                       // U_i for the chunk pair in sVq
+            const uint32_t bh = su32(sVq), bl = bh + C::OPVQ * 2, id = idesc_tf32(128, 32);
 #pragma unroll 1
             for (int ks = 0; ks < NPK / 8; ++ks) {
                 const uint32_t o = ks * 256;
@@ -396,7 +401,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 for (int t = 0; t < 3; ++t)
 #pragma unroll
                     for (int i = 0; i < 3; ++i)
-                        mma_ss_w(tm + UO + 16 * i, desc_k((t == 0 ? aQlo : aQ) + (1 + i) * FQB + o, 128, SBO_Q),
+                        mma_ss_w(tm + UO + 32 * i, desc_k((t == 0 ? aQlo : aQ) + (1 + i) * FQB + o, 128, SBO_Q),
                                  desc_k((t == 1 ? bl : bh) + o, 128, SBO_Q), id, (ks > 0 || t > 0) ? 1u : 0u);
             }
         };
@@ -428,19 +433,16 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             }
         };
         op_load(C::SL_DA, sDa, ops + C::O_DA, C::OPDA * 4);
-        op_load(C::SL_VQ, sVq(0), ops + C::O_VQ, C::OPVQ * 4);
+        op_load(C::SL_VQ, sVq, ops + C::O_VQ, C::OPVQ * 4);
         op_load(C::SL_PQ, sPq, ops + C::O_PQ, C::OPPQ * 4);
         op_load(C::SL_DTW, sDTW, ops + C::O_DTW, C::OPDTW * 4);
-        if (NCH > 1) {
-            op_load(C::SL_DA + 1, sDa + C::OPDA, ops + C::O_DA + C::OPDA, C::OPDA * 4);
-            op_load(C::SL_VQ + 1, sVq(1), ops + C::O_VQ + C::OPVQ, C::OPVQ * 4);
-        }
+        if (NCH > 1) op_load(C::SL_DA + 1, sDa + C::OPDA, ops + C::O_DA + C::OPDA, C::OPDA * 4);
         __syncwarp();
         op_wait(C::SL_DA);
         issue_v1p(0);
         commit_w(&bar[0]);
         op_wait(C::SL_VQ);
-        issue_v1u(0);
+        issue_v1u();                         // chunks 0, 1
         commit_w(&bar[7]);
         for (int ch = 0; ch < NCH; ++ch) {
             const bool more = ch + 1 < NCH;
@@ -465,9 +467,9 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             VTR(5);
             issue_v2u(ch);
             commit_w(&bar_v2[1]);
-            if (more) {
-                op_wait(C::SL_VQ + ((ch + 1) & 1));
-                issue_v1u(ch + 1);
+            if (more && (ch & 1)) {          // next chunk pair (ch + 1, ch + 2)
+                op_wait(C::SL_VQ);
+                issue_v1u();
             }
             commit_w(&bar[7]);
             // refills: the -Pq / D_a(ch) tiles are free once V2p(ch) (issued after V1p(ch))
@@ -482,8 +484,8 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             VTR(7);
 #undef VTR
             if (more) op_load(C::SL_DTW, sDTW, ops + C::O_DTW + (size_t)(ch + 1) * C::OPDTW, C::OPDTW * 4);
-            if (ch + 2 < NCH)
-                op_load(C::SL_VQ + (ch & 1), sVq(ch & 1), ops + C::O_VQ + (size_t)(ch + 2) * C::OPVQ, C::OPVQ * 4);
+            if (!(ch & 1) && ch + 2 < NCH)   // pair ch/2 consumed (V1u issued before V2u(ch)): next pair
+                op_load(C::SL_VQ, sVq, ops + C::O_VQ + (size_t)(ch / 2 + 1) * C::OPVQ, C::OPVQ * 4);
         }
         nB = NCH + 1;                        // group-B completions so far (V1u(0), per-chunk u commits)
         // ---- surface: per (face, half) step s: traces(s) (group A) are issued as
@@ -674,7 +676,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             {
                 float U[3][4];
 #pragma unroll
-                for (int i = 0; i < 3; ++i) ld4(tl + UO + 16 * i + 4 * sub, U[i]);
+                for (int i = 0; i < 3; ++i) ld4(tl + UO + 32 * i + 16 * (ch & 1) + 4 * sub, U[i]);
                 wait_ld();
 #pragma unroll
                 for (int m = 0; m < 3; ++m) {

@@ -139,7 +139,7 @@ def split_images(*blocks):
 
 def umma_operator_images(ref, ru, cfg):
     """All reference operators of the tcgen05 fused stage (csrc/wadg_fused_umma.cuh,
-    CfgU offsets): per volume chunk D_a, Vq, DTW_a, -Pq; Vfi per
+    CfgU offsets): per volume chunk D_a, DTW_a, -Pq and per chunk pair Vq; Vfi per
     16-point half of the face rule; -Pf per face and half; update chunks Vu, Pu."""
     NP, NQ = ref.Np, ref.Nq
     QC, NCH, NPK, NPN, NFPK, NFH = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"], cfg["nfq8"]
@@ -158,8 +158,8 @@ def umma_operator_images(ref, ru, cfg):
     parts = []
     for ch in range(NCH):                   # D_a: rows a*16 + qq
         parts.append(split_images(np.vstack([rows(D, ch * QC, QC, NPK) for D in ref.Dq])))
-    for ch in range(NCH):                   # Vq: rows qq of a chunk
-        parts.append(split_images(rows(ref.Vq, ch * QC, QC, NPK)))
+    for pr in range(-(-NCH // 2)):          # Vq: rows qq of a chunk pair (2 QC quadrature points)
+        parts.append(split_images(rows(ref.Vq, pr * 2 * QC, 2 * QC, NPK)))
     for ch in range(NCH):                   # DTW_a: 3 blocks of (NPN rows j) x (QC columns q)
         parts.append(split_images(*[rows(M.T, ch * QC, QC, NPN).T for M in DTW]))
     for ch in range(NCH):                   # -Pq: (NPN rows j) x (QC columns q)
