@@ -72,8 +72,9 @@ struct CfgD {
     static constexpr size_t SQ = (size_t)FLD * NPP * KBS * 8;
     static constexpr size_t PH_V = ((size_t)IMG_VA + IMG_VB + (size_t)6 * QC * KBS) * 8;
     static constexpr size_t S_P1 = (size_t)FLD * NFPK * KBS * 8;
+    static constexpr bool DBLP = N <= 6;                   // double-buffered neighbour face nodes
     static constexpr size_t S_TAB = (size_t)rup(2 * NF * KB + NF * NFP + NF * 6 * NFP + 6 * NFP, 4) * 4;
-    static constexpr size_t PH_S = 2 * S_P1 + ((size_t)FLD * NFQP * KBS + IMG_VFI + IMG_LIFT) * 8 + S_TAB;
+    static constexpr size_t PH_S = (DBLP ? 2 : 1) * S_P1 + ((size_t)FLD * NFQP * KBS + IMG_VFI + IMG_LIFT) * 8 + S_TAB;
     static constexpr size_t PH_U = ((size_t)FLD * NPP * KBS + IMG_U1 + IMG_U2 + (size_t)FLD * QC * KBS) * 8;
     static constexpr size_t PH = fused::maxz(PH_V, fused::maxz(PH_S, PH_U));
     static constexpr size_t SMEM = 16 + SQ + PH;
@@ -109,8 +110,8 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
     // volume
     double *sVA = ph, *sVB = sVA + C::IMG_VA, *sW = sVB + C::IMG_VB;           // sW: [6][QC][KBS]
     // surface
-    double *sP = ph;                                                           // [2][FLD][NFPK][KBS]
-    double *sG = sP + 2 * FLD * NFPK * KBS;                                    // [FLD][NFQP][KBS]
+    double *sP = ph;                                                           // [1 or 2][FLD][NFPK][KBS]
+    double *sG = sP + (C::DBLP ? 2 : 1) * FLD * NFPK * KBS;                    // [FLD][NFQP][KBS]
     double *sVfi = sG + FLD * NFQP * KBS;
     double *sLift = sVfi + C::IMG_VFI;
     int32_t *sNbr = reinterpret_cast<int32_t *>(sLift + C::IMG_LIFT);
@@ -311,12 +312,12 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
     };
     gather(0, sP);
     for (int f = 0; f < NF; ++f) {
-        double *cur = sP + (f & 1) * (FLD * NFPK * KBS);
-        if (f + 1 < NF) {
+        double *cur = C::DBLP ? sP + (f & 1) * (FLD * NFPK * KBS) : sP;
+        if (C::DBLP && f + 1 < NF) {
             gather(f + 1, sP + ((f + 1) & 1) * (FLD * NFPK * KBS));
             fused::cp_async_wait<1>();
         } else {
-            fused::cp_async_wait<0>();
+            fused::cp_async_wait<0>();   // single buffer: face f's nodes were gathered during face f-1's lift
         }
         tma(0, sLift, ops + C::O_LIFT + (size_t)f * C::IMG_LIFT, C::IMG_LIFT);   // lands during the traces
         __syncthreads();
@@ -387,6 +388,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
             }
         }
         __syncthreads();
+        if (!C::DBLP && f + 1 < NF) gather(f + 1, sP);   // the traces are done with the buffer
         twait(0);
         // lift: R_c += (-Pf_f) g_c
 #pragma unroll 2

@@ -769,10 +769,10 @@ static bool use_umma() {
     return true;
 }
 
-// DMMA (FP64 tensor core) fused stage: fp64, N = 2..5
+// DMMA (FP64 tensor core) fused stage: fp64, N = 2..7
 template <typename T, int N>
 static constexpr bool dmma_available() {
-    if constexpr (sizeof(T) == 8 && N >= 2 && N <= 5) return dk::CfgD<N>::SMEM <= 227 * 1024;
+    if constexpr (sizeof(T) == 8 && N >= 2 && N <= 7) return dk::CfgD<N>::SMEM <= 227 * 1024;
     return false;
 }
 
