@@ -43,7 +43,11 @@ struct CfgD {
     static constexpr int KBS = KB + 4;                     // shared row stride (doubles)
     static constexpr int MT = KB / 8;                      // element tiles
     static constexpr int WPM = NW / MT;                    // warps per element tile
-    static constexpr int QC = N <= 4 ? 32 : 16;            // quadrature points per chunk
+    static constexpr int QC = N == 4 ? 32 : 16;            // quadrature points per chunk
+    // two CTAs per SM at N <= 3 (<= 113 KB of shared memory, <= 128 registers):
+    // 12.5 -> 16.8 GDOF/s at N = 3; 16-element CTAs that would fit two per SM at
+    // N = 4, 5 leave half the warps idle in the point GEMMs and were 3 % slower
+    static constexpr int MINB = N <= 3 ? 2 : 1;
     static constexpr int NCH = cdiv(NQ, QC);
     static constexpr int QT = QC / 8;                      // point tiles per chunk
     static constexpr int JT = NPP / 8;                     // node tiles
@@ -94,7 +98,7 @@ __device__ __forceinline__ double afrag(const double *x, int mt, int ks, int lan
 }
 
 template <int N>
-__global__ void __launch_bounds__(CfgD<N>::NTH, 1)
+__global__ void __launch_bounds__(CfgD<N>::NTH, CfgD<N>::MINB)
 k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, double *__restrict__ Qout,
              double *__restrict__ res, double tau_p, double tau_u, double a_rk, double b_rk, double dt, int block0) {
     using C = CfgD<N>;

@@ -776,13 +776,13 @@ static constexpr bool dmma_available() {
     return false;
 }
 
-// default per order from B200 A/B timings: DMMA at N = 4, 5;
-// the DFMA tiles (two CTAs per SM) at N = 2, 3
+// default for every order it compiles for (N = 2..7): faster than the DFMA
+// tiles at every one in B200 A/B timings
 template <typename T, int N>
 static bool use_dmma() {
     if (!dmma_available<T, N>()) return false;
     if (g_fused_variant >= 0) return g_fused_variant == 3;
-    return N >= 4;
+    return true;
 }
 
 // info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),
