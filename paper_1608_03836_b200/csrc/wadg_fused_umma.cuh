@@ -782,11 +782,11 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             wait_st();
             to_mma(B_S0, true);
         };
-        // Face-node operands of the next face: with one step per face (N <= 3) they go
-        // in right after that step has read its traces, so the next face's traces
-        // overlap the step's flux; with two or more steps per face (N = 4) they go in
-        // at the face boundary, off the flux critical path.
-        if constexpr (NFH == 1) {
+        // Face-node operands of the next face go in right after the face's last step
+        // has read its traces, so the next face's traces overlap that step's flux
+        // (at N = 4 this beat writing them at the face boundary: surface 40.7k ->
+        // 38.3k cycles per tile).
+        {
             // face has read its traces (so the next traces overlap that step's flux)
             gather(0);
             load_fg(0);
@@ -832,78 +832,6 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 // neighbour nodes of the face after next: issued off the flux critical path,
                 // they have at least one step to land before node_store needs them
                 if (next_face && f + 2 < NF) gather(f + 2);
-            }
-        } else {
-            gather(0);
-            load_fg(0);
-            for (int f = 0; f < NF; ++f) {
-                fused::cp_async_wait<0>();       // this thread's staged neighbour nodes of face f
-                {
-                    const int c = sub;
-                    const float *xs = sStage + (size_t)c * NFP * ME + e;
-    #pragma unroll
-                    for (int i0 = 0; i0 < NFPK; i0 += 4) {
-                        float4 vh, vl, oh4, ol4;
-                        float *ph = reinterpret_cast<float *>(&vh), *pl = reinterpret_cast<float *>(&vl);
-                        float *qh = reinterpret_cast<float *>(&oh4), *ql = reinterpret_cast<float *>(&ol4);
-    #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const bool in = i0 + i < NFP;
-                            const float x = in ? xs[(i0 + i) * ME] : 0.f;
-                            const float y = in ? sQ[c * ME * NPK + kmaj_off<NPK>(e, sFmask[f * NFP + i0 + i]) / 4] : 0.f;
-                            ph[i] = tf32_split_hi(x);
-                            pl[i] = x - ph[i];
-                            qh[i] = tf32_split_hi(y);
-                            ql[i] = y - qh[i];
-                        }
-                        const uint32_t o = c * ME * NFPK + kmaj_off<NFPK>(e, i0) / 4;
-                        *reinterpret_cast<float4 *>(sExtHi + o) = vh;
-                        *reinterpret_cast<float4 *>(sExtLo + o) = vl;
-                        *reinterpret_cast<float4 *>(sOwnLo + o) = ol4;
-                        st4(tl + OWNH + 16 * c + i0, *reinterpret_cast<float (*)[4]>(qh));
-                    }
-    #pragma unroll
-                    for (int i0 = NFPK; i0 < 16; i0 += 4) {
-                        const float z4[4] = {0.f, 0.f, 0.f, 0.f};
-                        st4(tl + OWNH + 16 * c + i0, z4);
-                    }
-                }
-                wait_st();
-                to_mma(B_S0, true);
-                if (f + 1 < NF) gather(f + 1);   // in flight during this face's MMAs
-                for (int hh = 0; hh < NFH; ++hh) {
-                    const int step = f * NFH + hh;
-                    wait_A();                    // traces of this step
-                    float mM[4][4], mP[4][4];
-    #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        ld4(tl + OWN + 16 * c + 4 * sub, mM[c]);
-                        ld4(tl + EXT + 16 * c + 4 * sub, mP[c]);
-                    }
-                    wait_ld();
-                    fence_before();
-                    nb_arrive(B_S2, NB);         // trace columns free for the next step's MMAs
-                    float g[4][4];
-    #pragma unroll
-                    for (int p = 0; p < 4; ++p) {
-                        const float n0 = fg[0][p], n1 = fg[1][p], n2 = fg[2][p], sJh = fg[3][p];
-                        const float dpj = mP[0][p] - mM[0][p];
-                        const float dUn = (mP[1][p] - mM[1][p]) * n0 + (mP[2][p] - mM[2][p]) * n1 + (mP[3][p] - mM[3][p]) * n2;
-                        const float avg = (mP[1][p] + mM[1][p]) * n0 + (mP[2][p] + mM[2][p]) * n1 + (mP[3][p] + mM[3][p]) * n2;
-                        const float fpp = avg - tau_p * dpj;
-                        const float fuu = dpj - tau_u * dUn;
-                        g[0][p] = fpp * sJh;
-                        g[1][p] = fuu * (sJh * n0);
-                        g[2][p] = fuu * (sJh * n1);
-                        g[3][p] = fuu * (sJh * n2);
-                    }
-                    if (step + 1 < NSTEP) load_fg(step + 1);
-                    if (step > 0) wait_B();      // lift(step-1) done with the flux columns
-    #pragma unroll
-                    for (int c = 0; c < 4; ++c) st_split4(tl + GH + 16 * c + 4 * sub, tl + GL + 16 * c + 4 * sub, g[c]);
-                    wait_st();
-                    to_mma(B_S1);
-                }
             }
         }
         wait_B();                            // last lift: R complete
