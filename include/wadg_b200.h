@@ -155,16 +155,21 @@ int wadg_energy(const wadg_problem *P, const void *Q, double *partials,
  * the host packs opVA/opVB/opU1/opU2/liftT:
  *   info[0] kind: 0 = CUDA-core kernel ([nch][NPP][QC][4], [nch][QC][NPP][4],
  *                 [nch][NPP][QC], [nch][QC][NPP], [Nf*Nfq][NPP]);
- *                 1 = tensor-core kernel ([nch][4][NPP][QCS], [nch][4][QC][NJS],
- *                 [nch][NPP][QCS], [nch][QC][NJS], [Nf][NFQ8][NJS])
+ *                 2 = tcgen05 kernel (one buffer of K-major tile images);
+ *                 3 = DMMA kernel (one buffer of fragment-order images)
  *   info[1] elements per CTA, [2] QC, [3] nch, [4] NPP (K extent over nodes),
- *   info[5] QCS, [6] NJS (row strides), [7] NFQ8 (padded face points).
+ *   info[5], [6], [7]: kernel-specific extents (device.py reads them).
  * Returns nonzero if the pair is not compiled / does not fit. */
 int wadg_fused_config(int dtype, int order, int32_t *info, int64_t *smem_bytes);
 
-/* Debug: force the fused-stage kernel (0: CUDA-core FMA tiles, 1: split-TF32
- * warp-level mma.sync, 2: split-TF32 tcgen05 with TMEM accumulators, where
- * available); -1 restores the default.  Affects
+/* The same for a formulation (WADG_STRONG_WEAK or WADG_STRONG).  The strong
+ * form has a fused stage only on the FP64 tensor cores (kind 3, N = 2..5, the
+ * sufficiency rules at N_geo = N); other pairs return nonzero. */
+int wadg_fused_config_form(int dtype, int order, int formulation, int32_t *info, int64_t *smem_bytes);
+
+/* Debug: force the fused-stage kernel (0: CUDA-core FMA tiles, 2: split-TF32
+ * tcgen05 with TMEM accumulators, 3: FP64 DMMA, where available); -1 restores
+ * the default.  Affects
  * wadg_fused_config, so set it before building a problem. */
 int wadg_debug_set_fused_variant(int variant);
 

@@ -56,6 +56,8 @@ EXPORTS = {
     "wadg_energy": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, _vp], ctypes.c_int),
     "wadg_fused_config": ([ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i32),
                            ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "wadg_fused_config_form": ([ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_i32),
+                                ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "wadg_debug_set_fused_variant": ([ctypes.c_int], ctypes.c_int),
     "wadg_stage_fused": ([ctypes.POINTER(WadgProblem), _vp, _vp, _vp, ctypes.c_double, ctypes.c_double,
                           ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int,
@@ -106,13 +108,13 @@ def call(name, *args):
         raise NativeError(f"{name} failed ({rc}): {lib.wadg_last_error().decode()}")
 
 
-def fused_config(dtype_code, order):
-    """Layout of the fused stage for (dtype, order) as a dict, or None when
-    the pair is not compiled / does not fit (see include/wadg_b200.h)."""
+def fused_config(dtype_code, order, formulation=WADG_STRONG_WEAK):
+    """Layout of the fused stage for (dtype, order, formulation) as a dict, or
+    None when there is no fused stage for it (see include/wadg_b200.h)."""
     lib = load()
     info = (_i32 * 8)()
     smem = ctypes.c_int64()
-    if lib.wadg_fused_config(dtype_code, order, info, ctypes.byref(smem)) != 0:
+    if lib.wadg_fused_config_form(dtype_code, order, formulation, info, ctypes.byref(smem)) != 0:
         return None
     keys = ("kind", "kb", "qc", "nch", "npp", "qcs", "njs", "nfq8")
     out = dict(zip(keys, list(info)))

@@ -29,14 +29,19 @@ namespace dk {
 using fused::cdiv;
 using fused::rup;
 
-template <int N>
+// SW: strong-weak form with the 2N+1 rules ((N+1)^3 volume, (N+1)^2 face
+// points); otherwise the strong form with the sufficiency rules at N_geo = N
+// (4N-3 volume: (2N-1)^3 points, 4N-2 face: (2N)^2 points; R/PAPER.md:288,294),
+// the update always on the 2N+1 rule
+template <int N, bool SW = true>
 struct CfgD {
     static constexpr int NP = fused::np_tet(N);
     static constexpr int NPP = rup(NP, 8);                // nodes, padded to whole 8-wide tiles
-    static constexpr int NQ = (N + 1) * (N + 1) * (N + 1);
+    static constexpr int NQ = SW ? (N + 1) * (N + 1) * (N + 1) : (2 * N - 1) * (2 * N - 1) * (2 * N - 1);
+    static constexpr int NQU = (N + 1) * (N + 1) * (N + 1);
     static constexpr int NFP = fused::nfp_tri(N);
     static constexpr int NFPK = rup(NFP, 4);
-    static constexpr int NFQ = (N + 1) * (N + 1);
+    static constexpr int NFQ = SW ? (N + 1) * (N + 1) : 4 * N * N;
     static constexpr int NFQP = rup(NFQ, 8);
     static constexpr int NF = 4, FLD = 4, NTH = 256, NW = 8;
     static constexpr int KB = N <= 5 ? 32 : 16;            // elements per CTA
@@ -48,7 +53,11 @@ struct CfgD {
     // 12.5 -> 16.8 GDOF/s at N = 3; 16-element CTAs that would fit two per SM at
     // N = 4, 5 leave half the warps idle in the point GEMMs and were 3 % slower
     static constexpr int MINB = N <= 3 ? 2 : 1;
-    static constexpr int NCH = cdiv(NQ, QC);
+    static constexpr int NCH = cdiv(NQ, QC);               // volume chunks
+    static constexpr int NCHU = cdiv(NQU, QC);             // update chunks
+    static constexpr int NVA = SW ? 4 : 3;                 // operators of the point GEMM: D_a (and Vq)
+    static constexpr int NVB = SW ? 4 : 1;                 // of the projection GEMM: DTW_a, -Pq (or -Pq)
+    static constexpr int NWV = SW ? 6 : 4;                 // quadrature values per point: gp_i, F_a (or gp_i, div)
     static constexpr int QT = QC / 8;                      // point tiles per chunk
     static constexpr int JT = NPP / 8;                     // node tiles
     static constexpr int FT = NFQP / 8;                    // face-point tiles
@@ -59,8 +68,8 @@ struct CfgD {
     static constexpr int AT = cdiv(QT, WPM);               // point tiles per warp (volume A, update z)
     static constexpr int TT = cdiv(FT, WPM);               // face-point tiles per warp (traces)
     // operator images (doubles): [k step][n tile][32]
-    static constexpr int IMG_VA = 4 * (NPP / 4) * QT * 32;     // D_r, D_s, D_t, Vq of one chunk
-    static constexpr int IMG_VB = 4 * (QC / 4) * JT * 32;      // DTW_r, DTW_s, DTW_t, -Pq of one chunk
+    static constexpr int IMG_VA = NVA * (NPP / 4) * QT * 32;   // D_r, D_s, D_t (, Vq) of one chunk
+    static constexpr int IMG_VB = NVB * (QC / 4) * JT * 32;    // (DTW_r, DTW_s, DTW_t,) -Pq of one chunk
     static constexpr int IMG_VFI = (NFPK / 4) * FT * 32;
     static constexpr int IMG_LIFT = (NFQP / 4) * JT * 32;      // -Pf of one face
     static constexpr int IMG_U1 = (NPP / 4) * QT * 32;
@@ -70,13 +79,15 @@ struct CfgD {
     static constexpr size_t O_VFI = O_VB + (size_t)NCH * IMG_VB;
     static constexpr size_t O_LIFT = O_VFI + IMG_VFI;
     static constexpr size_t O_U1 = O_LIFT + (size_t)NF * IMG_LIFT;
-    static constexpr size_t O_U2 = O_U1 + (size_t)NCH * IMG_U1;
-    static constexpr size_t OP_TOTAL = O_U2 + (size_t)NCH * IMG_U2;
+    static constexpr size_t O_U2 = O_U1 + (size_t)NCHU * IMG_U1;
+    static constexpr size_t OP_TOTAL = O_U2 + (size_t)NCHU * IMG_U2;
     // shared memory (bytes)
     static constexpr size_t SQ = (size_t)FLD * NPP * KBS * 8;
-    static constexpr size_t PH_V = ((size_t)IMG_VA + IMG_VB + (size_t)6 * QC * KBS) * 8;
+    static constexpr size_t PH_V = ((size_t)IMG_VA + IMG_VB + (size_t)NWV * QC * KBS) * 8;
     static constexpr size_t S_P1 = (size_t)FLD * NFPK * KBS * 8;
-    static constexpr bool DBLP = N <= 6;                   // double-buffered neighbour face nodes
+    // double-buffered neighbour face nodes (single at N = 7 to fit; single for the
+    // strong form at N = 3, which would fit two CTAs per SM, was 3 % slower)
+    static constexpr bool DBLP = N <= 6;
     static constexpr size_t S_TAB = (size_t)rup(2 * NF * KB + NF * NFP + NF * 6 * NFP + 6 * NFP, 4) * 4;
     static constexpr size_t PH_S = (DBLP ? 2 : 1) * S_P1 + ((size_t)FLD * NFQP * KBS + IMG_VFI + IMG_LIFT) * 8 + S_TAB;
     static constexpr size_t PH_U = ((size_t)FLD * NPP * KBS + IMG_U1 + IMG_U2 + (size_t)FLD * QC * KBS) * 8;
@@ -97,12 +108,12 @@ __device__ __forceinline__ double afrag(const double *x, int mt, int ks, int lan
     return x[(4 * ks + (lane & 3)) * KBS + 8 * mt + (lane >> 2)];
 }
 
-template <int N>
-__global__ void __launch_bounds__(CfgD<N>::NTH, CfgD<N>::MINB)
+template <int N, bool SW>
+__global__ void __launch_bounds__(CfgD<N, SW>::NTH, CfgD<N, SW>::MINB)
 k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, double *__restrict__ Qout,
              double *__restrict__ res, double tau_p, double tau_u, double a_rk, double b_rk, double dt, int block0) {
-    using C = CfgD<N>;
-    constexpr int NP = C::NP, NPP = C::NPP, NQ = C::NQ, NFP = C::NFP, NFPK = C::NFPK, NFQ = C::NFQ;
+    using C = CfgD<N, SW>;
+    constexpr int NP = C::NP, NPP = C::NPP, NQ = C::NQ, NQU = C::NQU, NFP = C::NFP, NFPK = C::NFPK, NFQ = C::NFQ;
     constexpr int NFQP = C::NFQP, NF = 4, FLD = 4, KB = C::KB, KBS = C::KBS, MT = C::MT, WPM = C::WPM;
     constexpr int QC = C::QC, QT = C::QT, JT = C::JT, FT = C::FT, RT = C::RT, AT = C::AT, TT = C::TT;
     constexpr bool SPLIT = C::SPLIT;
@@ -112,7 +123,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
     double *sQ = reinterpret_cast<double *>(smem_raw + 16);
     double *ph = sQ + (size_t)FLD * NPP * KBS;
     // volume
-    double *sVA = ph, *sVB = sVA + C::IMG_VA, *sW = sVB + C::IMG_VB;           // sW: [6][QC][KBS]
+    double *sVA = ph, *sVB = sVA + C::IMG_VA, *sW = sVB + C::IMG_VB;           // sW: [NWV][QC][KBS]
     // surface
     double *sP = ph;                                                           // [1 or 2][FLD][NFPK][KBS]
     double *sG = sP + (C::DBLP ? 2 : 1) * FLD * NFPK * KBS;                    // [FLD][NFQP][KBS]
@@ -184,6 +195,66 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
     tma(1, sVB, ops + C::O_VB, C::IMG_VB);
     for (int ch = 0; ch < C::NCH; ++ch) {
         twait(0);
+        if constexpr (!SW) {
+            // strong form: du_a,c = D_a Q_c for all four fields; gp_i = sum_a G_ai du_a,0,
+            // div = sum_i sum_a G_ai du_a,i (R/pkg/src/wadg/solver.py:259-264)
+            double G[AT][2][9];
+#pragma unroll
+            for (int t = 0; t < AT; ++t)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int q = ch * QC + 8 * (w0 + WPM * t) + ec + h;
+                    const bool ok = w0 + WPM * t < QT && q < NQ;
+#pragma unroll
+                    for (int r = 0; r < 9; ++r)
+                        G[t][h][r] = ok ? __ldg(P.geo + (size_t)(r * NQ + q) * S + kblk + e) : 0.0;
+                }
+            double d[AT][3][FLD][2];
+#pragma unroll
+            for (int t = 0; t < AT; ++t)
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int c = 0; c < FLD; ++c) d[t][a][c][0] = d[t][a][c][1] = 0.0;
+#pragma unroll 2
+            for (int ks = 0; ks < NPP / 4; ++ks) {
+                double x[FLD];
+#pragma unroll
+                for (int c = 0; c < FLD; ++c) x[c] = afrag<KBS>(sQ + c * NPP * KBS, mt, ks, lane);
+#pragma unroll
+                for (int t = 0; t < AT; ++t) {
+                    const int qt = w0 + WPM * t;
+                    if (qt < QT) {
+#pragma unroll
+                        for (int a = 0; a < 3; ++a) {
+                            const double b = sVA[((a * (NPP / 4) + ks) * QT + qt) * 32 + lane];
+#pragma unroll
+                            for (int c = 0; c < FLD; ++c) dmma(d[t][a][c], x[c], b);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < AT; ++t) {
+                const int qt = w0 + WPM * t;
+                if (qt < QT) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int qq = 8 * qt + ec + h;
+                        const double *g = G[t][h];
+                        double div = 0.0;
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) {
+                            sW[(i * QC + qq) * KBS + e] =
+                                g[0 * 3 + i] * d[t][0][0][h] + g[1 * 3 + i] * d[t][1][0][h] + g[2 * 3 + i] * d[t][2][0][h];
+                            div += g[0 * 3 + i] * d[t][0][1 + i][h] + g[1 * 3 + i] * d[t][1][1 + i][h] +
+                                   g[2 * 3 + i] * d[t][2][1 + i][h];
+                        }
+                        sW[(3 * QC + qq) * KBS + e] = div;
+                    }
+                }
+            }
+        } else
         // A: dp_a = D_a p (m = 0..2), U_i = Vq u_i (m = 3..5) at the chunk's points; all
         // point tiles of this warp share the field fragments of a k step.  The
         // epilogue's geometric factors are loaded first, so their latency overlaps
@@ -248,7 +319,26 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
         __syncthreads();
         if (ch + 1 < C::NCH) tma(0, sVA, ops + C::O_VA + (size_t)(ch + 1) * C::IMG_VA, C::IMG_VA);
         twait(1);
-        // B: R_p += sum_a DTW_a F_a, R_u_i += (-Pq) gp_i
+        // B: R_p += sum_a DTW_a F_a (strong: (-Pq) div), R_u_i += (-Pq) gp_i
+        if constexpr (!SW) {
+#pragma unroll 2
+            for (int ks = 0; ks < QC / 4; ++ks) {
+                double w[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) w[m] = afrag<KBS>(sW + m * QC * KBS, mt, ks, lane);
+#pragma unroll
+                for (int t = 0; t < RT; ++t) {
+                    const int jt = rjt(t);
+                    if (jt < JT) {
+                        const double b = sVB[(ks * JT + jt) * 32 + lane];
+                        if (rfld(t, 0)) dmma(acc[t][0], w[3], b);
+#pragma unroll
+                        for (int i = 0; i < 3; ++i)
+                            if (rfld(t, 1 + i)) dmma(acc[t][1 + i], w[i], b);
+                    }
+                }
+            }
+        } else
 #pragma unroll 2
         for (int ks = 0; ks < QC / 4; ++ks) {
             double w[6];
@@ -380,7 +470,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
                                            (dpv[t][3][h] - dm[t][3][h]) * n2;
                         const double avg = (dpv[t][1][h] + dm[t][1][h]) * n0 + (dpv[t][2][h] + dm[t][2][h]) * n1 +
                                            (dpv[t][3][h] + dm[t][3][h]) * n2;
-                        const double fpp = avg - tau_p * djp;
+                        const double fpp = (SW ? avg : dUn) - tau_p * djp;   // strong: [u.n] (solver.py:220-232)
                         const double fuu = djp - tau_u * dUn;
                         // padded face points have zero factors, hence zero flux
                         sG[(0 * NFQP + fq) * KBS + e] = fpp * sJh;
@@ -434,7 +524,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
         }
     }
     __syncthreads();
-    for (int ch = 0; ch < C::NCH; ++ch) {
+    for (int ch = 0; ch < C::NCHU; ++ch) {
         twait(0);
         // z_c = Vu R_c at the chunk's points, times c^2/J (p) or 1/J (u); the weights
         // are loaded before the MMAs
@@ -445,7 +535,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int q = ch * QC + 8 * (w0 + WPM * t) + ec + h;
-                    const bool ok = w0 + WPM * t < QT && q < NQ;
+                    const bool ok = w0 + WPM * t < QT && q < NQU;
                     wu[t][h] = ok ? __ldg(P.wu + (size_t)q * S + kblk + e) : 0.0;
                     wp[t][h] = (ok && P.wp) ? __ldg(P.wp + (size_t)q * S + kblk + e) : 0.0;   // c^2 wu if no wp
                 }
@@ -484,7 +574,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
             }
         }
         __syncthreads();
-        if (ch + 1 < C::NCH) tma(0, sU1, ops + C::O_U1 + (size_t)(ch + 1) * C::IMG_U1, C::IMG_U1);
+        if (ch + 1 < C::NCHU) tma(0, sU1, ops + C::O_U1 + (size_t)(ch + 1) * C::IMG_U1, C::IMG_U1);
         twait(1);
         // R'_c += Pu (omega z_c)
 #pragma unroll 2
@@ -504,7 +594,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
             }
         }
         __syncthreads();
-        if (ch + 1 < C::NCH) tma(1, sU2, ops + C::O_U2 + (size_t)(ch + 1) * C::IMG_U2, C::IMG_U2);
+        if (ch + 1 < C::NCHU) tma(1, sU2, ops + C::O_U2 + (size_t)(ch + 1) * C::IMG_U2, C::IMG_U2);
     }
     WADG_PROF_MARK(4);
     // res = a res + dt Minv(rhs); Q_out = Q_in + b res  (this lane: element e, nodes ec, ec+1 of its tiles)

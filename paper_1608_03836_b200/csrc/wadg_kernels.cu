@@ -769,18 +769,19 @@ static bool use_umma() {
     return true;
 }
 
-// DMMA (FP64 tensor core) fused stage: fp64, N = 2..7
-template <typename T, int N>
+// DMMA (FP64 tensor core) fused stage: fp64, N = 2..7 (strong-weak), and the
+// strong form at N = 2..5 (its sufficiency rules at N_geo = N)
+template <typename T, int N, bool SW = true>
 static constexpr bool dmma_available() {
-    if constexpr (sizeof(T) == 8 && N >= 2 && N <= 7) return dk::CfgD<N>::SMEM <= 227 * 1024;
+    if constexpr (sizeof(T) == 8 && N >= 2 && N <= (SW ? 7 : 5)) return dk::CfgD<N, SW>::SMEM <= 227 * 1024;
     return false;
 }
 
 // default for every order it compiles for (N = 2..7): faster than the DFMA
 // tiles at every one in B200 A/B timings
-template <typename T, int N>
+template <typename T, int N, bool SW = true>
 static bool use_dmma() {
-    if (!dmma_available<T, N>()) return false;
+    if (!dmma_available<T, N, SW>()) return false;
     if (g_fused_variant >= 0) return g_fused_variant == 3;
     return true;
 }
@@ -788,10 +789,23 @@ static bool use_dmma() {
 // info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),
 //            quad-chunk row stride, node row stride, padded face points}
 template <typename T, int N>
-static int fused_cfg(int32_t *info, int64_t *smem) {
+static int fused_cfg(int32_t *info, int64_t *smem, int formulation = WADG_STRONG_WEAK) {
     size_t sm = 0;
     int32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool done = false;
+    if (formulation != WADG_STRONG_WEAK) {   // strong form: the DMMA stage only
+        if constexpr (dmma_available<T, N, false>()) {
+            if (use_dmma<T, N, false>()) {
+                using C = dk::CfgD<N, false>;
+                const int32_t w[8] = {3, C::KB, C::QC, C::NCH, C::NPP, C::NFPK, C::NFQP, (int32_t)C::OP_TOTAL};
+                if (info)
+                    for (int i = 0; i < 8; ++i) info[i] = w[i];
+                if (smem) *smem = (int64_t)C::SMEM;
+                return 0;
+            }
+        }
+        return 1;
+    }
     if constexpr (umma_available<T, N>()) {
         if (use_umma<T, N>()) {
             using C = uk::CfgU<N>;
@@ -867,6 +881,23 @@ static int fused_launch_umma(const wadg_problem *Pc, const void *Qin, void *Qout
     }
 }
 
+template <int N, bool SW>
+static int launch_dmma(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp, double tu,
+                       double a, double b, double dt, int b0, int b1, cudaStream_t st) {
+    using C = dk::CfgD<N, SW>;
+    if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
+    const int nblk = Pc->Kpad / C::KB;
+    if (b1 < 0 || b1 > nblk) b1 = nblk;
+    if (b0 < 0) b0 = 0;
+    if (b1 <= b0) return 0;
+    static bool attr_set[64] = {};
+    if (!attr_once(attr_set, (const void *)dk::k_stage_dmma<N, SW>, C::SMEM))
+        return fail("cudaFuncSetAttribute failed for the DMMA stage");
+    dk::k_stage_dmma<N, SW><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<double>(*Pc), (const double *)Qin,
+                                                            (double *)Qout, (double *)res, tp, tu, a, b, dt, b0);
+    return check_launch("wadg_stage_fused(dmma)");
+}
+
 template <typename T, int N>
 static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
                         double tu, double a, double b, double dt, int b0, int b1, int lay, cudaStream_t st) {
@@ -878,22 +909,15 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
         return fail("operators packed for the tcgen05 stage, which is not compiled for this dtype / order");
     }
     if (Pc->fused_kind == 3) {
-        if constexpr (dmma_available<T, N>()) {
-            using C = dk::CfgD<N>;
-            if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
-            if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
-            const int nblk = Pc->Kpad / C::KB;
-            if (b1 < 0 || b1 > nblk) b1 = nblk;
-            if (b0 < 0) b0 = 0;
-            if (b1 <= b0) return 0;
-            static bool attr_set[64] = {};
-            if (!attr_once(attr_set, (const void *)dk::k_stage_dmma<N>, C::SMEM))
-                return fail("cudaFuncSetAttribute failed for the DMMA stage");
-            dk::k_stage_dmma<N><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<double>(*Pc), (const double *)Qin,
-                                                                (double *)Qout, (double *)res, tp, tu, a, b, dt, b0);
-            return check_launch("wadg_stage_fused(dmma)");
+        if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
+        if (Pc->formulation == WADG_STRONG_WEAK) {
+            if constexpr (dmma_available<T, N, true>())
+                return launch_dmma<N, true>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+        } else {
+            if constexpr (dmma_available<T, N, false>())
+                return launch_dmma<N, false>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
         }
-        return fail("operators packed for the DMMA stage, which is not compiled for this dtype / order");
+        return fail("operators packed for the DMMA stage, which is not compiled for this dtype / order / form");
     }
     if (Pc->fused_kind != 0) return fail("unknown fused_kind");
     if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
@@ -1084,15 +1108,21 @@ int wadg_debug_set_fused_variant(int variant) {
 }
 
 int wadg_fused_config(int dtype, int order, int32_t *info, int64_t *smem) {
-    if (dtype == WADG_F64) { WADG_FUSED_SWITCH(double, order, fused_cfg, info, smem); }
-    if (dtype == WADG_F32) { WADG_FUSED_SWITCH(float, order, fused_cfg, info, smem); }
+    return wadg_fused_config_form(dtype, order, WADG_STRONG_WEAK, info, smem);
+}
+
+int wadg_fused_config_form(int dtype, int order, int formulation, int32_t *info, int64_t *smem) {
+    if (dtype == WADG_F64) { WADG_FUSED_SWITCH(double, order, fused_cfg, info, smem, formulation); }
+    if (dtype == WADG_F32) { WADG_FUSED_SWITCH(float, order, fused_cfg, info, smem, formulation); }
     return fail("bad dtype");
 }
 
 static int stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void *res, double tau_p, double tau_u,
                        double a, double b, double dt, int block_begin, int block_end, int lay, void *stream) {
     if (validate(P)) return 1;
-    if (P->dim != 3 || P->formulation != WADG_STRONG_WEAK) return fail("fused stage: 3D strong-weak only");
+    if (P->dim != 3) return fail("fused stage: tetrahedra only");
+    if (P->formulation != WADG_STRONG_WEAK && P->fused_kind != 3)
+        return fail("fused stage: the strong form runs on the DMMA stage (fp64) only");
     if (P->minv_p) return fail("fused stage: WADG mass inverse only (use wadg_stage for ExactCurvedMass)");
     if (!P->opVA || !P->opVB || !P->opU1 || !P->opU2 || !P->liftT) return fail("fused operators not packed");
     if (Qin == Qout) return fail("fused stage needs distinct Q_in / Q_out buffers");

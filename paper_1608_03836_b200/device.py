@@ -191,15 +191,19 @@ def frag_image(B, K, Nn):
     return Bp[kk, nn]
 
 
-def dmma_operator_images(ref, ru, cfg):
+def dmma_operator_images(ref, ru, cfg, strong_weak=True):
     """All reference operators of the DMMA fused stage (csrc/wadg_fused_dmma.cuh,
-    CfgD offsets), in fragment order: per volume chunk D_r, D_s, D_t, Vq (k = node,
-    n = point) and DTW_r, DTW_s, DTW_t, -Pq (k = point, n = node); Vfi; -Pf per
-    face; per update chunk Vu and Pu."""
+    CfgD offsets), in fragment order: per volume chunk D_r, D_s, D_t (, Vq) (k =
+    node, n = point) and (DTW_r, DTW_s, DTW_t,) -Pq (k = point, n = node); Vfi;
+    -Pf per face; per update chunk Vu and Pu.  The strong form has no Vq / DTW
+    images (its volume term is -Pq sum_i sum_a G_ai D_a u_i)."""
     NP, NQ = ref.Np, ref.Nq
     QC, NCH, NPP, NFPK, NFQP = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"]
+    NCHU = -(-ru.Nq // QC)
     nf, nfq = ref.n_faces, ref.nfq
     DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
+    va = list(ref.Dq) + ([ref.Vq] if strong_weak else [])
+    vb = (DTW if strong_weak else []) + [-ref.Pq]
 
     def cols(M, c0, n):                     # columns c0 .. c0+n of M (zero past the end)
         out = np.zeros((M.shape[0], n))
@@ -210,15 +214,15 @@ def dmma_operator_images(ref, ru, cfg):
 
     parts = []
     for ch in range(NCH):
-        parts += [frag_image(cols(Op.T, ch * QC, QC), NPP, QC) for Op in list(ref.Dq) + [ref.Vq]]
+        parts += [frag_image(cols(Op.T, ch * QC, QC), NPP, QC) for Op in va]
     for ch in range(NCH):
-        parts += [frag_image(cols(Op, ch * QC, QC).T, QC, NPP) for Op in DTW + [-ref.Pq]]
+        parts += [frag_image(cols(Op, ch * QC, QC).T, QC, NPP) for Op in vb]
     parts.append(frag_image(ref.face_interp.T, NFPK, NFQP))
     for f in range(nf):
         parts.append(frag_image(-ref.Pfq[:, f * nfq:(f + 1) * nfq].T, NFQP, NPP))
-    for ch in range(NCH):
+    for ch in range(NCHU):
         parts.append(frag_image(cols(ru.Vq.T, ch * QC, QC), NPP, QC))
-    for ch in range(NCH):
+    for ch in range(NCHU):
         parts.append(frag_image(cols(ru.Pq, ch * QC, QC).T, QC, NPP))
     out = np.concatenate([p.ravel() for p in parts])
     assert out.size == cfg["nfq8"], (out.size, cfg["nfq8"])
@@ -370,11 +374,16 @@ class DeviceProblem:
         None when the fused stage does not apply."""
         ref, ru = self.ref, self.ref_upd
         N = ref.N
-        if not (self.dim == 3 and self.sw and ref.Nq == (N + 1) ** 3 and ru.Nq == (N + 1) ** 3
-                and ref.nfq == (N + 1) ** 2):
+        if self.dim != 3 or ru.Nq != (N + 1) ** 3:
+            return None
+        if self.sw and not (ref.Nq == (N + 1) ** 3 and ref.nfq == (N + 1) ** 2):
+            return None
+        # strong form: the sufficiency rules at N_geo = N, (2N-1)^3 volume and (2N)^2 face points
+        if not self.sw and not (ref.Nq == (2 * N - 1) ** 3 and ref.nfq == (2 * N) ** 2):
             return None
         code = _native.WADG_F64 if self.dtype == torch.float64 else _native.WADG_F32
-        cfg = _native.fused_config(code, N)
+        form = _native.WADG_STRONG_WEAK if self.sw else _native.WADG_STRONG
+        cfg = _native.fused_config(code, N, form)
         if cfg is None:
             return None
         kb, qc, nch = cfg["kb"], cfg["qc"], cfg["nch"]
@@ -419,7 +428,7 @@ class DeviceProblem:
         if cfg["kind"] == 3:                    # DMMA kernel: one buffer of fragment-order images
             if self.Kpad % kb:
                 return None
-            self.ops["dmma"] = self._t(dmma_operator_images(ref, ru, cfg), torch.float64)
+            self.ops["dmma"] = self._t(dmma_operator_images(ref, ru, cfg, self.sw), torch.float64)
             for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
                 setattr(self.struct, name, self.ops["dmma"].data_ptr())
             self.fused_kind = 3

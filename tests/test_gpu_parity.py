@@ -358,3 +358,37 @@ def test_wadg_vs_exact_mass_error_ratio_3d():
         errs[mode] = np.sqrt(np.sum(W * (od.interp(np.asarray(st.p)) - pex) ** 2))
     ratio = errs[solver.MassMode.WADG] / errs[solver.MassMode.ExactCurvedMass]
     assert 0.99 <= ratio <= 1.01
+
+
+@pytest.mark.parametrize("N", [2, 3, 4])
+def test_fused_strong_form_stage_fp64(N, rng):
+    """The reference's default formulation (Strong, R/pkg/src/wadg/solver.py:70)
+    as one fused DMMA stage (fp64, the 4N-3 / 4N-2 sufficiency rules): against
+    the three-kernel stage and the oracle, heterogeneous medium, 2 steps; and
+    strong = strong-weak under sufficient quadrature on the same state."""
+    c2 = lambda x, y, z: 1 + 0.5 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y) * np.sin(2 * np.pi * z)
+    mesh = meshgen.warped_cube_tet_mesh(3, N)
+    cfg = SolverConfig(N=N, formulation=Formulation.Strong, flux=FluxParams(0.9, 1.2))
+    disc = solver.Discretization(mesh, cfg, solver.MediumField(c2))
+    assert disc.dev.fused is not None and disc.dev.fused_kind == 3
+    fl = _state3(mesh.K, disc.ref.Np, rng)
+    st = FieldState.from_fields(fl)
+    Qf = disc.to_device(st)
+    Qs = Qf.clone()
+    sf, ss = solver.DeviceStepper(disc, fused=True), solver.DeviceStepper(disc, fused=False)
+    dt = 2e-3
+    for _ in range(2):
+        Qf = sf.step(Qf, dt)
+        Qs = ss.step(Qs, dt)
+    a = disc.from_device(Qf, st, 0.0).fields()
+    b = disc.from_device(Qs, st, 0.0).fields()
+    assert rel(a, b) < 1e-13
+    od = O.OracleDiscretization(mesh, N, False, 0.9, 1.2, c2=c2)
+    ost = O.State(fl[0], fl[1:])
+    for _ in range(2):
+        ost = O.lsrk_step(ost, dt, lambda y: O.rhs_full(y, od))
+    assert rel(a, ost.fields()) < 1e-11
+    # lsrk_step(state, dt, disc.rhs) runs the fused stage for the strong form too
+    got = solver.lsrk_step(st, dt, disc.rhs)
+    want = O.lsrk_step(O.State(fl[0], fl[1:]), dt, lambda y: O.rhs_full(y, od))
+    assert rel(got.fields(), want.fields()) < 1e-11
