@@ -56,36 +56,43 @@ class SpectrumResult:
                 out.writerow([repr(lam.real), repr(lam.imag)])
 
 
-def assemble_evolution_matrix(mesh, config, medium=MediumField(), cap=6000):
+def assemble_evolution_matrix(mesh, config, medium=MediumField(), cap=6000, batch=None):
     """Dense matrix of the full semi-discrete operator (R/.../analysis.py:88-105).
 
     Column j is ``rhs_full`` applied to e_j. The ordering is field blocks of
-    K*Np, element-major within a block, as in the reference. The columns are
-    assembled on the device, and the result is returned as a host float64
-    array (n, n)."""
-    disc = Discretization(mesh, config, medium)
-    d = disc.dev
-    K, Np, fld = mesh.K, disc.ref.Np, disc.dim + 1
+    K*Np, element-major within a block, as in the reference. Columns are
+    assembled in batches: the mesh is replicated ``batch`` times
+    (``meshgen.replicate_mesh``), copy b carries the unit vector of column
+    j0 + b, and one device RHS pass (``wadg_volume`` + ``wadg_surface`` +
+    ``wadg_mass_inverse``) yields the whole batch. The result is returned as a
+    host float64 array (n, n)."""
+    from . import meshgen
+    K, fld = mesh.K, mesh.shape.dim + 1
+    probe = Discretization(mesh, config, medium)
+    Np = probe.ref.Np
     n = fld * K * Np
     if n > cap:
         raise SizeCapExceeded(f"{n} unknowns exceed cap {cap}")
-    Z = d.empty_fields()
-    pre = d.empty_fields()
-    out = d.empty_fields()
+    B = int(batch or max(1, min(n, (1 << 17) // max(K, 1))))
+    disc = Discretization(meshgen.replicate_mesh(mesh, B), config, medium)
+    d = disc.dev
+    Z, pre, out = d.empty_fields(), d.empty_fields(), d.empty_fields()
     A = torch.empty((n, n), dtype=torch.float64, device=d.device)
     s = d.struct
     sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     vp = lambda t: ctypes.c_void_p(t.data_ptr())
-    for j in range(n):
-        c, rem = divmod(j, K * Np)
-        k, i = divmod(rem, Np)
-        Z[c, i, k] = 1.0
+    for j0 in range(0, n, B):
+        nb = min(B, n - j0)
+        js = torch.arange(j0, j0 + nb, device=d.device)
+        c, rem = js // (K * Np), js % (K * Np)
+        Z.zero_()
+        Z[c, rem % Np, torch.arange(nb, device=d.device) * K + rem // Np] = 1.0
         _native.call("wadg_volume", ctypes.byref(s), vp(Z), vp(pre), sp)
         _native.call("wadg_surface", ctypes.byref(s), vp(Z), vp(pre), disc.flux.tau_p, disc.flux.tau_u,
                      1, 0, -1, sp)
         _native.call("wadg_mass_inverse", ctypes.byref(s), vp(pre), vp(out), sp)
-        A[:, j] = out[:, :, :K].permute(0, 2, 1).reshape(-1)
-        Z[c, i, k] = 0.0
+        cols = out[:, :, :nb * K].reshape(fld, Np, nb, K).permute(2, 0, 3, 1).reshape(nb, n)
+        A[:, j0:j0 + nb] = cols.T.to(torch.float64)
     return A.cpu().numpy()
 
 

@@ -257,6 +257,21 @@ def warped_cube_tet_mesh(n, N_geo, amp=0.1, nz=None, z_range=None, domain=(-1.0,
                       h=hx, provenance=prov, face_orientation=orient)
 
 
+def replicate_mesh(mesh, copies):
+    """``copies`` disjoint copies of ``mesh`` in one mesh (element k of copy b is
+    element b*K + k; neighbours stay within their copy).  Used to evaluate many
+    independent right-hand sides in one device pass (analysis.assemble_evolution_matrix)."""
+    K = mesh.K
+    off = (np.arange(copies, dtype=np.int64) * K)[:, None, None]
+    conn = np.broadcast_to(mesh.face_connectivity[None], (copies,) + mesh.face_connectivity.shape).copy()
+    inner = conn[..., 0] >= 0
+    conn[..., 0] = np.where(inner, conn[..., 0] + off, -1)
+    rep = lambda a: np.ascontiguousarray(np.broadcast_to(a[None], (copies,) + a.shape).reshape((copies * K,) + a.shape[1:]))
+    return CurvedMesh(mesh.shape, mesh.N_geo, rep(mesh.elem_map_nodes), conn.reshape(copies * K, -1, 2),
+                      rep(mesh.boundary_tags), h=mesh.h, provenance=dict(mesh.provenance, copies=copies),
+                      face_orientation=rep(np.asarray(mesh.face_orientation)))
+
+
 # ---------------------------------------------------------------------------
 # Interchange (R/.../meshgen.py:485-517, extended with shape "tetrahedron"
 # and the face_orientation array)
