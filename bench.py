@@ -127,16 +127,17 @@ def build_problem(cfg_name, N_override=None, dtype_override=None, rank=0, world=
     desc, n, N, dtype, het, _ = CONFIGS[cfg_name]
     N = N_override or N
     dtype = dtype_override or dtype
-    if cfg_name == "c5":
-        nz = 48 * world
-        mesh = meshgen.warped_cube_tet_mesh(n, N, nz=nz, z_range=(-1.0, -1.0 + 2.0 * nz / n))
-    else:
-        mesh = meshgen.warped_cube_tet_mesh(n, N)
+    nz, z_range = (48 * world, (-1.0, -1.0 + 2.0 * 48 * world / n)) if cfg_name == "c5" else (n, None)
     cfg = solver.SolverConfig(N=N, formulation=solver.Formulation.StrongWeak, dtype=dtype)
     medium = solver.MediumField(c2_het if het else 1.0)
     if world > 1:
-        disc = parallel.slab_discretization(mesh, cfg, medium, rank, world, n_layers=mesh.provenance["nz"])
+        # each rank generates only its z-slab plus one ghost layer per neighbour
+        # (parallel.ghosted_slab_mesh): no global mesh on any rank
+        disc = parallel.local_slab_discretization(n, N, cfg, medium, rank, world, nz=nz, z_range=z_range)
+        mesh = disc.mesh
+        mesh.K_total = 6 * n * n * nz
     else:
+        mesh = meshgen.warped_cube_tet_mesh(n, N, nz=nz, z_range=z_range)
         disc = solver.Discretization(mesh, cfg, medium)
     return mesh, cfg, medium, disc, desc
 
@@ -579,7 +580,8 @@ def main():
             "scaling": "weak" if args.config == "c5" else "strong",
             "vs_baseline": None,
             "dtype": "f32" if cfg.dtype == "float32" else "f64", "data": "synthetic",
-            "config": {"workload": desc, "K": mesh.K, "N": N, "Np": Np, "formulation": "strong-weak",
+            "config": {"workload": desc, "K": getattr(mesh, "K_total", mesh.K), "N": N, "Np": Np,
+                       "formulation": "strong-weak",
                        "dt": dt, "l2": "inputs > L2 (fields+geometry ~GBs); no flush needed",
                        "parallelism": f"z-slabs x{world}", "setup_s": round(setup_s, 1)},
             "roofline": ({"bound": "hbm", "kernel": top, "achieved": achieved, "peak": hbm_peak,

@@ -221,7 +221,7 @@ def warp_cube(x, y, z, amp=0.1):
             z + amp * cz * c3x * cy)
 
 
-def warped_cube_tet_mesh(n, N_geo, amp=0.1, nz=None, z_range=None, domain=(-1.0, 1.0)):
+def warped_cube_tet_mesh(n, N_geo, amp=0.1, nz=None, z_range=None, domain=(-1.0, 1.0), z_grid=None):
     """n x n x nz cubes on [-1,1]^2 x z_range, 6 Kuhn tets each, element
     order (kz, tet, ky, kx): z-major so z-slabs are contiguous ranges, and
     within a z-layer grouped by Kuhn tet type, so that consecutive elements
@@ -231,13 +231,20 @@ def warped_cube_tet_mesh(n, N_geo, amp=0.1, nz=None, z_range=None, domain=(-1.0,
 
     Default nz = n and z_range = domain (the cube of configs 2-4).  For the
     weak-scaling config 5 pass nz = 48*G and z_range = (-1, -1 + 2*nz/n) ...
-    the warp is evaluated in physical coordinates in any case."""
-    nz = n if nz is None else nz
+    the warp is evaluated in physical coordinates in any case.  ``z_grid``
+    (nz + 1 values) gives the layer planes explicitly (a slab of a larger mesh,
+    with node coordinates bitwise equal to the larger mesh's)."""
     lo, hi = domain
-    zlo, zhi = (lo, hi) if z_range is None else z_range
     hx = (hi - lo) / n
     gx = lo + hx * np.arange(n + 1)
-    gz = np.linspace(zlo, zhi, nz + 1)
+    if z_grid is not None:
+        gz = np.asarray(z_grid, dtype=np.float64)
+        nz = len(gz) - 1
+        zlo, zhi = float(gz[0]), float(gz[-1])
+    else:
+        nz = n if nz is None else nz
+        zlo, zhi = (lo, hi) if z_range is None else z_range
+        gz = np.linspace(zlo, zhi, nz + 1)
     local = _kuhn_local()                                           # (6, 4, 3)
     kz, ky, kx = np.meshgrid(np.arange(nz), np.arange(n), np.arange(n), indexing="ij")
     base = np.stack([kx.ravel(), ky.ravel(), kz.ravel()], axis=1)   # (C, 3) z-major

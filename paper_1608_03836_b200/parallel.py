@@ -177,6 +177,57 @@ class HaloExchange:
                            lambda b0, b1, st: self.native.call("wadg_stage_fused", *args, b0, b1, st))
 
 
+def ghosted_slab_mesh(n, N_geo, rank, world, nz=None, z_range=None, amp=0.1, domain=(-1.0, 1.0)):
+    """Rank's z-slab of the warped cube (meshgen.warped_cube_tet_mesh) with one
+    ghost layer of cubes towards each neighbour rank, generated directly: no
+    global mesh.  Node coordinates are bitwise those of the global mesh (the
+    global layer planes are passed through), and element numbering is the
+    global one shifted by a constant, so canonical halo orders agree.
+    Returns (mesh, owned element range in it, [(local range, global rank)] of
+    all parts)."""
+    from . import meshgen
+    nz = n if nz is None else nz
+    zlo, zhi = domain if z_range is None else z_range
+    gz = np.linspace(zlo, zhi, nz + 1)
+    bounds = [(r * nz) // world for r in range(world + 1)]
+    l0, l1 = bounds[rank], bounds[rank + 1]
+    g0, g1 = max(0, l0 - 1), min(nz, l1 + 1)
+    mesh = meshgen.warped_cube_tet_mesh(n, N_geo, amp=amp, domain=domain, z_grid=gz[g0:g1 + 1])
+    per = mesh.K // (g1 - g0)
+    parts = []
+    if l0 > g0:
+        parts.append(((0, (l0 - g0) * per), rank - 1))
+    owned = ((l0 - g0) * per, (l1 - g0) * per)
+    parts.append((owned, rank))
+    if g1 > l1:
+        parts.append((((l1 - g0) * per, (g1 - g0) * per), rank + 1))
+    return mesh, owned, parts
+
+
+def local_halo_plan(mesh, parts, rank):
+    """The rank's HaloPlan from its ghosted slab mesh (same message orders and
+    slots as halo_plans on the global mesh; peers are global ranks)."""
+    ranges = [r for r, _ in parts]
+    ranks = [g for _, g in parts]
+    me = ranks.index(rank)
+    plan = halo_plans(mesh, ranges)[me]
+    plan.peers = [(ranks[s], ns, nr) for s, ns, nr in plan.peers]
+    return plan
+
+
+def local_slab_discretization(n, N_geo, config, medium, rank, world, nz=None, z_range=None, amp=0.1,
+                              group=None, dist=None):
+    """slab_discretization without the global mesh: the rank builds only its
+    ghosted slab (ghosted_slab_mesh) and its own halo plan."""
+    from .solver import Discretization
+    mesh, owned, parts = ghosted_slab_mesh(n, N_geo, rank, world, nz, z_range, amp)
+    plan = local_halo_plan(mesh, parts, rank)
+    disc = Discretization(mesh, config, medium, k_range=owned, halo=plan)
+    disc.dev
+    disc.exchange = HaloExchange(disc, plan, group, dist)
+    return disc
+
+
 def slab_discretization(mesh, config, medium, rank, world, n_layers, group=None, dist=None):
     """Discretization of rank's z-slab with its halo exchange attached as
     ``disc.exchange``."""

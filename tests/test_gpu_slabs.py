@@ -61,9 +61,10 @@ class LoopbackDist:
         return reqs
 
 
+@pytest.mark.parametrize("local", [False, True])
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 @pytest.mark.parametrize("fused", [True, False])
-def test_slab_exchange_loopback_is_bitwise_single_domain(dtype, fused, rng):
+def test_slab_exchange_loopback_is_bitwise_single_domain(dtype, fused, local, rng):
     N, world, nz = 3, 3, 6
     mesh = meshgen.warped_cube_tet_mesh(4, N, nz=nz, z_range=(-1.0, 2.0))
     cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype=dtype)
@@ -72,7 +73,11 @@ def test_slab_exchange_loopback_is_bitwise_single_domain(dtype, fused, rng):
     whole = solver.Discretization(mesh, cfg, medium)
     net = LoopbackNet()
     dists = [LoopbackDist(net, r) for r in range(world)]
-    slabs = [parallel.slab_discretization(mesh, cfg, medium, r, world, nz, dist=dists[r]) for r in range(world)]
+    if local:       # each rank builds only its ghosted slab (no global mesh)
+        slabs = [parallel.local_slab_discretization(4, N, cfg, medium, r, world, nz=nz, z_range=(-1.0, 2.0),
+                                                    dist=dists[r]) for r in range(world)]
+    else:
+        slabs = [parallel.slab_discretization(mesh, cfg, medium, r, world, nz, dist=dists[r]) for r in range(world)]
     ranges = parallel.slab_ranges(mesh.K, world, nz)
     assert all(len(s.exchange.halo_runs_f if fused else s.exchange.halo_runs) > 0 for s in slabs)
     if dtype == "float32":

@@ -109,3 +109,27 @@ def test_gloo_two_rank_halo_exchange():
         err, n = out[r]
         assert n == 2 * 2 * 2
         assert err < 1e-14
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_ghosted_slab_mesh_matches_global_partition(world):
+    """Per-rank slab generation (no global mesh): the owned elements' nodes,
+    the halo plan (message orders, receive slots, peers) and the device
+    neighbour tables equal those derived from the global mesh."""
+    n, N, nz = 3, 2, 8
+    mesh = meshgen.warped_cube_tet_mesh(n, N, nz=nz, z_range=(-1.0, 1.5))
+    ranges = parallel.slab_ranges(mesh.K, world, nz)
+    plans = parallel.halo_plans(mesh, ranges)
+    for r in range(world):
+        lm, owned, parts = parallel.ghosted_slab_mesh(n, N, r, world, nz=nz, z_range=(-1.0, 1.5))
+        lp = parallel.local_halo_plan(lm, parts, r)
+        a, b = ranges[r]
+        assert owned[1] - owned[0] == b - a
+        assert np.array_equal(lm.elem_map_nodes[owned[0]:owned[1]], mesh.elem_map_nodes[a:b])
+        gp = plans[r]
+        assert lp.peers == gp.peers
+        assert np.array_equal(lp.send_k, gp.send_k) and np.array_equal(lp.send_f, gp.send_f)
+        assert lp.recv_slot == gp.recv_slot
+        ln, lc = device.neighbour_tables(lm, 6, owned[0], owned[1], lp)
+        gn, gc = device.neighbour_tables(mesh, 6, a, b, gp)
+        assert np.array_equal(ln, gn) and np.array_equal(lc, gc)
