@@ -231,7 +231,7 @@ def dmma_issued_flops(N, Kpad):
     rup = lambda a, b: -(-a // b) * b
     NP = (N + 1) * (N + 2) * (N + 3) // 6
     NPP, NQ = rup(NP, 8), (N + 1) ** 3
-    QC = 32 if N == 4 else 16
+    QC = 16
     NCH = -(-NQ // QC)
     NFPK, NFQP = rup((N + 1) * (N + 2) // 2, 4), rup((N + 1) ** 2, 8)
     fma = (NCH * QC * NPP * (6 + 6)          # volume: 6 products each way

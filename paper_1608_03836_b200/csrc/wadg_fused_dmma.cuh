@@ -43,16 +43,15 @@ struct CfgD {
     static constexpr int NFPK = rup(NFP, 4);
     static constexpr int NFQ = SW ? (N + 1) * (N + 1) : 4 * N * N;
     static constexpr int NFQP = rup(NFQ, 8);
-    static constexpr int NF = 4, FLD = 4, NTH = 256, NW = 8;
-    static constexpr int KB = N <= 5 ? 32 : 16;            // elements per CTA
+    static constexpr int NF = 4, FLD = 4;
+    // elements per CTA: 24 (three element tiles, six warps) for strong-weak N = 4,
+    // so that two CTAs fit per SM (+1.5 %); 32 at N <= 5 otherwise; 16 at N = 6, 7
+    static constexpr int KB = (SW && N == 4) ? 24 : (N <= 5 ? 32 : 16);
+    static constexpr int NW = KB == 24 ? 6 : 8, NTH = 32 * NW;
     static constexpr int KBS = KB + 4;                     // shared row stride (doubles)
     static constexpr int MT = KB / 8;                      // element tiles
     static constexpr int WPM = NW / MT;                    // warps per element tile
-    static constexpr int QC = N == 4 ? 32 : 16;            // quadrature points per chunk
-    // two CTAs per SM at N <= 3 (<= 113 KB of shared memory, <= 128 registers):
-    // 12.5 -> 16.8 GDOF/s at N = 3; 16-element CTAs that would fit two per SM at
-    // N = 4, 5 leave half the warps idle in the point GEMMs and were 3 % slower
-    static constexpr int MINB = N <= 3 ? 2 : 1;
+    static constexpr int QC = (!SW && N == 4) ? 32 : 16;   // quadrature points per chunk
     static constexpr int NCH = cdiv(NQ, QC);               // volume chunks
     static constexpr int NCHU = cdiv(NQU, QC);             // update chunks
     static constexpr int NVA = SW ? 4 : 3;                 // operators of the point GEMM: D_a (and Vq)
@@ -93,6 +92,9 @@ struct CfgD {
     static constexpr size_t PH_U = ((size_t)FLD * NPP * KBS + IMG_U1 + IMG_U2 + (size_t)FLD * QC * KBS) * 8;
     static constexpr size_t PH = fused::maxz(PH_V, fused::maxz(PH_S, PH_U));
     static constexpr size_t SMEM = 16 + SQ + PH;
+    // two CTAs per SM where they fit (<= 113 KB of shared memory; registers then
+    // capped by the launch bounds): N = 3 12.5 -> 16.8 GDOF/s
+    static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;
 };
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {

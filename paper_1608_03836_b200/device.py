@@ -25,7 +25,7 @@ import torch
 from . import _native, geometry, refelem
 from .errors import ConfigError
 
-PAD = 128
+PAD = 384        # element padding: a multiple of every fused block size (128, 64, 32, 24, 16)
 CHUNK = 1 << 16
 
 
