@@ -202,12 +202,11 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
              float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt, int block0) {
     using C = CfgU<N>;
     using namespace umma;
-    constexpr int NP = C::NP, NPK = C::NPK, NPN = C::NPN, NQ = C::NQ, QC = C::QC, QU = C::QU;
+    constexpr int NP = C::NP, NPK = C::NPK, NPN = C::NPN, QC = C::QC, QU = C::QU;
     constexpr int NFP = C::NFP, NFPK = C::NFPK, NFQ = C::NFQ, NFH = C::NFH, NF = 4, ME = 128;
     constexpr int NCH = C::NCH, NCHU = C::NCHU, NSTEP = NF * NFH;
     constexpr uint32_t SBO_Q = (NPK / 4) * 128;        // 8-row group stride of NPK-wide tiles
     constexpr uint32_t SBO_16 = 4 * 128;                // ... of 16-wide tiles
-    constexpr uint32_t SBO_32 = 8 * 128;                // ... of 32-wide tiles
     constexpr uint32_t SBO_FP = (NFPK / 4) * 128;
     constexpr uint32_t RACC = C::RACC, SCR = C::SCR;
     constexpr uint32_t FQB = ME * NPK * 4;              // bytes of one field in sQ / sQlo

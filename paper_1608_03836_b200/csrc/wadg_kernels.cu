@@ -376,7 +376,7 @@ k_update(const Prob<T> P, const T *__restrict__ rhs, T *__restrict__ out, T *__r
         }
         __syncthreads();
     }
-    if (MODE == 0) {
+    if constexpr (MODE == 0) {
 #pragma unroll
         for (int r = 0; r < RJ; ++r) {
             const int j = g + r * NG;
@@ -386,7 +386,7 @@ k_update(const Prob<T> P, const T *__restrict__ rhs, T *__restrict__ out, T *__r
             }
         }
         return;
-    }
+    } else {
     // LSRK: the old res / Q values of one node row (all fields) are loaded
     // before its stores (the stores could alias the loads, so the compiler
     // would otherwise serialise one load-store round trip per value)
@@ -409,6 +409,7 @@ k_update(const Prob<T> P, const T *__restrict__ rhs, T *__restrict__ out, T *__r
                 Qo[o] = qo[c] + b * rr;
             }
         }
+    }
     }
 }
 
