@@ -392,3 +392,24 @@ def test_fused_strong_form_stage_fp64(N, rng):
     got = solver.lsrk_step(st, dt, disc.rhs)
     want = O.lsrk_step(O.State(fl[0], fl[1:]), dt, lambda y: O.rhs_full(y, od))
     assert rel(got.fields(), want.fields()) < 1e-11
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("N", [2, 3, 4])
+def test_single_curved_tet_fused_stage(N, dtype, rng):
+    """Edge case: one curved tetrahedron (K = 1, every face a mirror boundary,
+    a block that is almost all padding) through the default fused stage
+    (tcgen05 / DMMA) against the oracle, 3 steps."""
+    from test_oracle_3d import single_curved_tet
+    mesh = single_curved_tet(N)
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, flux=FluxParams(0.6, 1.4), dtype=dtype)
+    disc = solver.Discretization(mesh, cfg)
+    assert disc.dev.fused is not None
+    fl = _state3(1, disc.ref.Np, rng)
+    st = FieldState.from_fields(fl)
+    od = O.OracleDiscretization(mesh, N, True, 0.6, 1.4)
+    ost = O.State(fl[0], fl[1:])
+    for _ in range(3):
+        st = solver.lsrk_step(st, 1e-2, disc.rhs)
+        ost = O.lsrk_step(ost, 1e-2, lambda y: O.rhs_full(y, od))
+    assert rel(st.fields(), ost.fields()) < TOL[dtype]
