@@ -86,7 +86,8 @@ typedef struct wadg_problem {
      * operators repacked into quadrature chunks of QC points (see
      * wadg_fused_config), NPP = Np rounded up to 4, zero padded:          */
     int32_t order;
-    int32_t fused_kind;   /* kernel the operators below are packed for: 0 CUDA cores, 2 tcgen05 */
+    int32_t fused_kind;   /* kernel the operators below are packed for: 0 CUDA cores, 2 tcgen05,
+                           * 3 FP64 DMMA, 4 split-TF32 mma.sync (fp32, N >= 5)           */
     const void *opVA;     /* D_r, D_s, D_t, Vq at (q, j)   (layout: wadg_fused_config) */
     const void *opVB;     /* DTW_r, DTW_s, DTW_t, Pq at (j, q)                         */
     const void *opU1;     /* Vu                                                        */
@@ -168,7 +169,8 @@ int wadg_fused_config(int dtype, int order, int32_t *info, int64_t *smem_bytes);
 int wadg_fused_config_form(int dtype, int order, int formulation, int32_t *info, int64_t *smem_bytes);
 
 /* Debug: force the fused-stage kernel (0: CUDA-core FMA tiles, 2: split-TF32
- * tcgen05 with TMEM accumulators, 3: FP64 DMMA, where available); -1 restores
+ * tcgen05 with TMEM accumulators, 3: FP64 DMMA, 4: split-TF32 mma.sync m16n8k8,
+ * where available); -1 restores
  * the default.  Affects
  * wadg_fused_config, so set it before building a problem. */
 int wadg_debug_set_fused_variant(int variant);

@@ -29,6 +29,7 @@ namespace wadg {
 #include "wadg_umma.cuh"
 #include "wadg_fused_umma.cuh"
 #include "wadg_fused_dmma.cuh"
+#include "wadg_fused_tmma.cuh"
 
 namespace wadg {
 
@@ -739,7 +740,8 @@ static fused::FProb<T> make_fprob(const wadg_problem &p) {
     return q;
 }
 
-static int g_fused_variant = -1;   // debug override of the packing choice: 0 CUDA-core, 2 tcgen05, 3 DMMA, -1 default
+static int g_fused_variant = -1;   // debug override of the packing choice: 0 CUDA-core, 2 tcgen05, 3 DMMA,
+                                   // 4 split-TF32 mma.sync, -1 default
 
 // cudaFuncSetAttribute (max dynamic shared memory) is per device: one flag per
 // (kernel instantiation, device)
@@ -787,6 +789,20 @@ static bool use_dmma() {
     return true;
 }
 
+// split-TF32 mma.sync fused stage: fp32 at the orders the tcgen05 tile does not fit
+template <typename T, int N>
+static constexpr bool tmma_available() {
+    if constexpr (sizeof(T) == 4 && N >= 5 && N <= 7) return tk::CfgT<N>::SMEM <= 227 * 1024;
+    return false;
+}
+
+template <typename T, int N>
+static bool use_tmma() {
+    if (!tmma_available<T, N>()) return false;
+    if (g_fused_variant >= 0) return g_fused_variant == 4;
+    return false;
+}
+
 // info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),
 //            quad-chunk row stride, node row stride, padded face points}
 template <typename T, int N>
@@ -820,6 +836,15 @@ static int fused_cfg(int32_t *info, int64_t *smem, int formulation = WADG_STRONG
         if (!done && use_dmma<T, N>()) {
             using C = dk::CfgD<N>;
             const int32_t w[8] = {3, C::KB, C::QC, C::NCH, C::NPP, C::NFPK, C::NFQP, (int32_t)C::OP_TOTAL};
+            for (int i = 0; i < 8; ++i) v[i] = w[i];
+            sm = C::SMEM;
+            done = true;
+        }
+    }
+    if constexpr (tmma_available<T, N>()) {
+        if (!done && use_tmma<T, N>()) {
+            using C = tk::CfgT<N>;
+            const int32_t w[8] = {4, C::KB, C::QC, C::NCH, C::NPP, C::NFPK, C::NFQP, (int32_t)C::OP_TOTAL};
             for (int i = 0; i < 8; ++i) v[i] = w[i];
             sm = C::SMEM;
             done = true;
@@ -899,6 +924,24 @@ static int launch_dmma(const wadg_problem *Pc, const void *Qin, void *Qout, void
     return check_launch("wadg_stage_fused(dmma)");
 }
 
+template <int N>
+static int launch_tmma(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp, double tu,
+                       double a, double b, double dt, int b0, int b1, cudaStream_t st) {
+    using C = tk::CfgT<N>;
+    if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
+    const int nblk = Pc->Kpad / C::KB;
+    if (b1 < 0 || b1 > nblk) b1 = nblk;
+    if (b0 < 0) b0 = 0;
+    if (b1 <= b0) return 0;
+    static bool attr_set[64] = {};
+    if (!attr_once(attr_set, (const void *)tk::k_stage_tmma<N>, C::SMEM))
+        return fail("cudaFuncSetAttribute failed for the split-TF32 mma.sync stage");
+    tk::k_stage_tmma<N><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin, (float *)Qout,
+                                                         (float *)res, (float)tp, (float)tu, (float)a, (float)b,
+                                                         (float)dt, b0);
+    return check_launch("wadg_stage_fused(tmma)");
+}
+
 template <typename T, int N>
 static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp,
                         double tu, double a, double b, double dt, int b0, int b1, int lay, cudaStream_t st) {
@@ -919,6 +962,12 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
                 return launch_dmma<N, false>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
         }
         return fail("operators packed for the DMMA stage, which is not compiled for this dtype / order / form");
+    }
+    if (Pc->fused_kind == 4) {
+        if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
+        if constexpr (tmma_available<T, N>())
+            if (Pc->formulation == WADG_STRONG_WEAK) return launch_tmma<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+        return fail("operators packed for the split-TF32 mma.sync stage, which is not compiled for this dtype / order / form");
     }
     if (Pc->fused_kind != 0) return fail("unknown fused_kind");
     if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
@@ -1103,7 +1152,8 @@ int wadg_debug_set_phase_clock_buffer(void *buf) {
 }
 
 int wadg_debug_set_fused_variant(int variant) {
-    if (variant != -1 && variant != 0 && variant != 2 && variant != 3) return fail("variant must be -1, 0, 2 or 3");
+    if (variant != -1 && variant != 0 && variant != 2 && variant != 3 && variant != 4)
+        return fail("variant must be -1, 0, 2, 3 or 4");
     g_fused_variant = variant;
     return 0;
 }

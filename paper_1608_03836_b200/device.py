@@ -229,6 +229,55 @@ def dmma_operator_images(ref, ru, cfg, strong_weak=True):
     return out
 
 
+def tmma_frag_image(B, K, Nn):
+    """split-TF32 mma.sync m16n8k8 B-fragment image of B (k x n, zero padded to
+    K x Nn): [K/8][Nn/8][32][4], lane (g = lane // 4, t = lane % 4) holding
+    hi(B[8ks+t][8nt+g]), hi(B[8ks+t+4][8nt+g]) and the two lo parts, hi / lo
+    the round-to-nearest tf32 split (csrc/wadg_fused_tmma.cuh)."""
+    Bp = np.zeros((K, Nn))
+    Bp[:B.shape[0], :B.shape[1]] = B
+    lane = np.arange(32)
+    ks, nt = np.arange(K // 8), np.arange(Nn // 8)
+    kk = 8 * ks[:, None, None] + (lane % 4)[None, None, :]
+    nn = 8 * nt[None, :, None] + (lane // 4)[None, None, :]
+    hi, lo = tf32_split(Bp, "rn")
+    return np.stack([hi[kk, nn], hi[kk + 4, nn], lo[kk, nn], lo[kk + 4, nn]], axis=-1)
+
+
+def tmma_operator_images(ref, ru, cfg):
+    """All reference operators of the split-TF32 mma.sync stage (CfgT offsets),
+    in the order of dmma_operator_images (strong-weak form)."""
+    QC, NCH, NPP, NFPK, NFQP = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"]
+    NCHU = -(-ru.Nq // QC)
+    nf, nfq = ref.n_faces, ref.nfq
+    DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
+    va = list(ref.Dq) + [ref.Vq]
+    vb = DTW + [-ref.Pq]
+
+    def cols(M, c0, n):
+        out = np.zeros((M.shape[0], n))
+        c1 = min(M.shape[1], c0 + n)
+        if c1 > c0:
+            out[:, :c1 - c0] = M[:, c0:c1]
+        return out
+
+    parts = []
+    for ch in range(NCH):
+        parts += [tmma_frag_image(cols(Op.T, ch * QC, QC), NPP, QC) for Op in va]
+    for ch in range(NCH):
+        parts += [tmma_frag_image(cols(Op, ch * QC, QC).T, QC, NPP) for Op in vb]
+    parts.append(tmma_frag_image(ref.face_interp.T, NFPK, NFQP))
+    for f in range(nf):
+        parts.append(tmma_frag_image(-ref.Pfq[:, f * nfq:(f + 1) * nfq].T, NFQP, NPP))
+    for ch in range(NCHU):
+        parts.append(tmma_frag_image(cols(ru.Vq.T, ch * QC, QC), NPP, QC))
+    for ch in range(NCHU):
+        parts.append(tmma_frag_image(cols(ru.Pq, ch * QC, QC).T, QC, NPP))
+    out = np.concatenate([p.ravel() for p in parts]).astype(np.float32)
+    assert out.size == cfg["nfq8"], (out.size, cfg["nfq8"])
+    return out
+
+
 class DeviceProblem:
     """All device arrays of one (mesh range, reference elements, medium) and
     the C struct pointing at them."""
@@ -434,6 +483,16 @@ class DeviceProblem:
             self.fused_kind = 3
             self.struct.order = N
             self.struct.fused_kind = 3
+            return kb
+        if cfg["kind"] == 4:                    # split-TF32 mma.sync kernel: fragment-order hi / lo images
+            if self.Kpad % kb or not self.sw:
+                return None
+            self.ops["tmma"] = self._t(tmma_operator_images(ref, ru, cfg), torch.float32)
+            for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
+                setattr(self.struct, name, self.ops["tmma"].data_ptr())
+            self.fused_kind = 4
+            self.struct.order = N
+            self.struct.fused_kind = 4
             return kb
         # CUDA-core kernel layouts (kind 0)
         NPP = roundup(NP, 4)

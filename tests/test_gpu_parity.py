@@ -10,7 +10,7 @@ import pytest
 import torch
 
 import wadg_oracle as O
-from conftest import GOLDEN_CASES, golden_mesh, load_golden
+from conftest import GOLDEN_CASES, golden_mesh, load_golden, record_parity
 from paper_1608_03836_b200 import meshgen, solver
 from paper_1608_03836_b200.solver import FieldState, FluxParams, Formulation, SolverConfig
 
@@ -287,6 +287,36 @@ def test_tensor_core_and_cuda_core_fused_kernels_agree(N, rng):
         ost = O.lsrk_step(ost, 2e-3, lambda y: O.rhs_full(y, od))
     assert rel(outs[0], ost.fields()) < 1e-5
     assert rel(outs[2], ost.fields()) < 1e-5
+
+
+@pytest.mark.parametrize("N", [5, 6, 7])
+def test_tmma_and_cuda_core_fused_kernels_agree(N, rng):
+    """fp32 N >= 5: the split-TF32 mma.sync fused stage (kind 4) and the
+    CUDA-core FMA one give the same 2 steps to fp32 rounding, and both match
+    the oracle."""
+    from paper_1608_03836_b200 import _native
+    mesh = meshgen.warped_cube_tet_mesh(3, N)
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, flux=FluxParams(0.7, 1.3), dtype="float32")
+    fl = _state3(mesh.K, refelem_np(N), rng)
+    outs = {}
+    try:
+        for v in (0, 4):
+            _native.call("wadg_debug_set_fused_variant", v)
+            disc = solver.Discretization(mesh, cfg)
+            assert disc.dev.fused_kind == v and disc.dev.struct.fused_kind == v
+            st = FieldState.from_fields(fl)
+            for _ in range(2):
+                st = solver.lsrk_step(st, 2e-3, disc.rhs)
+            outs[v] = st.fields()
+    finally:
+        _native.call("wadg_debug_set_fused_variant", -1)
+    assert rel(outs[0], outs[4]) < 2e-6
+    od = O.OracleDiscretization(mesh, N, True, tau_p=0.7, tau_u=1.3)
+    ost = O.State(fl[0], fl[1:])
+    for _ in range(2):
+        ost = O.lsrk_step(ost, 2e-3, lambda y: O.rhs_full(y, od))
+    record_parity(f"tmma vs oracle N={N} fp32 2 steps", rel(outs[4], ost.fields()), 1e-5)
+    assert rel(outs[4], ost.fields()) < 1e-5
 
 
 def refelem_np(N):
