@@ -796,11 +796,13 @@ static constexpr bool tmma_available() {
     return false;
 }
 
+// default for every order it compiles for (N = 5..7): faster than the FFMA
+// tiles at each (config-5 mesh: 11.1 -> 13.2, 5.8 -> 8.6, 5.6 -> 7.3 GDOF/s)
 template <typename T, int N>
 static bool use_tmma() {
     if (!tmma_available<T, N>()) return false;
     if (g_fused_variant >= 0) return g_fused_variant == 4;
-    return false;
+    return true;
 }
 
 // info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),

@@ -98,7 +98,9 @@ def test_config4_physics_100_steps(dtype):
 
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
 def test_config5_physics_100_steps(dtype):
-    _check("config-5 physics", 6, 5, False, dtype, 100)
+    disc = _check("config-5 physics", 6, 5, False, dtype, 100)
+    if dtype == "float32":
+        assert disc.dev.fused_kind == 4          # the split-TF32 mma.sync stage
 
 
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
