@@ -240,6 +240,22 @@ def dmma_issued_flops(N, Kpad):
     return 2.0 * fma * Kpad
 
 
+def tmma_issued_flops(N, Kpad):
+    """Tensor-core flops the split-TF32 mma.sync stage issues per launch
+    (csrc/wadg_fused_tmma.cuh: m16n8k8 tf32 MMAs over padded extents, three per
+    product)."""
+    rup = lambda a, b: -(-a // b) * b
+    NP = (N + 1) * (N + 2) * (N + 3) // 6
+    NPP, NQ = rup(NP, 8), (N + 1) ** 3
+    QC = 16
+    NCH = -(-NQ // QC)
+    NFPK, NFQP = rup((N + 1) * (N + 2) // 2, 8), rup((N + 1) ** 2, 8)
+    fma = (NCH * QC * NPP * (6 + 6)
+           + 4 * (NFQP * NFPK * 8 + NFQP * NPP * 4)
+           + NCH * QC * NPP * (4 + 4))
+    return 2.0 * 3 * fma * Kpad
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -460,17 +476,20 @@ def main():
     # measured peaks (profiles/r02_measured_peaks.json), and the binding roof =
     # the larger of the two lower-bound times
     kind = getattr(d, "fused_kind", -1) if fused else -1
-    peaks_r02 = {"tcgen05_tf32": 1105.2, "dmma_f64": 37.1, "ffma": 71.8, "dfma": 34.1}
+    peaks_r02 = {"tcgen05_tf32": 1105.2, "dmma_f64": 37.1, "ffma": 71.8, "dfma": 34.1, "mma_sync_tf32": 278.8}
     pk_path = os.path.join(ROOT, "profiles", "r02_measured_peaks.json")
     if os.path.exists(pk_path):
         with open(pk_path) as f:
             tf = json.load(f)["tflops"]
         peaks_r02 = {"tcgen05_tf32": tf["tcgen05_tf32_tflops_TS_N256"], "dmma_f64": tf["dmma_f64_tflops"],
-                     "ffma": tf["fp32_fma_tflops"], "dfma": tf["fp64_fma_tflops"]}
+                     "ffma": tf["fp32_fma_tflops"], "dfma": tf["fp64_fma_tflops"],
+                     "mma_sync_tf32": tf["mma_sync_tf32_tflops"]}
     if kind == 2:
         issued, cpeak, cname = umma_issued_flops(N, d.Kpad), peaks_r02["tcgen05_tf32"], "tcgen05 kind::tf32"
     elif kind == 3:
         issued, cpeak, cname = dmma_issued_flops(N, d.Kpad), peaks_r02["dmma_f64"], "DMMA f64"
+    elif kind == 4:
+        issued, cpeak, cname = tmma_issued_flops(N, d.Kpad), peaks_r02["mma_sync_tf32"], "mma.sync tf32"
     else:
         issued = FL[top]
         cpeak, cname = (peaks_r02["ffma"], "FFMA") if cfg.dtype == "float32" else (peaks_r02["dfma"], "DFMA")
@@ -482,7 +501,7 @@ def main():
                "lower_bound_ms": {"hbm": t_hbm * 1e3, "compute": t_cmp * 1e3}}
     # measured DRAM traffic per launch from the committed ncu --set full capture
     traffic = None
-    kname = {2: "umma", 3: "dmma"}.get(getattr(d, "fused_kind", 0), "fused")
+    kname = {2: "umma", 3: "dmma", 4: "tmma"}.get(getattr(d, "fused_kind", 0), "fused")
     tname = f"ncu_stage_{kname}_{'f32' if cfg.dtype == 'float32' else 'f64'}_N{N}_{args.config}.json"
     tpath = os.path.join(ROOT, "profiles", "r02_" + tname)
     if not os.path.exists(tpath):
@@ -605,7 +624,8 @@ def main():
             "gpu_launches": (5 if fused else 15) * args.steps,
             "stage_kernel": "wadg_stage_fused" if fused else "wadg_volume+wadg_surface+wadg_update_lsrk",
             "fused_kernel": ({0: "k_stage_fused (CUDA-core FMA)", 2: "k_stage_umma (tcgen05 split-TF32, TMEM)",
-                              3: "k_stage_dmma (FP64 tensor cores, mma.sync m8n8k4)"}.get(getattr(d, "fused_kind", -1))
+                              3: "k_stage_dmma (FP64 tensor cores, mma.sync m8n8k4)",
+                              4: "k_stage_tmma (split-TF32 mma.sync m16n8k8)"}.get(getattr(d, "fused_kind", -1))
                              if fused else None),
             "clocks": clk,
             "storage_words_per_element": {"wadg_weights": 2 * Nqu, "dense_inverse": 2 * Np2,

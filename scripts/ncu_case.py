@@ -2,7 +2,7 @@
 the chosen case after warm-up, so `ncu -k regex:... -s W -c 1` lands on a
 steady-state launch.
 
-    python scripts/ncu_case.py c5_f32 | split_c4 | strong_f64_N4
+    python scripts/ncu_case.py c5_f32 | split_c4 | strong_f64_N4    (WADG_VARIANT=4: kernel kind)
 """
 import os, sys
 import numpy as np
@@ -15,6 +15,9 @@ from paper_1608_03836_b200 import meshgen, solver  # noqa: E402
 from paper_1608_03836_b200.solver import Formulation, SolverConfig  # noqa: E402
 
 case = sys.argv[1]
+if os.environ.get("WADG_VARIANT"):          # force a fused kernel (wadg_debug_set_fused_variant)
+    from paper_1608_03836_b200 import _native  # noqa: E402
+    _native.call("wadg_debug_set_fused_variant", int(os.environ["WADG_VARIANT"]))
 het = lambda x, y, z: 1.0 + 0.5 * torch.sin(2 * np.pi * x) * torch.sin(2 * np.pi * y) * torch.sin(2 * np.pi * z)
 if case == "c5_f32":
     mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(48, 5), SolverConfig(N=5, formulation=Formulation.StrongWeak, dtype="float32"), 1.0, True
