@@ -136,6 +136,12 @@ __device__ __forceinline__ void prod3(float (&d)[4], const AF &a, uint4 b) {
     hmma(d, a.h, b.x, b.y);
 }
 
+// the three split terms one at a time, so that a site issuing several
+// independent products interleaves them (consecutive HMMAs independent)
+__device__ __forceinline__ void term1(float (&d)[4], const AF &a, uint4 b) { hmma_z(d, a.l, b.x, b.y); }
+__device__ __forceinline__ void term2(float (&d)[4], const AF &a, uint4 b) { hmma(d, a.h, b.z, b.w); }
+__device__ __forceinline__ void term3(float (&d)[4], const AF &a, uint4 b) { hmma(d, a.h, b.x, b.y); }
+
 // running sum += A B in split-TF32
 __device__ __forceinline__ void prod3_acc(float (&d)[4], const AF &a, uint4 b) {
     hmma(d, a.l, b.x, b.y);
@@ -164,6 +170,7 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     constexpr int NFQP = C::NFQP, NF = 4, FLD = 4, KB = C::KB, KBS = C::KBS, MT = C::MT, WPM = C::WPM;
     constexpr int QC = C::QC, QT = C::QT, JT = C::JT, FT = C::FT, RT = C::RT;
 
+    static_assert(C::NTH == 256 && QC == 16 && KB == 32, "the volume epilogue maps 256 threads to 16 x 32 pairs");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
     float *sQ = reinterpret_cast<float *>(smem_raw + 16);
@@ -247,20 +254,22 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     tma(1, sVB, ops + C::O_VB, C::IMG_VB);
     for (int ch = 0; ch < C::NCH; ++ch) {
         twait(0);
-        // A: dp_a = D_a p (group 0) or U_i = Vq u_i (group 1) at point tile qt
+        // geometric factors of this thread's two (point, element) pairs of the
+        // chunk epilogue below, loaded before the MMAs so that their latency overlaps
+        float G[2][9];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int q = ch * QC + (tid >> 5) + 8 * h;
+#pragma unroll
+            for (int r = 0; r < 9; ++r) G[h][r] = q < NQ ? __ldg(P.geo + (size_t)(r * NQ + q) * S + kblk + lane) : 0.f;
+        }
+        // A: dp_a = D_a p (group 0) -> sW rows a, U_i = Vq u_i (group 1) -> sW rows 3 + i,
+        // at point tile qt; the independent products of a k step are issued term by term
 #pragma unroll
         for (int t = 0; t < C::AU; ++t) {
             const int u = w0 + WPM * t;
             if (u >= 2 * QT) continue;
             const int qt = u % QT, grp = u / QT;
-            float G[4][9];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int q = ch * QC + 8 * qt + 2 * tl + (i & 1);
-#pragma unroll
-                for (int r = 0; r < 9; ++r)
-                    G[i][r] = q < NQ ? __ldg(P.geo + (size_t)(r * NQ + q) * S + kblk + ent_e(i)) : 0.f;
-            }
             float d[3][4];
 #pragma unroll
             for (int m = 0; m < 3; ++m)
@@ -271,47 +280,55 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 for (int ks = 0; ks < NPP / 8; ++ks) {
                     AF x;
                     afrag<KBS>(x, sQ, mt, ks, lane);
+                    uint4 b[3];
+                    float f[3][4];
 #pragma unroll
-                    for (int m = 0; m < 3; ++m) {
-                        float f[4];
-                        prod3(f, x, bfrag(sVA, (m * (NPP / 8) + ks) * QT + qt, lane));
-                        add4(d[m], f);
-                    }
-                }
-                // gp_i = sum_a G_ai dp_a
+                    for (int m = 0; m < 3; ++m) b[m] = bfrag(sVA, (m * (NPP / 8) + ks) * QT + qt, lane);
 #pragma unroll
-                for (int i3 = 0; i3 < 3; ++i3) {
-                    float v[4];
+                    for (int m = 0; m < 3; ++m) term1(f[m], x, b[m]);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        v[i] = G[i][0 * 3 + i3] * d[0][i] + G[i][1 * 3 + i3] * d[1][i] + G[i][2 * 3 + i3] * d[2][i];
+                    for (int m = 0; m < 3; ++m) term2(f[m], x, b[m]);
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) st2(sW, i3 * QC + 8 * qt + 2 * tl + h, v[h], v[2 + h]);
+                    for (int m = 0; m < 3; ++m) term3(f[m], x, b[m]);
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) add4(d[m], f[m]);
                 }
             } else {
 #pragma unroll 1
                 for (int ks = 0; ks < NPP / 8; ++ks) {
                     const uint4 b = bfrag(sVA, (3 * (NPP / 8) + ks) * QT + qt, lane);
+                    AF x[3];
+                    float f[3][4];
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        AF x;
-                        afrag<KBS>(x, sQ + (1 + c) * NPP * KBS, mt, ks, lane);
-                        float f[4];
-                        prod3(f, x, b);
-                        add4(d[c], f);
-                    }
-                }
-                // F_a = sum_i G_ai U_i (the quadrature weight is folded into DTW)
+                    for (int c = 0; c < 3; ++c) afrag<KBS>(x[c], sQ + (1 + c) * NPP * KBS, mt, ks, lane);
 #pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    float v[4];
+                    for (int c = 0; c < 3; ++c) term1(f[c], x[c], b);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        v[i] = G[i][a * 3 + 0] * d[0][i] + G[i][a * 3 + 1] * d[1][i] + G[i][a * 3 + 2] * d[2][i];
+                    for (int c = 0; c < 3; ++c) term2(f[c], x[c], b);
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) st2(sW, (3 + a) * QC + 8 * qt + 2 * tl + h, v[h], v[2 + h]);
+                    for (int c = 0; c < 3; ++c) term3(f[c], x[c], b);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) add4(d[c], f[c]);
                 }
             }
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) st2(sW, (3 * grp + m) * QC + 8 * qt + 2 * tl + h, d[m][h], d[m][2 + h]);
+        }
+        __syncthreads();
+        // epilogue, one thread per (point, element) pair, in place: gp_i = sum_a G_ai dp_a,
+        // F_a = sum_i G_ai U_i (the quadrature weight is folded into DTW)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float *w = sW + ((tid >> 5) + 8 * h) * KBS + epos(lane);
+            const float *g = G[h];
+            const float d0 = w[0], d1 = w[QC * KBS], d2 = w[2 * QC * KBS];
+            const float u0 = w[3 * QC * KBS], u1 = w[4 * QC * KBS], u2 = w[5 * QC * KBS];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) w[i * QC * KBS] = g[0 * 3 + i] * d0 + g[1 * 3 + i] * d1 + g[2 * 3 + i] * d2;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) w[(3 + a) * QC * KBS] = g[a * 3 + 0] * u0 + g[a * 3 + 1] * u1 + g[a * 3 + 2] * u2;
         }
         __syncthreads();
         if (ch + 1 < C::NCH) tma(0, sVA, ops + C::O_VA + (size_t)(ch + 1) * C::IMG_VA, C::IMG_VA);
