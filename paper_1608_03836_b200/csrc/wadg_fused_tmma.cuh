@@ -114,6 +114,17 @@ __device__ __forceinline__ void afrag(AF &a, const float *x, int mt, int ks, int
     split2(a, 2, *reinterpret_cast<const float2 *>(x + (8 * ks + t + 4) * KBS + 16 * mt + 2 * g));
 }
 
+// the same fragment from pre-split hi / lo arrays
+template <int KBS>
+__device__ __forceinline__ void afrag_hl(AF &a, const float *xh, const float *xl, int mt, int ks, int lane) {
+    const int g = lane >> 2, t = lane & 3;
+    const int o0 = (8 * ks + t) * KBS + 16 * mt + 2 * g, o1 = o0 + 4 * KBS;
+    const uint2 h0 = *reinterpret_cast<const uint2 *>(xh + o0), h1 = *reinterpret_cast<const uint2 *>(xh + o1);
+    const uint2 l0 = *reinterpret_cast<const uint2 *>(xl + o0), l1 = *reinterpret_cast<const uint2 *>(xl + o1);
+    a.h[0] = h0.x, a.h[1] = h0.y, a.h[2] = h1.x, a.h[3] = h1.y;
+    a.l[0] = l0.x, a.l[1] = l0.y, a.l[2] = l1.x, a.l[3] = l1.y;
+}
+
 __device__ __forceinline__ void hmma(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
@@ -188,8 +199,9 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     int32_t *sExt = sFmask + NF * NFP;
     int32_t *sPerm = sExt + NF * 6 * NFP;
     // update
-    float *sR = ph;                                                            // [FLD][NPP][KBS]
-    float *sU1 = sR + FLD * NPP * KBS, *sU2 = sU1 + C::IMG_U1, *sW2 = sU2 + C::IMG_U2;   // sW2: [FLD][QC][KBS]
+    // R split once into hi (over sQ, free after the surface) and lo parts
+    float *sRh = sQ, *sRl = ph;                                                // [FLD][NPP][KBS]
+    float *sU1 = sRl + FLD * NPP * KBS, *sU2 = sU1 + C::IMG_U1, *sW2 = sU2 + C::IMG_U2;   // sW2: [FLD][QC][KBS]
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int mt = warp % MT, w0 = warp / MT;          // element tile; first n tile of this warp
@@ -513,7 +525,9 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     WADG_PROF_MARK(3);
     tma(0, sU1, ops + C::O_U1, C::IMG_U1);
     tma(1, sU2, ops + C::O_U2, C::IMG_U2);
-    // R -> sR[c][j][pos(e)] (the A operand of z = Vu R); accumulators restart at zero
+    // R -> sRh / sRl[c][j][pos(e)] (the A operand of z = Vu R, split once);
+    // accumulators restart at zero.  sQ is overwritten: the LSRK write re-reads Q_in.
+    __syncthreads();
 #pragma unroll
     for (int t = 0; t < RT; ++t) {
         const int jt = w0 + WPM * t;
@@ -521,7 +535,12 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 #pragma unroll
             for (int c = 0; c < FLD; ++c) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) st2(sR, c * NPP + 8 * jt + 2 * tl + h, acc[t][c][h], acc[t][c][2 + h]);
+                for (int h = 0; h < 2; ++h) {
+                    AF sp;
+                    split2(sp, 0, make_float2(acc[t][c][h], acc[t][c][2 + h]));
+                    st2(sRh, c * NPP + 8 * jt + 2 * tl + h, __uint_as_float(sp.h[0]), __uint_as_float(sp.h[1]));
+                    st2(sRl, c * NPP + 8 * jt + 2 * tl + h, __uint_as_float(sp.l[0]), __uint_as_float(sp.l[1]));
+                }
 #pragma unroll
                 for (int i = 0; i < 4; ++i) acc[t][c][i] = 0.f;
             }
@@ -555,7 +574,7 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
                     AF x;
-                    afrag<KBS>(x, sR + (2 * pr + cc) * NPP * KBS, mt, ks, lane);
+                    afrag_hl<KBS>(x, sRh + (2 * pr + cc) * NPP * KBS, sRl + (2 * pr + cc) * NPP * KBS, mt, ks, lane);
                     float f4[4];
                     prod3(f4, x, b);
                     add4(z[cc], f4);
@@ -616,7 +635,7 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                         const size_t o = (size_t)(c * NP + j) * S + kblk + ent_e(i);
                         const float r = a_rk * rold[i] + dt * acc[t][c][i];
                         res[o] = r;
-                        Qout[o] = sQ[(c * NPP + j) * KBS + pe + (i >> 1)] + b_rk * r;
+                        Qout[o] = __ldg(Qin + o) + b_rk * r;
                     }
                 }
             }
