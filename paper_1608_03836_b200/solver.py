@@ -732,6 +732,9 @@ class HostPipeline:
                     cur.wait_event(self.ev_in[waited])
             b0, b1 = self.blocks[c]
             qi, qo = self.bufs[(st - 1) % 2], self.bufs[st % 2]
+            if self.trace is not None:       # debug: per-launch start times
+                ev0 = torch.cuda.Event(enable_timing=True)
+                ev0.record(cur)
             if direct and st == 5:           # the last stage writes the row layout
                 _native.call("wadg_stage_fused_rows", s, _vp(qi), _vp(self.rows_out), _vp(res), fl.tau_p,
                              fl.tau_u, LSRK4A[st - 1], LSRK4B[st - 1], dt, b0, b1, 2, sp(cur))
@@ -741,7 +744,7 @@ class HostPipeline:
             if self.trace is not None:       # debug: per-launch end times on the compute stream
                 ev = torch.cuda.Event(enable_timing=True)
                 ev.record(cur)
-                self.trace.append((st, c, ev))
+                self.trace.append((st, c, ev0, ev))
             if st == 5:
                 self.ev_out[c].record(cur)
                 k0, k1 = self.elems[c]

@@ -9,6 +9,9 @@ __graft_entry__.build()
 import bench
 from paper_1608_03836_b200 import solver, _native
 
+TRACE_ONLY = "--trace-only" in sys.argv
+if TRACE_ONLY:
+    sys.argv.remove("--trace-only")
 mesh, cfg, medium, disc, desc = bench.build_problem("c4")
 d = disc.dev
 K, Np = d.K, disc.ref.Np
@@ -28,6 +31,8 @@ def timed(fn, n=4):
     return e0.elapsed_time(e1) / n
 
 
+if TRACE_ONLY:
+    sys.argv = sys.argv[:1] + ["none"]
 sp = solver.DeviceStepper(disc, fused=True)
 hold = [disc.to_device(st)]
 def dstep():
@@ -62,6 +67,8 @@ print(json.dumps(r), flush=True)
 del dev, hout
 args = sys.argv[1:] or ["auto", str(3 * sms), str(2 * sms)]
 for a in args:
+    if a == "none":
+        break
     if a == "auto":
         cb = None
     elif a.startswith("r"):      # ramped head: 1, 1, 1, 2 waves, then 3-wave chunks
@@ -158,15 +165,16 @@ def variant(copy_in=True, pack=True, copy_out=True, unpack=True, compute=True):
     cur.wait_stream(pipe.h2d); cur.wait_stream(pipe.d2h)
 
 
-for name, kw in (("all", {}), ("no_copies", dict(copy_in=False, copy_out=False)),
-                 ("no_pack_unpack", dict(pack=False, unpack=False)),
-                 ("no_copy_out", dict(copy_out=False, unpack=False)),
-                 ("no_copy_in", dict(copy_in=False, pack=False)),
-                 ("copies_only", dict(compute=False))):
+VARIANTS = (("all", {}), ("no_copies", dict(copy_in=False, copy_out=False)),
+            ("no_pack_unpack", dict(pack=False, unpack=False)),
+            ("no_copy_out", dict(copy_out=False, unpack=False)),
+            ("no_copy_in", dict(copy_in=False, pack=False)),
+            ("copies_only", dict(compute=False)))
+for name, kw in ([] if TRACE_ONLY else VARIANTS):
     print(json.dumps({"variant": name, "ms": timed(lambda: variant(**kw))}), flush=True)
 
 
-# per-launch timeline of one pipelined step (compute stream): gaps between launches
+# per-launch timeline of one pipelined step (compute stream): idle gaps before launches
 pipe = solver.HostPipeline(disc)
 for _ in range(2):
     pipe.step(st, dt)
@@ -175,14 +183,17 @@ start = torch.cuda.Event(enable_timing=True)
 pipe.trace = []
 start.record()
 pipe.step(st, dt)
+end = torch.cuda.Event(enable_timing=True)
+end.record()
 torch.cuda.synchronize()
-ends = [(s_, c_, start.elapsed_time(e)) for s_, c_, e in pipe.trace]
-ms_chunk = {}
-prev = 0.0
-gaps = []
-for s_, c_, t in ends:
-    gaps.append((s_, c_, round(t - prev, 3)))
-    prev = t
-print(json.dumps({"timeline_first_20 (stage, chunk, ms since previous end)": gaps[:20],
-                  "last_end_ms": round(ends[-1][2], 3), "n_launches": len(ends),
-                  "largest_10": sorted(gaps, key=lambda g: -g[2])[:10]}), flush=True)
+tl = [(s_, c_, start.elapsed_time(a), start.elapsed_time(b)) for s_, c_, a, b in pipe.trace]
+gaps, prev, busy = [], 0.0, 0.0
+for s_, c_, a, b in tl:
+    gaps.append((s_, c_, round(a - prev, 3)))
+    busy += b - a
+    prev = b
+print(json.dumps({"step_ms": round(start.elapsed_time(end), 3), "first_start_ms": round(tl[0][2], 3),
+                  "last_end_ms": round(tl[-1][3], 3), "kernel_busy_ms": round(busy, 3),
+                  "idle_ms": round(sum(g[2] for g in gaps), 3), "n_launches": len(tl),
+                  "largest_gaps (stage, chunk, ms)": sorted(gaps, key=lambda g: -g[2])[:12],
+                  "stage1_launch_ends": [round(b, 2) for s_, c_, a, b in tl if s_ == 1]}), flush=True)
