@@ -32,15 +32,19 @@ namespace tk {
 using fused::cdiv;
 using fused::rup;
 
-template <int N>
+// SW: strong-weak form with the 2N+1 rules ((N+1)^3 volume, (N+1)^2 face
+// points); otherwise the strong form with the sufficiency rules at N_geo = N
+// ((2N-1)^3 volume, (2N)^2 face points; R/PAPER.md:288,294), as in the DMMA
+// stage; the update always on the 2N+1 rule
+template <int N, bool SW = true>
 struct CfgT {
     static constexpr int NP = fused::np_tet(N);
     static constexpr int NPP = rup(NP, 8);
-    static constexpr int NQ = (N + 1) * (N + 1) * (N + 1);
-    static constexpr int NQU = NQ;
+    static constexpr int NQ = SW ? (N + 1) * (N + 1) * (N + 1) : (2 * N - 1) * (2 * N - 1) * (2 * N - 1);
+    static constexpr int NQU = (N + 1) * (N + 1) * (N + 1);
     static constexpr int NFP = fused::nfp_tri(N);
     static constexpr int NFPK = rup(NFP, 8);
-    static constexpr int NFQ = (N + 1) * (N + 1);
+    static constexpr int NFQ = SW ? (N + 1) * (N + 1) : 4 * N * N;
     static constexpr int NFQP = rup(NFQ, 8);
     static constexpr int NF = 4, FLD = 4;
     static constexpr int KB = 32;                          // elements per CTA: two 16-element tiles
@@ -52,12 +56,18 @@ struct CfgT {
     static constexpr int NCH = cdiv(NQ, QC), NCHU = cdiv(NQU, QC);
     static constexpr int QT = QC / 8, JT = NPP / 8, FT = NFQP / 8;
     static constexpr int RT = cdiv(JT, WPM);               // R node tiles per warp
-    static constexpr int AU = cdiv(2 * QT, WPM);           // (point tile, D_a p | Vq u) units per warp
+    // point-GEMM units: (point tile, D_a p | Vq u) for strong-weak, (point tile,
+    // field: D_a Q_c) for the strong form
+    static constexpr int NAU = SW ? 2 * QT : 4 * QT;
+    static constexpr int AU = cdiv(NAU, WPM);
+    static constexpr int NVA = SW ? 4 : 3;                 // operators of the point GEMM: D_a (, Vq)
+    static constexpr int NVB = SW ? 4 : 1;                 // of the projection: (DTW_a,) -Pq
+    static constexpr int NWR = SW ? 6 : 12;                // point-value rows of the volume (sW)
     static constexpr int TT = cdiv(FT, WPM);               // face-point tiles per warp
     static constexpr int ZU = cdiv(2 * QT, WPM);           // (point tile, field pair) units per warp
     static constexpr int FR = 128;                         // floats per fragment image (32 lanes x 4)
-    static constexpr int IMG_VA = 4 * (NPP / 8) * QT * FR; // D_r, D_s, D_t, Vq of one chunk
-    static constexpr int IMG_VB = 4 * (QC / 8) * JT * FR;  // DTW_r, DTW_s, DTW_t, -Pq of one chunk
+    static constexpr int IMG_VA = NVA * (NPP / 8) * QT * FR; // D_r, D_s, D_t (, Vq) of one chunk
+    static constexpr int IMG_VB = NVB * (QC / 8) * JT * FR;  // (DTW_r, DTW_s, DTW_t,) -Pq of one chunk
     static constexpr int IMG_VFI = (NFPK / 8) * FT * FR;
     static constexpr int IMG_LIFT = (NFQP / 8) * JT * FR;  // -Pf of one face
     static constexpr int IMG_U1 = (NPP / 8) * QT * FR;
@@ -71,7 +81,7 @@ struct CfgT {
     static constexpr size_t OP_TOTAL = O_U2 + (size_t)NCHU * IMG_U2;
     // shared memory (bytes)
     static constexpr size_t SQ = (size_t)FLD * NPP * KBS * 4;
-    static constexpr size_t PH_V = ((size_t)IMG_VA + IMG_VB + (size_t)6 * QC * KBS) * 4;
+    static constexpr size_t PH_V = ((size_t)IMG_VA + IMG_VB + (size_t)NWR * QC * KBS) * 4;
     static constexpr size_t S_P1 = (size_t)FLD * NFPK * KBS * 4;
     static constexpr size_t S_TAB = (size_t)rup(2 * NF * KB + NF * NFP + NF * 6 * NFP + 6 * NFP, 4) * 4;
     static constexpr size_t PH_S1 = ((size_t)FLD * NFQP * KBS + IMG_VFI + IMG_LIFT) * 4 + S_TAB;
@@ -172,11 +182,11 @@ __device__ __forceinline__ uint4 bfrag(const float *img, int idx, int lane) {
 // shared-memory position of element el (0..KB-1) of the CTA
 __device__ __forceinline__ int epos(int el) { return (el & ~15) + 2 * (el & 7) + ((el >> 3) & 1); }
 
-template <int N>
-__global__ void __launch_bounds__(CfgT<N>::NTH, CfgT<N>::MINB)
+template <int N, bool SW>
+__global__ void __launch_bounds__(CfgT<N, SW>::NTH, CfgT<N, SW>::MINB)
 k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *__restrict__ Qout,
              float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt, int block0) {
-    using C = CfgT<N>;
+    using C = CfgT<N, SW>;
     constexpr int NP = C::NP, NPP = C::NPP, NQ = C::NQ, NQU = C::NQU, NFP = C::NFP, NFPK = C::NFPK, NFQ = C::NFQ;
     constexpr int NFQP = C::NFQP, NF = 4, FLD = 4, KB = C::KB, KBS = C::KBS, MT = C::MT, WPM = C::WPM;
     constexpr int QC = C::QC, QT = C::QT, JT = C::JT, FT = C::FT, RT = C::RT;
@@ -187,7 +197,7 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     float *sQ = reinterpret_cast<float *>(smem_raw + 16);
     float *ph = sQ + (size_t)FLD * NPP * KBS;
     // volume
-    float *sVA = ph, *sVB = sVA + C::IMG_VA, *sW = sVB + C::IMG_VB;            // sW: [6][QC][KBS]
+    float *sVA = ph, *sVB = sVA + C::IMG_VA, *sW = sVB + C::IMG_VB;            // sW: [NWR][QC][KBS]
     // surface
     float *sP = ph;                                                            // [1 or 2][FLD][NFPK][KBS]
     float *sG = sP + (C::DBLP ? 2 : 1) * FLD * NFPK * KBS;                     // [FLD][NFQP][KBS]
@@ -275,23 +285,25 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 #pragma unroll
             for (int r = 0; r < 9; ++r) G[h][r] = q < NQ ? __ldg(P.geo + (size_t)(r * NQ + q) * S + kblk + lane) : 0.f;
         }
-        // A: dp_a = D_a p (group 0) -> sW rows a, U_i = Vq u_i (group 1) -> sW rows 3 + i,
-        // at point tile qt; the independent products of a k step are issued term by term
+        // A, strong-weak: dp_a = D_a p (group 0) -> sW rows a, U_i = Vq u_i (group 1) ->
+        // sW rows 3 + i; strong: du_a,c = D_a Q_c (unit field c) -> sW rows 3 c + a; at
+        // point tile qt, the independent products of a k step issued term by term
 #pragma unroll
         for (int t = 0; t < C::AU; ++t) {
             const int u = w0 + WPM * t;
-            if (u >= 2 * QT) continue;
+            if (u >= C::NAU) continue;
             const int qt = u % QT, grp = u / QT;
             float d[3][4];
 #pragma unroll
             for (int m = 0; m < 3; ++m)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) d[m][i] = 0.f;
-            if (grp == 0) {
+            if (!SW || grp == 0) {
+                const float *xf = sQ + (SW ? 0 : grp) * NPP * KBS;
 #pragma unroll 1
                 for (int ks = 0; ks < NPP / 8; ++ks) {
                     AF x;
-                    afrag<KBS>(x, sQ, mt, ks, lane);
+                    afrag<KBS>(x, xf, mt, ks, lane);
                     uint4 b[3];
                     float f[3][4];
 #pragma unroll
@@ -329,23 +341,59 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 for (int h = 0; h < 2; ++h) st2(sW, (3 * grp + m) * QC + 8 * qt + 2 * tl + h, d[m][h], d[m][2 + h]);
         }
         __syncthreads();
-        // epilogue, one thread per (point, element) pair, in place: gp_i = sum_a G_ai dp_a,
-        // F_a = sum_i G_ai U_i (the quadrature weight is folded into DTW)
+        // epilogue, one thread per (point, element) pair, in place: gp_i = sum_a G_ai dp_a
+        // and F_a = sum_i G_ai U_i (the quadrature weight is folded into DTW), or for the
+        // strong form gp_i and div = sum_i sum_a G_ai du_a,i (R/pkg/src/wadg/solver.py:259-264)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             float *w = sW + ((tid >> 5) + 8 * h) * KBS + epos(lane);
             const float *g = G[h];
             const float d0 = w[0], d1 = w[QC * KBS], d2 = w[2 * QC * KBS];
-            const float u0 = w[3 * QC * KBS], u1 = w[4 * QC * KBS], u2 = w[5 * QC * KBS];
+            if constexpr (SW) {
+                const float u0 = w[3 * QC * KBS], u1 = w[4 * QC * KBS], u2 = w[5 * QC * KBS];
 #pragma unroll
-            for (int i = 0; i < 3; ++i) w[i * QC * KBS] = g[0 * 3 + i] * d0 + g[1 * 3 + i] * d1 + g[2 * 3 + i] * d2;
+                for (int i = 0; i < 3; ++i) w[i * QC * KBS] = g[0 * 3 + i] * d0 + g[1 * 3 + i] * d1 + g[2 * 3 + i] * d2;
 #pragma unroll
-            for (int a = 0; a < 3; ++a) w[(3 + a) * QC * KBS] = g[a * 3 + 0] * u0 + g[a * 3 + 1] * u1 + g[a * 3 + 2] * u2;
+                for (int a = 0; a < 3; ++a)
+                    w[(3 + a) * QC * KBS] = g[a * 3 + 0] * u0 + g[a * 3 + 1] * u1 + g[a * 3 + 2] * u2;
+            } else {
+                float du[3][3];                  // [field i][a]
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) du[i][a] = w[(3 * (1 + i) + a) * QC * KBS];
+                float div = 0.f;
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    div += g[0 * 3 + i] * du[i][0] + g[1 * 3 + i] * du[i][1] + g[2 * 3 + i] * du[i][2];
+#pragma unroll
+                for (int i = 0; i < 3; ++i) w[i * QC * KBS] = g[0 * 3 + i] * d0 + g[1 * 3 + i] * d1 + g[2 * 3 + i] * d2;
+                w[3 * QC * KBS] = div;
+            }
         }
         __syncthreads();
         if (ch + 1 < C::NCH) tma(0, sVA, ops + C::O_VA + (size_t)(ch + 1) * C::IMG_VA, C::IMG_VA);
         twait(1);
-        // B: R_p += sum_a DTW_a F_a, R_u_i += (-Pq) gp_i
+        // B: R_p += sum_a DTW_a F_a (strong: (-Pq) div), R_u_i += (-Pq) gp_i
+        if constexpr (!SW) {
+#pragma unroll
+            for (int ks = 0; ks < QC / 8; ++ks) {
+#pragma unroll
+                for (int c = 0; c < FLD; ++c) {
+                    AF w;
+                    afrag<KBS>(w, sW + (c == 0 ? 3 : c - 1) * QC * KBS, mt, ks, lane);
+#pragma unroll
+                    for (int t = 0; t < RT; ++t) {
+                        const int jt = w0 + WPM * t;
+                        if (jt < JT) {
+                            float f[4];
+                            prod3(f, w, bfrag(sVB, ks * JT + jt, lane));
+                            add4(acc[t][c], f);
+                        }
+                    }
+                }
+            }
+        } else
 #pragma unroll
         for (int ks = 0; ks < QC / 8; ++ks) {
             float fp[RT][4];
@@ -484,7 +532,7 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                 const float djp = dp[0][i] - dm[0][i];
                 const float dUn = (dp[1][i] - dm[1][i]) * n0 + (dp[2][i] - dm[2][i]) * n1 + (dp[3][i] - dm[3][i]) * n2;
                 const float avg = (dp[1][i] + dm[1][i]) * n0 + (dp[2][i] + dm[2][i]) * n1 + (dp[3][i] + dm[3][i]) * n2;
-                const float fpp = avg - tau_p * djp;
+                const float fpp = (SW ? avg : dUn) - tau_p * djp;   // strong: [u.n] (solver.py:220-232)
                 const float fuu = djp - tau_u * dUn;
                 // padded face points have zero factors, hence zero flux
                 gv[0][i] = fpp * sJh;

@@ -790,17 +790,20 @@ static bool use_dmma() {
 }
 
 // split-TF32 mma.sync fused stage: fp32 at the orders the tcgen05 tile does not fit
-template <typename T, int N>
+// (strong-weak at N = 5..7, below which tcgen05 is faster; the strong form at
+// N = 2..5, its only fp32 fused stage)
+template <typename T, int N, bool SW = true>
 static constexpr bool tmma_available() {
-    if constexpr (sizeof(T) == 4 && N >= 5 && N <= 7) return tk::CfgT<N>::SMEM <= 227 * 1024;
+    if constexpr (sizeof(T) == 4 && (SW ? (N >= 5 && N <= 7) : (N >= 2 && N <= 5)))
+        return tk::CfgT<N, SW>::SMEM <= 227 * 1024;
     return false;
 }
 
 // default for every order it compiles for (N = 5..7): faster than the FFMA
 // tiles at each (config-5 mesh: 11.1 -> 13.2, 5.8 -> 8.6, 5.6 -> 7.3 GDOF/s)
-template <typename T, int N>
+template <typename T, int N, bool SW = true>
 static bool use_tmma() {
-    if (!tmma_available<T, N>()) return false;
+    if (!tmma_available<T, N, SW>()) return false;
     if (g_fused_variant >= 0) return g_fused_variant == 4;
     return true;
 }
@@ -812,7 +815,17 @@ static int fused_cfg(int32_t *info, int64_t *smem, int formulation = WADG_STRONG
     size_t sm = 0;
     int32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool done = false;
-    if (formulation != WADG_STRONG_WEAK) {   // strong form: the DMMA stage only
+    if (formulation != WADG_STRONG_WEAK) {   // strong form: the DMMA (fp64) or mma.sync tf32 (fp32) stage
+        if constexpr (tmma_available<T, N, false>()) {
+            if (use_tmma<T, N, false>()) {
+                using C = tk::CfgT<N, false>;
+                const int32_t w[8] = {4, C::KB, C::QC, C::NCH, C::NPP, C::NFPK, C::NFQP, (int32_t)C::OP_TOTAL};
+                if (info)
+                    for (int i = 0; i < 8; ++i) info[i] = w[i];
+                if (smem) *smem = (int64_t)C::SMEM;
+                return 0;
+            }
+        }
         if constexpr (dmma_available<T, N, false>()) {
             if (use_dmma<T, N, false>()) {
                 using C = dk::CfgD<N, false>;
@@ -926,19 +939,19 @@ static int launch_dmma(const wadg_problem *Pc, const void *Qin, void *Qout, void
     return check_launch("wadg_stage_fused(dmma)");
 }
 
-template <int N>
+template <int N, bool SW>
 static int launch_tmma(const wadg_problem *Pc, const void *Qin, void *Qout, void *res, double tp, double tu,
                        double a, double b, double dt, int b0, int b1, cudaStream_t st) {
-    using C = tk::CfgT<N>;
+    using C = tk::CfgT<N, SW>;
     if (Pc->Kpad % C::KB) return fail("Kpad must be a multiple of the fused block size");
     const int nblk = Pc->Kpad / C::KB;
     if (b1 < 0 || b1 > nblk) b1 = nblk;
     if (b0 < 0) b0 = 0;
     if (b1 <= b0) return 0;
     static bool attr_set[64] = {};
-    if (!attr_once(attr_set, (const void *)tk::k_stage_tmma<N>, C::SMEM))
+    if (!attr_once(attr_set, (const void *)tk::k_stage_tmma<N, SW>, C::SMEM))
         return fail("cudaFuncSetAttribute failed for the split-TF32 mma.sync stage");
-    tk::k_stage_tmma<N><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin, (float *)Qout,
+    tk::k_stage_tmma<N, SW><<<b1 - b0, C::NTH, C::SMEM, st>>>(make_fprob<float>(*Pc), (const float *)Qin, (float *)Qout,
                                                          (float *)res, (float)tp, (float)tu, (float)a, (float)b,
                                                          (float)dt, b0);
     return check_launch("wadg_stage_fused(tmma)");
@@ -967,8 +980,13 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
     }
     if (Pc->fused_kind == 4) {
         if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
-        if constexpr (tmma_available<T, N>())
-            if (Pc->formulation == WADG_STRONG_WEAK) return launch_tmma<N>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+        if (Pc->formulation == WADG_STRONG_WEAK) {
+            if constexpr (tmma_available<T, N, true>())
+                return launch_tmma<N, true>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+        } else {
+            if constexpr (tmma_available<T, N, false>())
+                return launch_tmma<N, false>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
+        }
         return fail("operators packed for the split-TF32 mma.sync stage, which is not compiled for this dtype / order / form");
     }
     if (Pc->fused_kind != 0) return fail("unknown fused_kind");
@@ -1174,8 +1192,8 @@ static int stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void 
                        double a, double b, double dt, int block_begin, int block_end, int lay, void *stream) {
     if (validate(P)) return 1;
     if (P->dim != 3) return fail("fused stage: tetrahedra only");
-    if (P->formulation != WADG_STRONG_WEAK && P->fused_kind != 3)
-        return fail("fused stage: the strong form runs on the DMMA stage (fp64) only");
+    if (P->formulation != WADG_STRONG_WEAK && P->fused_kind != 3 && P->fused_kind != 4)
+        return fail("fused stage: the strong form runs on the DMMA (fp64) or mma.sync tf32 (fp32) stage only");
     if (P->minv_p) return fail("fused stage: WADG mass inverse only (use wadg_stage for ExactCurvedMass)");
     if (!P->opVA || !P->opVB || !P->opU1 || !P->opU2 || !P->liftT) return fail("fused operators not packed");
     if (Qin == Qout) return fail("fused stage needs distinct Q_in / Q_out buffers");

@@ -244,15 +244,16 @@ def tmma_frag_image(B, K, Nn):
     return np.stack([hi[kk, nn], hi[kk + 4, nn], lo[kk, nn], lo[kk + 4, nn]], axis=-1)
 
 
-def tmma_operator_images(ref, ru, cfg):
+def tmma_operator_images(ref, ru, cfg, strong_weak=True):
     """All reference operators of the split-TF32 mma.sync stage (CfgT offsets),
-    in the order of dmma_operator_images (strong-weak form)."""
+    in the order of dmma_operator_images (no Vq / DTW images for the strong
+    form)."""
     QC, NCH, NPP, NFPK, NFQP = cfg["qc"], cfg["nch"], cfg["npp"], cfg["qcs"], cfg["njs"]
     NCHU = -(-ru.Nq // QC)
     nf, nfq = ref.n_faces, ref.nfq
     DTW = [ref.Mhat_inv @ D.T @ np.diag(ref.wq) for D in ref.Dq]
-    va = list(ref.Dq) + [ref.Vq]
-    vb = DTW + [-ref.Pq]
+    va = list(ref.Dq) + ([ref.Vq] if strong_weak else [])
+    vb = (DTW if strong_weak else []) + [-ref.Pq]
 
     def cols(M, c0, n):
         out = np.zeros((M.shape[0], n))
@@ -485,9 +486,9 @@ class DeviceProblem:
             self.struct.fused_kind = 3
             return kb
         if cfg["kind"] == 4:                    # split-TF32 mma.sync kernel: fragment-order hi / lo images
-            if self.Kpad % kb or not self.sw:
+            if self.Kpad % kb:
                 return None
-            self.ops["tmma"] = self._t(tmma_operator_images(ref, ru, cfg), torch.float32)
+            self.ops["tmma"] = self._t(tmma_operator_images(ref, ru, cfg, self.sw), torch.float32)
             for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
                 setattr(self.struct, name, self.ops["tmma"].data_ptr())
             self.fused_kind = 4

@@ -1,7 +1,8 @@
 """Parity at the BASELINE step counts (north_star: relative L2 of (p, u)
 after the stated number of steps <= 1e-11 in fp64 and <= 1e-5 in fp32),
-the default kernels (tcgen05 stage for fp32 N = 2..4, CUDA-core fused stage
-otherwise) against the fp64 oracle (oracle/wadg_oracle.py) on meshes of
+the default kernels (fp32: tcgen05 stage at N = 2..4, split-TF32 mma.sync
+stage at N = 5..7, CUDA cores at N = 1; fp64: DMMA stage at N = 2..7, CUDA
+cores at N = 1) against the fp64 oracle (oracle/wadg_oracle.py) on meshes of
 several 128-element tiles, so cross-tile neighbour gathers are checked
 against the oracle and not against the product.
 
@@ -10,6 +11,8 @@ against the oracle and not against the product.
 * config-5 physics: N = 5, c^2 = 1, Gaussian pulse, 100 steps, 6^3 x 6 tets;
 * config-3 physics: N = 1..7, Gaussian pulse, 50 steps, 4^3 x 6 tets (3
   tiles), fp32 and fp64;
+* the strong form (the reference default) with the heterogeneous medium at
+  N = 2..4, 50 steps, fp32 and fp64 (fused stages with the sufficiency rules);
 * the full config-4 mesh (K = 1,572,864): one LSRK stage (a != 0) of the
   tcgen05 kernel checked element by element against the oracle on a sample
   of tets, each with its face neighbours (a stage is local to that patch).
@@ -52,12 +55,12 @@ def rel(got, want):
 
 
 @functools.lru_cache(maxsize=None)
-def oracle_run(n, N, het, steps):
+def oracle_run(n, N, het, steps, strong=False):
     """(mesh, initial oracle state, final oracle state, dt); cached so the
     fp32 and fp64 cases share one oracle trajectory."""
     mesh = meshgen.warped_cube_tet_mesh(n, N)
     c2 = c2_het if het else 1.0
-    od = O.OracleDiscretization(mesh, N, True, c2=c2)
+    od = O.OracleDiscretization(mesh, N, not strong, c2=c2)
     st0 = O.project_initial_condition(mesh, N, gaussian)
     dt = 0.5 * (2.0 / n) / (N + 1) ** 2
     st = st0
@@ -66,8 +69,8 @@ def oracle_run(n, N, het, steps):
     return mesh, st0, st, dt
 
 
-def device_run(mesh, N, het, dtype, st0, dt, steps):
-    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype=dtype)
+def device_run(mesh, N, het, dtype, st0, dt, steps, strong=False):
+    cfg = SolverConfig(N=N, formulation=Formulation.Strong if strong else Formulation.StrongWeak, dtype=dtype)
     medium = solver.MediumField(c2_het if het else 1.0)
     disc = solver.Discretization(mesh, cfg, medium)
     Q = disc.to_device(FieldState.from_fields(st0.fields()))
@@ -78,9 +81,9 @@ def device_run(mesh, N, het, dtype, st0, dt, steps):
     return disc, [np.asarray(a) for a in out.fields()]
 
 
-def _check(name, n, N, het, dtype, steps):
-    mesh, st0, want, dt = oracle_run(n, N, het, steps)
-    disc, got = device_run(mesh, N, het, dtype, st0, dt, steps)
+def _check(name, n, N, het, dtype, steps, strong=False):
+    mesh, st0, want, dt = oracle_run(n, N, het, steps, strong)
+    disc, got = device_run(mesh, N, het, dtype, st0, dt, steps, strong)
     err = rel(got, want.fields())
     change = rel(st0.fields(), want.fields())
     record_parity(f"{name} K={mesh.K} N={N} {dtype} {steps} steps kernel={disc.dev.fused_kind}", err, TOL[dtype])
@@ -107,6 +110,15 @@ def test_config5_physics_100_steps(dtype):
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 6, 7])
 def test_config3_physics_50_steps(N, dtype):
     _check("config-3 physics", 4, N, False, dtype, 50)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("N", [2, 3, 4])
+def test_strong_form_50_steps(N, dtype):
+    """The reference's default formulation through its fused stages (fp32
+    split-TF32 mma.sync, fp64 DMMA), heterogeneous medium."""
+    disc = _check("strong form, config-3 physics + het c2", 4, N, True, dtype, 50, strong=True)
+    assert disc.dev.fused_kind == (4 if dtype == "float32" else 3)
 
 
 def test_projection_matches_oracle():

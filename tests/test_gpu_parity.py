@@ -424,6 +424,37 @@ def test_fused_strong_form_stage_fp64(N, rng):
     assert rel(got.fields(), want.fields()) < 1e-11
 
 
+@pytest.mark.parametrize("N", [2, 3, 4, 5])
+def test_fused_strong_form_stage_fp32(N, rng):
+    """The strong form in fp32 as one fused split-TF32 mma.sync stage (kind 4):
+    against the fp32 three-kernel strong stage and the fp64 oracle,
+    heterogeneous medium, 2 steps."""
+    c2 = lambda x, y, z: 1 + 0.5 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y) * np.sin(2 * np.pi * z)
+    mesh = meshgen.warped_cube_tet_mesh(3, N)
+    cfg = SolverConfig(N=N, formulation=Formulation.Strong, flux=FluxParams(0.9, 1.2), dtype="float32")
+    disc = solver.Discretization(mesh, cfg, solver.MediumField(c2))
+    assert disc.dev.fused is not None and disc.dev.fused_kind == 4
+    fl = _state3(mesh.K, disc.ref.Np, rng)
+    st = FieldState.from_fields(fl)
+    Qf = disc.to_device(st)
+    Qs = Qf.clone()
+    sf, ss = solver.DeviceStepper(disc, fused=True), solver.DeviceStepper(disc, fused=False)
+    dt = 2e-3
+    for _ in range(2):
+        Qf = sf.step(Qf, dt)
+        Qs = ss.step(Qs, dt)
+    a = disc.from_device(Qf, st, 0.0).fields()
+    b = disc.from_device(Qs, st, 0.0).fields()
+    assert rel(a, b) < 2e-6
+    od = O.OracleDiscretization(mesh, N, False, 0.9, 1.2, c2=c2)
+    ost = O.State(fl[0], fl[1:])
+    for _ in range(2):
+        ost = O.lsrk_step(ost, dt, lambda y: O.rhs_full(y, od))
+    err = rel(a, ost.fields())
+    record_parity(f"strong form fused fp32 (tmma) N={N} 2 steps", err, 1e-5)
+    assert err < 1e-5
+
+
 @pytest.mark.parametrize("dtype", ["float64", "float32"])
 @pytest.mark.parametrize("N", [2, 3, 4])
 def test_single_curved_tet_fused_stage(N, dtype, rng):
