@@ -169,6 +169,9 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
         fused::mbar_wait(&bar[k], ph);
         ph ^= 1u;
     };
+    // chunk 0's volume operators land while the fields are staged
+    tma(0, sVA, ops + C::O_VA, C::IMG_VA);
+    tma(1, sVB, ops + C::O_VB, C::IMG_VB);
     // ---- fields -> sQ[c][j][e] (rows NP..NPP-1 zero) ------------------------
     for (int r = tid; r < FLD * NPP * (KB / 2); r += C::NTH) {
         const int e2 = (r % (KB / 2)) * 2, row = r / (KB / 2);
@@ -192,9 +195,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
 
     // ======================= volume =======================================
     // operator images double as a pipeline: VA(ch+1) loads during phase B(ch),
-    // VB(ch+1) during phase A(ch+1)
-    tma(0, sVA, ops + C::O_VA, C::IMG_VA);
-    tma(1, sVB, ops + C::O_VB, C::IMG_VB);
+    // VB(ch+1) during phase A(ch+1); chunk 0's were issued before the fields
     for (int ch = 0; ch < C::NCH; ++ch) {
         twait(0);
         if constexpr (!SW) {

@@ -240,6 +240,9 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         fused::mbar_wait(&bar[k], phs);
         phs ^= 1u;
     };
+    // chunk 0's volume operators land while the fields are staged
+    tma(0, sVA, ops + C::O_VA, C::IMG_VA);
+    tma(1, sVB, ops + C::O_VB, C::IMG_VB);
     // ---- fields -> sQ[c][j][pos(e)] (rows NP..NPP-1 zero): 16-byte loads of 4
     // elements, stored to their interleaved positions
     for (int r = tid; r < FLD * NPP * (KB / 4); r += C::NTH) {
@@ -272,8 +275,7 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     };
 
     // ======================= volume =======================================
-    tma(0, sVA, ops + C::O_VA, C::IMG_VA);
-    tma(1, sVB, ops + C::O_VB, C::IMG_VB);
+    // (chunk 0's operator images were issued before the fields)
     for (int ch = 0; ch < C::NCH; ++ch) {
         twait(0);
         // geometric factors of this thread's two (point, element) pairs of the
