@@ -37,6 +37,7 @@ template <int N, bool SW = true>
 struct CfgD {
     static constexpr int NP = fused::np_tet(N);
     static constexpr int NPP = rup(NP, 8);                // nodes, padded to whole 8-wide tiles
+    static constexpr int NKS = rup(NP, 4) / 4;            // k steps of a contraction over nodes (rows past NP are zero)
     static constexpr int NQ = SW ? (N + 1) * (N + 1) * (N + 1) : (2 * N - 1) * (2 * N - 1) * (2 * N - 1);
     static constexpr int NQU = (N + 1) * (N + 1) * (N + 1);
     static constexpr int NFP = fused::nfp_tri(N);
@@ -220,7 +221,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
 #pragma unroll
                     for (int c = 0; c < FLD; ++c) d[t][a][c][0] = d[t][a][c][1] = 0.0;
 #pragma unroll 2
-            for (int ks = 0; ks < NPP / 4; ++ks) {
+            for (int ks = 0; ks < C::NKS; ++ks) {
                 double x[FLD];
 #pragma unroll
                 for (int c = 0; c < FLD; ++c) x[c] = afrag<KBS>(sQ + c * NPP * KBS, mt, ks, lane);
@@ -280,7 +281,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
 #pragma unroll
                 for (int m = 0; m < 6; ++m) d[t][m][0] = d[t][m][1] = 0.0;
 #pragma unroll 2
-            for (int ks = 0; ks < NPP / 4; ++ks) {
+            for (int ks = 0; ks < C::NKS; ++ks) {
                 double x[4];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) x[c] = afrag<KBS>(sQ + c * NPP * KBS, mt, ks, lane);
@@ -548,7 +549,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
 #pragma unroll
                 for (int c = 0; c < FLD; ++c) z[t][c][0] = z[t][c][1] = 0.0;
 #pragma unroll 2
-            for (int ks = 0; ks < NPP / 4; ++ks) {
+            for (int ks = 0; ks < C::NKS; ++ks) {
                 double x[FLD];
 #pragma unroll
                 for (int c = 0; c < FLD; ++c) x[c] = afrag<KBS>(sR + c * NPP * KBS, mt, ks, lane);

@@ -26,6 +26,8 @@ elif case == "split_c4":
 elif case.startswith("c3_f64_N"):           # config-3 mesh, fp64 strong-weak at order N
     Nc = int(case[len("c3_f64_N"):])
     mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(32, Nc), SolverConfig(N=Nc, formulation=Formulation.StrongWeak), 1.0, True
+elif case == "strong_f32_N4":
+    mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(32, 4), SolverConfig(N=4, formulation=Formulation.Strong, dtype="float32"), 1.0, True
 elif case == "strong_f64_N4":
     mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(32, 4), SolverConfig(N=4, formulation=Formulation.Strong), 1.0, True
 else:
