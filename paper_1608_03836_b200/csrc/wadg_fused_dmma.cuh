@@ -44,6 +44,7 @@ struct CfgD {
     static constexpr int NFPK = rup(NFP, 4);
     static constexpr int NFQ = SW ? (N + 1) * (N + 1) : 4 * N * N;
     static constexpr int NFQP = rup(NFQ, 8);
+    static constexpr int NFKS = rup(NFQ, 4) / 4;           // k steps of the lift (face points past NFQ are zero)
     static constexpr int NF = 4, FLD = 4;
     // elements per CTA: 24 (three element tiles, six warps) for strong-weak N = 4,
     // so that two CTAs fit per SM (+1.5 %); 32 at N <= 5 otherwise; 16 at N = 6, 7
@@ -490,7 +491,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
         twait(0);
         // lift: R_c += (-Pf_f) g_c
 #pragma unroll 2
-        for (int ks = 0; ks < NFQP / 4; ++ks) {
+        for (int ks = 0; ks < C::NFKS; ++ks) {
             double gv[FLD];
 #pragma unroll
             for (int c = 0; c < FLD; ++c) gv[c] = afrag<KBS>(sG + c * NFQP * KBS, mt, ks, lane);
