@@ -245,10 +245,25 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         P.prof[(size_t)blockIdx.x * 32 + 30] = smid;
     }
 
-    if (tid == 0) {
+    // the MMA warp's lane 0 initialises the barriers and at once issues the first
+    // volume operator tiles (static data, a region not used before the volume):
+    // their copies overlap the prologue and the field staging below
+    if (mma_warp && lane == 0) {
         for (int i = 0; i < 8; ++i) fused::mbar_init(&bar[i], 1);
         fused::mbar_init(&bar_v2[0], 1);
         fused::mbar_init(&bar_v2[1], 1);
+        fused::fence_proxy_async();
+        const float *ops0 = P.opVA;
+        float *sOp0 = sQ + 2 * C::SQF;
+        auto ld0 = [&](int slot, float *dst, const float *src, uint32_t bytes) {
+            fused::mbar_expect_tx(&bar[1 + slot], bytes);
+            fused::bulk_g2s(dst, src, bytes, &bar[1 + slot]);
+        };
+        ld0(C::SL_DA, sOp0, ops0 + C::O_DA, C::OPDA * 4);
+        ld0(C::SL_VQ, sOp0 + 2 * C::OPDA, ops0 + C::O_VQ, C::OPVQ * 4);
+        ld0(C::SL_PQ, sOp0 + 2 * C::OPDA + C::OPVQ, ops0 + C::O_PQ, C::OPPQ * 4);
+        ld0(C::SL_DTW, sOp0 + 2 * C::OPDA + C::OPVQ + C::OPPQ, ops0 + C::O_DTW, C::OPDTW * 4);
+        if (NCH > 1) ld0(C::SL_DA + 1, sOp0 + C::OPDA, ops0 + C::O_DA + C::OPDA, C::OPDA * 4);
     }
     if (warp == 0) tmem_alloc<512>(tslot);
     for (int r = tid; r < NF * 6 * NFP; r += C::NTH) sExt[r] = __ldg(P.ext_node + r);
@@ -431,11 +446,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
                                  (ch > 0 || ks > 0 || a > 0 || t == 1) ? 1u : 0u);
             }
         };
-        op_load(C::SL_DA, sDa, ops + C::O_DA, C::OPDA * 4);
-        op_load(C::SL_VQ, sVq, ops + C::O_VQ, C::OPVQ * 4);
-        op_load(C::SL_PQ, sPq, ops + C::O_PQ, C::OPPQ * 4);
-        op_load(C::SL_DTW, sDTW, ops + C::O_DTW, C::OPDTW * 4);
-        if (NCH > 1) op_load(C::SL_DA + 1, sDa + C::OPDA, ops + C::O_DA + C::OPDA, C::OPDA * 4);
+        // (chunk 0 / 1's operator tiles were issued at kernel entry)
         __syncwarp();
         op_wait(C::SL_DA);
         issue_v1p(0);
