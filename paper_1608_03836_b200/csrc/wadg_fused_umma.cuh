@@ -47,7 +47,7 @@ namespace uk {
 #endif
 #define UMMA_MARK(slot, cond)                                                                  \
     do {                                                                                       \
-        if (P.prof && (cond)) P.prof[(size_t)blockIdx.x * 32 + (slot)] = clock64();            \
+        if (P.prof && (cond)) P.prof[(blk - (size_t)block0) * 32 + (slot)] = clock64();        \
     } while (0)
 
 using fused::cdiv;
@@ -109,6 +109,9 @@ struct CfgU {
     // op-tile barrier slots (bar[1 + slot]) in the volume phase; the surface and update
     // phases use slots 0 and 1
     static constexpr int SL_DA = 0, SL_VQ = 2, SL_PQ = 4, SL_DTW = 5;
+    // persistent CTAs looping over tiles (N = 2, 3: +3.8 / +2.3 %); at N = 4 the
+    // loop-carried state costs spills at the 96-register cap, so one tile per CTA
+    static constexpr bool PERSIST = N <= 3;
 };
 
 // Split-TF32 K loops, issued by one whole warp (one elected lane issues):
@@ -199,7 +202,8 @@ __device__ __forceinline__ void wait_k(uint64_t *bar, uint32_t k, int site = -1)
 template <int N, int LAY>
 __global__ void __launch_bounds__(CfgU<N>::NTH, 1)
 k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *__restrict__ Qout,
-             float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt, int block0) {
+             float *__restrict__ res, float tau_p, float tau_u, float a_rk, float b_rk, float dt, int block0,
+             int block_end) {
     using C = CfgU<N>;
     using namespace umma;
     constexpr int NP = C::NP, NPK = C::NPK, NPN = C::NPN, QC = C::QC, QU = C::QU;
@@ -235,15 +239,8 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     const int qd = warp & 3, sub = (warp >> 2) & 3;                // lane quarter, sub-group 0..3
     const int e = 32 * qd + lane;                                  // element row = TMEM lane
     const size_t S = P.Kpad;
-    const size_t blk = (size_t)(block0 + blockIdx.x);
-    const size_t kblk = blk * ME;
-    UMMA_MARK0(0);
+    // persistent CTAs: tiles block0 + blockIdx.x, + gridDim.x, ... < block_end
     asm volatile("griddepcontrol.launch_dependents;");   // the next stage may start its prologue
-    if (P.prof && threadIdx.x == 0) {   // debug: SM id (slot 30), for per-SM gap analysis
-        uint32_t smid;
-        asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        P.prof[(size_t)blockIdx.x * 32 + 30] = smid;
-    }
 
     // the MMA warp's lane 0 initialises the barriers and at once issues the first
     // volume operator tiles (static data, a region not used before the volume):
@@ -274,6 +271,26 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     // written by that kernel are read (and Qout / res written) only after this
     // wait.  Without the launch attribute the wait is a no-op.
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // barrier-completion counts carried from tile to tile: the MMA warp's operator
+    // slot phases, V2p / V2u (and update U2) completions and group-B completions
+    // before the current tile; the epilogue's consumed group-A / group-B completions
+    // (one set of registers: the MMA warp's {slot phases, V2p, V2u, group B} and the
+    // epilogue warps' {group A, group B})
+    uint32_t cnt[4] = {0u, 0u, 0u, 0u};
+    // group-B (bar[7]) commits per tile: volume NCH + 1, surface NSTEP, update NCHU + 1
+    constexpr uint32_t TILE_B = (uint32_t)(NCH + 1 + NSTEP + NCHU + 1);
+    fence_before();
+    __syncthreads();                      // barrier init, TMEM address and index tables visible
+    fence_after();
+    const uint32_t tm = *tslot;
+    for (size_t blk = (size_t)block0 + blockIdx.x;;) {
+    const size_t kblk = blk * ME;
+    UMMA_MARK0(0);
+    if (P.prof && threadIdx.x == 0) {   // debug: SM id (slot 30), for per-SM gap analysis
+        uint32_t smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        P.prof[(blk - (size_t)block0) * 32 + 30] = smid;
+    }
     // neighbour tables of all faces (consumed in the surface phase)
     int nbr[NF], ncode[NF];
     if (!mma_warp) {
@@ -327,7 +344,6 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     fence_before();
     __syncthreads();
     fence_after();
-    const uint32_t tm = *tslot;
     const uint32_t tl = tm + ((uint32_t)(32 * qd) << 16);         // this warp's lane quarter
     const uint32_t aQ = su32(sQ), aQlo = su32(sQlo);
     UMMA_MARK0(1);
@@ -372,7 +388,8 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 
     if (mma_warp) {
         // =================== MMA warp =====================================
-        uint32_t ph_op = 0, nv2p = 0, nv2u = 0, nB = 0;
+        uint32_t &ph_op = cnt[0], &nv2p = cnt[1], &nv2u = cnt[2];
+        uint32_t nB = cnt[3];
         auto op_load = [&](int slot, float *dst, const float *src, uint32_t bytes) {
             if (lane == 0) {
                 fused::mbar_expect_tx(&bar[1 + slot], bytes);
@@ -497,7 +514,7 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             if (!(ch & 1) && ch + 2 < NCH)   // pair ch/2 consumed (V1u issued before V2u(ch)): next pair
                 op_load(C::SL_VQ, sVq, ops + C::O_VQ + (size_t)(ch / 2 + 1) * C::OPVQ, C::OPVQ * 4);
         }
-        nB = NCH + 1;                        // group-B completions so far (V1u(0), per-chunk u commits)
+        nB = cnt[3] + NCH + 1;               // group-B completions so far (V1u(0), per-chunk u commits)
         // ---- surface: per (face, half) step s: traces(s) (group A) are issued as
         // soon as the epilogue has read traces(s-1) out of TMEM, the lift of s-1
         // (group B) once its flux is written; the flux has its own columns ----
@@ -633,15 +650,25 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             commit_w(&bar_v2[0]);            // last reader of the chunk-u tiles
             if (more) issue_u1(1, u + 1);
             commit_w(&bar[7]);
-            if (u + 2 < NCHU) {
-                wait_k(&bar_v2[0], ++nv2p);
+            wait_k(&bar_v2[0], ++nv2p);      // every completion is consumed (a parity wait needs that)
+            if (u + 2 < NCHU)
                 op_load2(u & 1, sU(u & 1), ops + C::O_U1 + (size_t)(u + 2) * C::OPU1, C::OPU1 * 4,
                          sU(u & 1) + C::OPU1, ops + C::O_U2 + (size_t)(u + 2) * C::OPU2, C::OPU2 * 4);
-            }
         }
+        cnt[3] += TILE_B;
+        // every MMA of this tile is done (the last U2 commit): the next tile's first
+        // volume operator tiles load while the epilogue warps write this tile out
+        if (C::PERSIST && blk + gridDim.x < (size_t)block_end) {
+            op_load(C::SL_DA, sDa, ops + C::O_DA, C::OPDA * 4);
+            op_load(C::SL_VQ, sVq, ops + C::O_VQ, C::OPVQ * 4);
+            op_load(C::SL_PQ, sPq, ops + C::O_PQ, C::OPPQ * 4);
+            op_load(C::SL_DTW, sDTW, ops + C::O_DTW, C::OPDTW * 4);
+            if (NCH > 1) op_load(C::SL_DA + 1, sDa + C::OPDA, ops + C::O_DA + C::OPDA, C::OPDA * 4);
+        }
+        __syncwarp();
     } else {
         // =================== epilogue warps ===============================
-        uint32_t nA = 0, nB = 0;             // consumed completions of MMA groups A and B
+        uint32_t &nA = cnt[0], &nB = cnt[1]; // consumed completions of MMA groups A and B
         auto wait_A = [&]() { wait_k(&bar[0], ++nA); fence_after(); };
         auto wait_B = [&]() { wait_k(&bar[7], ++nB); fence_after(); };
         // hand TMEM (and, with smem = true, shared-memory operand) writes to the
@@ -912,10 +939,8 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             // (read by the LSRK write) and the fields, neighbour tables and first
             // geometric-factor chunk of the tile that will most likely start on this SM
             // next (launch order: one resident CTA per SM)
-            uint32_t nsm;
-            asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
-            const size_t nxt = blk + nsm;
-            const bool has_next = nxt < (size_t)(P.Kpad / ME);
+            const size_t nxt = blk + gridDim.x;                  // this CTA's next tile
+            const bool has_next = nxt < (size_t)block_end;
             const int t512 = warp * 32 + lane;                   // 0..511
             auto pf = [](const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); };
             for (int r = t512; r < 4 * NP * 4; r += 512) {     // 4 x 128 B lines per 512 B row
@@ -1045,7 +1070,12 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     }
     fence_before();
     __syncthreads();
+    fence_after();
     UMMA_MARK0(5);
+    if constexpr (!C::PERSIST) break;
+    blk += gridDim.x;
+    if (blk >= (size_t)block_end) break;
+    }   // tiles
     if (warp == 0) tmem_dealloc<512>(tm);
 }
 

@@ -894,8 +894,15 @@ static int launch_umma_lay(const wadg_problem *Pc, const void *Qin, void *Qout, 
     // programmatic dependent launch: consecutive stage kernels on a stream overlap
     // the next one's prologue with this one's tail (the kernel waits on
     // griddepcontrol.wait before touching data the previous kernel wrote)
+    // persistent CTAs (one per SM, the tcgen05 tile's shared memory and TMEM
+    // allow no more): each loops over tiles b0 + blockIdx.x, + gridDim.x, ...
+    static int nsm_dev[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return fail("cudaGetDevice failed");
+    if (!nsm_dev[dev] && cudaDeviceGetAttribute(&nsm_dev[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return fail("cudaDeviceGetAttribute failed");
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(b1 - b0);
+    cfg.gridDim = dim3((C::PERSIST && b1 - b0 > nsm_dev[dev]) ? nsm_dev[dev] : b1 - b0);
     cfg.blockDim = dim3(C::NTH);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
@@ -906,7 +913,7 @@ static int launch_umma_lay(const wadg_problem *Pc, const void *Qin, void *Qout, 
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, uk::k_stage_umma<N, LAY>, make_fprob<float>(*Pc), (const float *)Qin,
                                        (float *)Qout, (float *)res, (float)tp, (float)tu, (float)a, (float)b,
-                                       (float)dt, b0);
+                                       (float)dt, b0, b1);
     if (e != cudaSuccess) return fail(cudaGetErrorString(e));
     return check_launch("wadg_stage_fused(umma)");
 }

@@ -424,6 +424,32 @@ def test_fused_strong_form_stage_fp64(N, rng):
     assert rel(got.fields(), want.fields()) < 1e-11
 
 
+@pytest.mark.parametrize("N", [2, 3, 4])
+def test_tcgen05_stage_more_tiles_than_sms(N):
+    """More 128-element tiles than SMs (K = 16^3 x 6 = 24,576: 192 tiles), so the
+    persistent tcgen05 CTAs (N = 2, 3) loop over several tiles each: one fused
+    stage against the three-kernel stage, heterogeneous medium."""
+    c2 = lambda x, y, z: 1 + 0.5 * np.sin(2 * np.pi * x) * np.sin(2 * np.pi * y) * np.sin(2 * np.pi * z)
+    mesh = meshgen.warped_cube_tet_mesh(16, N)
+    cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype="float32")
+    disc = solver.Discretization(mesh, cfg, solver.MediumField(c2))
+    assert disc.dev.fused_kind == 2 and disc.dev.Kpad // 128 > torch.cuda.get_device_properties(0).multi_processor_count
+    g = torch.Generator(device="cuda").manual_seed(3)
+    Q = torch.randn(disc.dev.empty_fields().shape, generator=g, device="cuda")
+    Q[:, :, mesh.K:] = 0
+    sf, ss = solver.DeviceStepper(disc, fused=True), solver.DeviceStepper(disc, fused=False)
+    res = torch.randn(Q.shape, generator=g, device="cuda")
+    res[:, :, mesh.K:] = 0
+    sf.res.copy_(res)
+    ss.res.copy_(res)
+    a, b, dt = solver.LSRK4A[1], solver.LSRK4B[1], 1e-3
+    Qf, Qs = sf.stage(Q, a, b, dt), ss.stage(Q, a, b, dt)
+    K = mesh.K
+    err = (torch.linalg.norm((Qf - Qs)[:, :, :K]) / torch.linalg.norm(Qs[:, :, :K])).item()
+    err_r = (torch.linalg.norm((sf.res - ss.res)[:, :, :K]) / torch.linalg.norm(ss.res[:, :, :K])).item()
+    assert err < 2e-6 and err_r < 2e-6, (err, err_r)
+
+
 @pytest.mark.parametrize("N", [2, 3, 4, 5])
 def test_fused_strong_form_stage_fp32(N, rng):
     """The strong form in fp32 as one fused split-TF32 mma.sync stage (kind 4):
