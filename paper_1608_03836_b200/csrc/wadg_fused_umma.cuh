@@ -692,6 +692,18 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         };
         load_G(0);
         for (int ch = 0; ch < NCH; ++ch) {
+            if (N >= 4 && ch == NCH - 1 && nbr[0] >= 0) {
+                // L2 prefetch of face 0's neighbour nodes: the surface gathers them
+                // first, right after the volume, with nothing to overlap the load
+                // (N = 4: +1.1 %; at N = 2, 3 the extra registers cost more)
+                const int code = ncode[0], c = sub;
+#pragma unroll 1
+                for (int i = 0; i < NFP; ++i) {
+                    const float *a = (LAY & 1) ? Qin + ((size_t)c * P.K + nbr[0]) * NP + sExt[code * NFP + i]
+                                               : Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nbr[0];
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                }
+            }
             wait_A();                        // V1p(ch) and V2p(ch-1) done
             {
                 float dp[3][4];
