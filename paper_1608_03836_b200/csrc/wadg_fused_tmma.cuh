@@ -63,6 +63,20 @@ struct CfgT {
     static constexpr int NVA = SW ? 4 : 3;                 // operators of the point GEMM: D_a (, Vq)
     static constexpr int NVB = SW ? 4 : 1;                 // of the projection: (DTW_a,) -Pq
     static constexpr int NWR = SW ? 6 : 12;                // point-value rows of the volume (sW)
+    // point-GEMM products (operator, point tile), in the order the warps of an
+    // element tile take them: strong-weak (m, qt), m = D_r, D_s, D_t (on p), Vq (on
+    // u1, u2, u3); strong (c, a, qt), D_a on field c
+    static constexpr int NPROD = SW ? 6 * QT : 12 * QT;
+    __host__ __device__ static constexpr int prod_qt(int P) { return P % QT; }
+    __host__ __device__ static constexpr int prod_field(int P) { return SW ? (P / QT < 3 ? 0 : P / QT - 2) : P / (3 * QT); }
+    __host__ __device__ static constexpr int prod_op(int P) { return SW ? (P / QT < 3 ? P / QT : 3) : (P / QT) % 3; }
+    __host__ __device__ static constexpr int prod_row(int P) { return SW ? P / QT : 3 * (P / (3 * QT)) + (P / QT) % 3; }
+    // number of products from P on (at most n) that share P's field
+    __host__ __device__ static constexpr int prod_run(int P, int n) {
+        int k = 0;
+        while (k < n && prod_field(P + k) == prod_field(P)) ++k;
+        return k;
+    }
     static constexpr int TT = cdiv(FT, WPM);               // face-point tiles per warp
     static constexpr int ZU = cdiv(2 * QT, WPM);           // (point tile, field pair) units per warp
     static constexpr int FR = 128;                         // floats per fragment image (32 lanes x 4)
@@ -179,6 +193,11 @@ __device__ __forceinline__ uint4 bfrag(const float *img, int idx, int lane) {
     return *reinterpret_cast<const uint4 *>(img + (size_t)(idx * 32 + lane) * 4);
 }
 
+template <int V>
+struct IC {
+    static constexpr int value = V;
+};
+
 // shared-memory position of element el (0..KB-1) of the CTA
 __device__ __forceinline__ int epos(int el) { return (el & ~15) + 2 * (el & 7) + ((el >> 3) & 1); }
 
@@ -192,6 +211,7 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     constexpr int QC = C::QC, QT = C::QT, JT = C::JT, FT = C::FT, RT = C::RT;
 
     static_assert(C::NTH == 256 && QC == 16 && KB == 32, "the volume epilogue maps 256 threads to 16 x 32 pairs");
+    static_assert(C::WPM == 4 && C::NPROD % 4 == 0, "the point GEMMs are split between four warps per element tile");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
     float *sQ = reinterpret_cast<float *>(smem_raw + 16);
@@ -287,9 +307,67 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 #pragma unroll
             for (int r = 0; r < 9; ++r) G[h][r] = q < NQ ? __ldg(P.geo + (size_t)(r * NQ + q) * S + kblk + lane) : 0.f;
         }
-        // A, strong-weak: dp_a = D_a p (group 0) -> sW rows a, U_i = Vq u_i (group 1) ->
-        // sW rows 3 + i; strong: du_a,c = D_a Q_c (unit field c) -> sW rows 3 c + a; at
-        // point tile qt, the independent products of a k step issued term by term
+        // A (strong-weak): the chunk's point GEMMs, as products (operator, point tile):
+        // D_r p, D_s p, D_t p, Vq u1, Vq u2, Vq u3 (-> sW rows 0..5) on both point
+        // tiles.  The four warps of an element tile take consecutive runs of three, so
+        // that each splits at most two field fragments per k step (p | p | u1, u2 |
+        // u2, u3; one field per product group before: +1.7 % at N = 5); the products
+        // of a k step are issued term by term.
+        {
+            auto phase_a = [&](auto wtag) {
+                constexpr int W = decltype(wtag)::value;
+                constexpr int PPW = C::NPROD / WPM;
+                constexpr int F0 = C::prod_field(PPW * W), F1 = C::prod_field(PPW * W + PPW - 1);
+                constexpr int N0 = C::prod_run(PPW * W, PPW);        // leading products on field F0
+                float d[PPW][4];
+#pragma unroll
+                for (int k = 0; k < PPW; ++k)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) d[k][i] = 0.f;
+#pragma unroll 1
+                for (int ks = 0; ks < NPP / 8; ++ks) {
+                    AF x0, x1;
+                    afrag<KBS>(x0, sQ + F0 * NPP * KBS, mt, ks, lane);
+                    if constexpr (N0 < PPW) afrag<KBS>(x1, sQ + F1 * NPP * KBS, mt, ks, lane);
+                    uint4 b[PPW];
+                    float f[PPW][4];
+#pragma unroll
+                    for (int k = 0; k < PPW; ++k)
+                        b[k] = bfrag(sVA, (C::prod_op(PPW * W + k) * (NPP / 8) + ks) * QT + C::prod_qt(PPW * W + k), lane);
+#pragma unroll
+                    for (int k = 0; k < N0; ++k) term1(f[k], x0, b[k]);
+#pragma unroll
+                    for (int k = N0; k < PPW; ++k) term1(f[k], x1, b[k]);
+#pragma unroll
+                    for (int k = 0; k < N0; ++k) term2(f[k], x0, b[k]);
+#pragma unroll
+                    for (int k = N0; k < PPW; ++k) term2(f[k], x1, b[k]);
+#pragma unroll
+                    for (int k = 0; k < N0; ++k) term3(f[k], x0, b[k]);
+#pragma unroll
+                    for (int k = N0; k < PPW; ++k) term3(f[k], x1, b[k]);
+#pragma unroll
+                    for (int k = 0; k < PPW; ++k) add4(d[k], f[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < PPW; ++k)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        st2(sW, C::prod_row(PPW * W + k) * QC + 8 * C::prod_qt(PPW * W + k) + 2 * tl + h, d[k][h],
+                            d[k][2 + h]);
+            };
+            if constexpr (SW) {
+                switch (w0) {
+                    case 0: phase_a(IC<0>{}); break;
+                    case 1: phase_a(IC<1>{}); break;
+                    case 2: phase_a(IC<2>{}); break;
+                    default: phase_a(IC<3>{}); break;
+                }
+            }
+        }
+        if constexpr (!SW) {
+        // strong form: units (point tile, field c), du_a,c = D_a Q_c -> sW rows 3 c + a
+        // (one field per unit measured faster than one field per warp here)
 #pragma unroll
         for (int t = 0; t < C::AU; ++t) {
             const int u = w0 + WPM * t;
@@ -341,6 +419,7 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             for (int m = 0; m < 3; ++m)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) st2(sW, (3 * grp + m) * QC + 8 * qt + 2 * tl + h, d[m][h], d[m][2 + h]);
+        }
         }
         __syncthreads();
         // epilogue, one thread per (point, element) pair, in place: gp_i = sum_a G_ai dp_a
