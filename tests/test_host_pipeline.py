@@ -124,6 +124,28 @@ def test_host_pipeline_bitwise_device_stepper(dtype, N, direct):
 
 
 @pytest.mark.gpu
+def test_host_pipeline_chunks_of_more_tiles_than_sms():
+    """Chunks larger than the SM count: the persistent tcgen05 CTAs (N = 3) loop
+    over several tiles of a block range [b0, b1) with b0 > 0; bitwise equal to
+    the device stepper."""
+    mesh = meshgen.warped_cube_tet_mesh(16, 3)
+    disc = solver.Discretization(mesh, SolverConfig(N=3, formulation=Formulation.StrongWeak, dtype="float32"))
+    d = disc.dev
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    nblk = d.Kpad // d.fused
+    assert d.fused_kind == 2 and nblk > sms + 8
+    g = torch.Generator().manual_seed(5)
+    host = [torch.randn((mesh.K, disc.ref.Np), generator=g).pin_memory() for _ in range(4)]
+    st = FieldState.from_fields(host)
+    pipe = solver.HostPipeline(disc, chunk_blocks=[8, sms + 8, nblk - sms - 16])
+    Q = disc.to_device(st)
+    a = pipe.step(st, 1e-3)
+    Q = solver.DeviceStepper(disc, fused=True).step(Q, 1e-3)
+    for x, y in zip(a.fields(), disc.from_device(Q, st, 0.0).fields()):
+        assert torch.equal(x, y)
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("layout", [1, 2])
 def test_stage_fused_rows_matches_field_layout(layout):
     """wadg_stage_fused_rows with Q_in (1) or Q_out (2) in the FieldState row
