@@ -1028,30 +1028,39 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
 // host row layout (fld, K, Np) <-> device field layout (fld, Np, Kpad) for
 // elements [k0, k1): 32 x 32 tiles through shared memory, both sides coalesced
 namespace wadg {
+// one CTA per 32 elements of one field: the 32 x Np block is one contiguous run
+// in the row layout and Np runs of 32 elements in the field layout; both sides
+// are read / written linearly (no partly idle node tiles when Np % 32 != 0)
 template <typename T, bool TO_FIELDS>
 __global__ void __launch_bounds__(256) k_rows_fields(const T *__restrict__ src, T *__restrict__ dst, int K, int Kpad,
                                                       int Np, int k0, int k1) {
-    __shared__ T tile[32][33];
-    const int f = blockIdx.z, kb = k0 + 32 * blockIdx.x, jb = 32 * blockIdx.y;
+    extern __shared__ __align__(16) unsigned char tile_raw[];
+    T *tile = reinterpret_cast<T *>(tile_raw);          // [32][Np + 1]
+    const int f = blockIdx.y, kb = k0 + 32 * blockIdx.x;
+    const int ne = min(32, k1 - kb);
     const size_t rows = (size_t)f * K * Np, flds = (size_t)f * Np * Kpad;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    for (int r = ty; r < 32; r += 8) {
-        if (TO_FIELDS) {                 // read row k = kb + r, node jb + tx
-            const int k = kb + r, j = jb + tx;
-            if (k < k1 && j < Np) tile[r][tx] = src[rows + (size_t)k * Np + j];
-        } else {                         // read field node j = jb + r, element kb + tx
-            const int j = jb + r, k = kb + tx;
-            if (k < k1 && j < Np) tile[r][tx] = src[flds + (size_t)j * Kpad + k];
+    const int NS = Np + 1;
+    if (TO_FIELDS) {
+        const T *s0 = src + rows + (size_t)kb * Np;
+        for (int t = threadIdx.x; t < ne * Np; t += blockDim.x) {
+            const int el = t / Np, j = t - el * Np;
+            tile[el * NS + j] = s0[t];
         }
-    }
-    __syncthreads();
-    for (int r = ty; r < 32; r += 8) {
-        if (TO_FIELDS) {                 // write node j = jb + r, element kb + tx
-            const int j = jb + r, k = kb + tx;
-            if (k < k1 && j < Np) dst[flds + (size_t)j * Kpad + k] = tile[tx][r];
-        } else {                         // write row k = kb + r, node jb + tx
-            const int k = kb + r, j = jb + tx;
-            if (k < k1 && j < Np) dst[rows + (size_t)k * Np + j] = tile[tx][r];
+        __syncthreads();
+        for (int t = threadIdx.x; t < Np * 32; t += blockDim.x) {
+            const int j = t >> 5, el = t & 31;
+            if (el < ne) dst[flds + (size_t)j * Kpad + kb + el] = tile[el * NS + j];
+        }
+    } else {
+        for (int t = threadIdx.x; t < Np * 32; t += blockDim.x) {
+            const int j = t >> 5, el = t & 31;
+            if (el < ne) tile[el * NS + j] = src[flds + (size_t)j * Kpad + kb + el];
+        }
+        __syncthreads();
+        T *d0 = dst + rows + (size_t)kb * Np;
+        for (int t = threadIdx.x; t < ne * Np; t += blockDim.x) {
+            const int el = t / Np, j = t - el * Np;
+            d0[t] = tile[el * NS + j];
         }
     }
 }
@@ -1062,13 +1071,14 @@ static int rows_fields(const wadg_problem *P, const void *src, void *dst, int k0
     if (validate(P)) return 1;
     if (k0 < 0 || k1 > P->K || k0 > k1) return fail("element range outside [0, K]");
     if (k0 == k1) return 0;
-    const dim3 grid((k1 - k0 + 31) / 32, (P->Np + 31) / 32, P->dim + 1);
+    const dim3 grid((k1 - k0 + 31) / 32, P->dim + 1);
+    const size_t smem = (size_t)32 * (P->Np + 1) * (P->dtype == WADG_F64 ? 8 : 4);
     if (P->dtype == WADG_F64)
-        wadg::k_rows_fields<double, TO_FIELDS><<<grid, 256, 0, st>>>((const double *)src, (double *)dst, P->K,
-                                                                     P->Kpad, P->Np, k0, k1);
+        wadg::k_rows_fields<double, TO_FIELDS><<<grid, 256, smem, st>>>((const double *)src, (double *)dst, P->K,
+                                                                        P->Kpad, P->Np, k0, k1);
     else
-        wadg::k_rows_fields<float, TO_FIELDS><<<grid, 256, 0, st>>>((const float *)src, (float *)dst, P->K,
-                                                                    P->Kpad, P->Np, k0, k1);
+        wadg::k_rows_fields<float, TO_FIELDS><<<grid, 256, smem, st>>>((const float *)src, (float *)dst, P->K,
+                                                                       P->Kpad, P->Np, k0, k1);
     return check_launch(TO_FIELDS ? "wadg_rows_to_fields" : "wadg_fields_to_rows");
 }
 
