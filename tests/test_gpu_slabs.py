@@ -62,10 +62,12 @@ class LoopbackDist:
 
 
 @pytest.mark.parametrize("local", [False, True])
-@pytest.mark.parametrize("dtype", ["float32", "float64"])
+@pytest.mark.parametrize("dtype,N", [("float32", 3), ("float64", 3), ("float32", 5)])
 @pytest.mark.parametrize("fused", [True, False])
-def test_slab_exchange_loopback_is_bitwise_single_domain(dtype, fused, local, rng):
-    N, world, nz = 3, 3, 6
+def test_slab_exchange_loopback_is_bitwise_single_domain(dtype, N, fused, local, rng):
+    """N = 3: the tcgen05 (fp32) and DMMA (fp64) stages; N = 5 fp32: the
+    split-TF32 mma.sync stage of config 5 (the weak-scaling configuration)."""
+    world, nz = 3, 6
     mesh = meshgen.warped_cube_tet_mesh(4, N, nz=nz, z_range=(-1.0, 2.0))
     cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype=dtype)
     c2 = lambda x, y, z: 1.0 + 0.5 * np.sin(np.pi * x) * np.sin(np.pi * y) * np.sin(np.pi * z)
@@ -81,7 +83,8 @@ def test_slab_exchange_loopback_is_bitwise_single_domain(dtype, fused, local, rn
     ranges = parallel.slab_ranges(mesh.K, world, nz)
     assert all(len(s.exchange.halo_runs_f if fused else s.exchange.halo_runs) > 0 for s in slabs)
     if dtype == "float32":
-        assert whole.dev.fused_kind == 2 and all(s.dev.fused_kind == 2 for s in slabs)
+        kind = 2 if N <= 4 else 4
+        assert whole.dev.fused_kind == kind and all(s.dev.fused_kind == kind for s in slabs)
     fl = [rng.standard_normal((mesh.K, whole.ref.Np)) for _ in range(4)]
     Qw = whole.to_device(FieldState.from_fields(fl))
     Qs = [s.to_device(FieldState.from_fields([a[lo:hi] for a in fl])) for s, (lo, hi) in zip(slabs, ranges)]
