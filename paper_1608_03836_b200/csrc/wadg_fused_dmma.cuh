@@ -48,12 +48,14 @@ struct CfgD {
     static constexpr int NF = 4, FLD = 4;
     // elements per CTA: 24 (three element tiles, six warps) for strong-weak N = 4,
     // so that two CTAs fit per SM (+1.5 %); 32 at N <= 5 otherwise; 16 at N = 6, 7
-    static constexpr int KB = (SW && N == 4) ? 24 : (N <= 5 ? 32 : 16);
+    static constexpr int KB = (SW && N == 4) ? 24 : ((N <= 5 && (SW || N <= 4)) ? 32 : 16);
     static constexpr int NW = KB == 24 ? 6 : 8, NTH = 32 * NW;
     static constexpr int KBS = KB + 4;                     // shared row stride (doubles)
     static constexpr int MT = KB / 8;                      // element tiles
     static constexpr int WPM = NW / MT;                    // warps per element tile
-    static constexpr int QC = (!SW && N == 4) ? 32 : 16;   // quadrature points per chunk
+    // quadrature points per chunk (32 for the strong form at N = 4, 5, so that
+    // the four warps of an element tile each own a point tile)
+    static constexpr int QC = (!SW && N >= 4) ? 32 : 16;
     static constexpr int NCH = cdiv(NQ, QC);               // volume chunks
     static constexpr int NCHU = cdiv(NQU, QC);             // update chunks
     static constexpr int NVA = SW ? 4 : 3;                 // operators of the point GEMM: D_a (and Vq)

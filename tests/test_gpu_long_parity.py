@@ -12,7 +12,7 @@ against the oracle and not against the product.
 * config-3 physics: N = 1..7, Gaussian pulse, 50 steps, 4^3 x 6 tets (3
   tiles), fp32 and fp64;
 * the strong form (the reference default) with the heterogeneous medium at
-  N = 2..4, 50 steps, fp32 and fp64 (fused stages with the sufficiency rules);
+  N = 2..5, 50 steps, fp32 and fp64 (fused stages with the sufficiency rules);
 * the full config-4 mesh (K = 1,572,864): one LSRK stage (a != 0) of the
   tcgen05 kernel checked element by element against the oracle on a sample
   of tets, each with its face neighbours (a stage is local to that patch).
@@ -113,7 +113,7 @@ def test_config3_physics_50_steps(N, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["float32", "float64"])
-@pytest.mark.parametrize("N", [2, 3, 4])
+@pytest.mark.parametrize("N", [2, 3, 4, 5])
 def test_strong_form_50_steps(N, dtype):
     """The reference's default formulation through its fused stages (fp32
     split-TF32 mma.sync, fp64 DMMA), heterogeneous medium."""

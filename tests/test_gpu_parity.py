@@ -390,7 +390,7 @@ def test_wadg_vs_exact_mass_error_ratio_3d():
     assert 0.99 <= ratio <= 1.01
 
 
-@pytest.mark.parametrize("N", [2, 3, 4])
+@pytest.mark.parametrize("N", [2, 3, 4, 5])
 def test_fused_strong_form_stage_fp64(N, rng):
     """The reference's default formulation (Strong, R/pkg/src/wadg/solver.py:70)
     as one fused DMMA stage (fp64, the 4N-3 / 4N-2 sufficiency rules): against
