@@ -157,15 +157,18 @@ int wadg_energy(const wadg_problem *P, const void *Q, double *partials,
  *   info[0] kind: 0 = CUDA-core kernel ([nch][NPP][QC][4], [nch][QC][NPP][4],
  *                 [nch][NPP][QC], [nch][QC][NPP], [Nf*Nfq][NPP]);
  *                 2 = tcgen05 kernel (one buffer of K-major tile images);
- *                 3 = DMMA kernel (one buffer of fragment-order images)
+ *                 3 = DMMA kernel (one buffer of fragment-order images);
+ *                 4 = split-TF32 mma.sync kernel (one buffer of fragment-order
+ *                     hi / lo images)
  *   info[1] elements per CTA, [2] QC, [3] nch, [4] NPP (K extent over nodes),
  *   info[5], [6], [7]: kernel-specific extents (device.py reads them).
  * Returns nonzero if the pair is not compiled / does not fit. */
 int wadg_fused_config(int dtype, int order, int32_t *info, int64_t *smem_bytes);
 
 /* The same for a formulation (WADG_STRONG_WEAK or WADG_STRONG).  The strong
- * form has a fused stage only on the FP64 tensor cores (kind 3, N = 2..5, the
- * sufficiency rules at N_geo = N); other pairs return nonzero. */
+ * form (the sufficiency rules at N_geo = N) has fused stages at N = 2..5: fp64
+ * on the FP64 tensor cores (kind 3), fp32 on split-TF32 mma.sync (kind 4);
+ * other pairs return nonzero. */
 int wadg_fused_config_form(int dtype, int order, int formulation, int32_t *info, int64_t *smem_bytes);
 
 /* Debug: force the fused-stage kernel (0: CUDA-core FMA tiles, 2: split-TF32
@@ -175,7 +178,8 @@ int wadg_fused_config_form(int dtype, int order, int formulation, int32_t *info,
  * wadg_fused_config, so set it before building a problem. */
 int wadg_debug_set_fused_variant(int variant);
 
-/* One whole LSRK stage for strong-weak tetrahedra in a single kernel:
+/* One whole LSRK stage for tetrahedra in a single kernel (strong-weak, or the
+ * strong form where wadg_fused_config_form reports a kernel):
  * Q_out = Q_in + b*res, res = a*res + dt*Minv(volume + surface)(Q_in).
  * Q_in and Q_out must be different buffers (ping-pong).  Blocks are in units
  * of the fused elems_per_block; block_end < 0 means all. */
