@@ -1006,6 +1006,12 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             }
             to_mma(B_Z1);
         }
+        // the first pass's old res values (and w-bar) load while the last U2 MMAs run
+        float rv0[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            rv0[i] = (a_rk != 0.f && i < NP) ? __ldg(res + (size_t)(sub * NP + i) * S + kblk + e) : 0.f;
+        const float wb = P.wbar ? __ldg(P.wbar + (size_t)(sub == 0 ? 1 : 0) * S + kblk + e) : 0.f;
         wait_A();                            // U2 of the last chunk, chain 0
         wait_B();                            // U2 of the last chunk
         UMMA_MARK0(4);
@@ -1014,7 +1020,6 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             const int c = sub;
             // WADG update = wbar R + (tensor-core deviation term in RACC); the
             // pre-update R of pair 0 is in shared memory (hi, lo), of pair 1 in TMEM
-            const float wb = P.wbar ? __ldg(P.wbar + (size_t)(c == 0 ? 1 : 0) * S + kblk + e) : 0.f;
             // 16 nodes per pass: the old res values are all loaded before the first
             // store (one load latency per pass instead of one per node)
 #pragma unroll
@@ -1023,7 +1028,10 @@ k_stage_umma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int j = h0 + i;
-                    rv[i] = (a_rk != 0.f && j < NP) ? __ldg(res + (size_t)(c * NP + j) * S + kblk + e) : 0.f;
+                    if (h0 == 0)
+                        rv[i] = rv0[i];
+                    else
+                        rv[i] = (a_rk != 0.f && j < NP) ? __ldg(res + (size_t)(c * NP + j) * S + kblk + e) : 0.f;
                 }
 #pragma unroll
                 for (int hh = 0; hh < 16; hh += 8) {
