@@ -510,7 +510,9 @@ def main():
     if fused and world == 1 and os.path.exists(tpath):
         with open(tpath) as f:
             nd = json.load(f)
-        traffic = (float(nd["dram__bytes_read.sum"][0]) + float(nd["dram__bytes_write.sum"][0])) * 1e9
+        unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        traffic = sum(float(nd[k][0]) * unit.get(nd[k][1], 1e9)
+                      for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     kernels = {k: {"ms": avg[k], "GB/s": B[k] / (avg[k] * 1e-3) / 1e9,
                    "hbm_frac": B[k] / (avg[k] * 1e-3) / 1e9 / hbm_peak,
                    "TFLOP/s": FL[k] / (avg[k] * 1e-3) / 1e12,
