@@ -56,9 +56,8 @@ struct CfgT {
     static constexpr int NCH = cdiv(NQ, QC), NCHU = cdiv(NQU, QC);
     static constexpr int QT = QC / 8, JT = NPP / 8, FT = NFQP / 8;
     static constexpr int RT = cdiv(JT, WPM);               // R node tiles per warp
-    // point-GEMM units: (point tile, D_a p | Vq u) for strong-weak, (point tile,
-    // field: D_a Q_c) for the strong form
-    static constexpr int NAU = SW ? 2 * QT : 4 * QT;
+    // point-GEMM units of the strong form: (point tile, field c: D_a Q_c)
+    static constexpr int NAU = 4 * QT;
     static constexpr int AU = cdiv(NAU, WPM);
     static constexpr int NVA = SW ? 4 : 3;                 // operators of the point GEMM: D_a (, Vq)
     static constexpr int NVB = SW ? 4 : 1;                 // of the projection: (DTW_a,) -Pq
@@ -366,24 +365,22 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
             }
         }
         if constexpr (!SW) {
-        // strong form: units (point tile, field c), du_a,c = D_a Q_c -> sW rows 3 c + a
-        // (one field per unit measured faster than one field per warp here)
+            // strong form: units (point tile, field c), du_a,c = D_a Q_c -> sW rows
+            // 3 c + a (one field per unit measured faster than one field per warp here)
 #pragma unroll
-        for (int t = 0; t < C::AU; ++t) {
-            const int u = w0 + WPM * t;
-            if (u >= C::NAU) continue;
-            const int qt = u % QT, grp = u / QT;
-            float d[3][4];
+            for (int t = 0; t < C::AU; ++t) {
+                const int u = w0 + WPM * t;
+                if (u >= C::NAU) continue;
+                const int qt = u % QT, c = u / QT;
+                float d[3][4];
 #pragma unroll
-            for (int m = 0; m < 3; ++m)
+                for (int m = 0; m < 3; ++m)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) d[m][i] = 0.f;
-            if (!SW || grp == 0) {
-                const float *xf = sQ + (SW ? 0 : grp) * NPP * KBS;
+                    for (int i = 0; i < 4; ++i) d[m][i] = 0.f;
 #pragma unroll 1
                 for (int ks = 0; ks < NPP / 8; ++ks) {
                     AF x;
-                    afrag<KBS>(x, xf, mt, ks, lane);
+                    afrag<KBS>(x, sQ + c * NPP * KBS, mt, ks, lane);
                     uint4 b[3];
                     float f[3][4];
 #pragma unroll
@@ -397,29 +394,11 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
 #pragma unroll
                     for (int m = 0; m < 3; ++m) add4(d[m], f[m]);
                 }
-            } else {
-#pragma unroll 1
-                for (int ks = 0; ks < NPP / 8; ++ks) {
-                    const uint4 b = bfrag(sVA, (3 * (NPP / 8) + ks) * QT + qt, lane);
-                    AF x[3];
-                    float f[3][4];
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) afrag<KBS>(x[c], sQ + (1 + c) * NPP * KBS, mt, ks, lane);
+                for (int m = 0; m < 3; ++m)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) term1(f[c], x[c], b);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) term2(f[c], x[c], b);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) term3(f[c], x[c], b);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) add4(d[c], f[c]);
-                }
+                    for (int h = 0; h < 2; ++h) st2(sW, (3 * c + m) * QC + 8 * qt + 2 * tl + h, d[m][h], d[m][2 + h]);
             }
-#pragma unroll
-            for (int m = 0; m < 3; ++m)
-#pragma unroll
-                for (int h = 0; h < 2; ++h) st2(sW, (3 * grp + m) * QC + 8 * qt + 2 * tl + h, d[m][h], d[m][2 + h]);
-        }
         }
         __syncthreads();
         // epilogue, one thread per (point, element) pair, in place: gp_i = sum_a G_ai dp_a
