@@ -69,6 +69,9 @@ struct CfgD {
     // tile is shared, fields 0, 1 to the first warp and 2, 3 to the second
     static constexpr bool SPLIT = WPM == 2 && JT % 2 == 1;
     static constexpr int AT = cdiv(QT, WPM);               // point tiles per warp (volume A, update z)
+    // strong-weak point GEMMs split by group (D_a p | Vq u_i) where there are at
+    // least twice as many warps per element tile as point tiles (N = 6, 7)
+    static constexpr bool GSPLIT = SW && WPM >= 2 * QT;
     static constexpr int TT = cdiv(FT, WPM);               // face-point tiles per warp (traces)
     // operator images (doubles): [k step][n tile][32]
     static constexpr int IMG_VA = NVA * (NPP / 4) * QT * 32;   // D_r, D_s, D_t (, Vq) of one chunk
@@ -258,6 +261,53 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
                                    g[2 * 3 + i] * d[t][2][1 + i][h];
                         }
                         sW[(3 * QC + qq) * KBS + e] = div;
+                    }
+                }
+            }
+        } else
+        if constexpr (C::GSPLIT) {
+            // A, one (point tile, group) unit per warp: group 0 dp_a = D_a p -> gp_i,
+            // group 1 U_i = Vq u_i -> F_a (N = 6, 7: 2.x point tiles per four warps)
+            const int qt = w0 % QT, grp = w0 / QT;
+            if (grp < 2) {
+                double G[2][9];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int q = ch * QC + 8 * qt + ec + h;
+#pragma unroll
+                    for (int r = 0; r < 9; ++r) G[h][r] = q < NQ ? __ldg(P.geo + (size_t)(r * NQ + q) * S + kblk + e) : 0.0;
+                }
+                double d[3][2];
+#pragma unroll
+                for (int m = 0; m < 3; ++m) d[m][0] = d[m][1] = 0.0;
+                if (grp == 0) {
+#pragma unroll 2
+                    for (int ks = 0; ks < C::NKS; ++ks) {
+                        const double x = afrag<KBS>(sQ, mt, ks, lane);
+#pragma unroll
+                        for (int m = 0; m < 3; ++m) dmma(d[m], x, sVA[((m * (NPP / 4) + ks) * QT + qt) * 32 + lane]);
+                    }
+                } else {
+#pragma unroll 2
+                    for (int ks = 0; ks < C::NKS; ++ks) {
+                        const double b = sVA[((3 * (NPP / 4) + ks) * QT + qt) * 32 + lane];
+#pragma unroll
+                        for (int i = 0; i < 3; ++i) dmma(d[i], afrag<KBS>(sQ + (1 + i) * NPP * KBS, mt, ks, lane), b);
+                    }
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int qq = 8 * qt + ec + h;
+                    const double *g = G[h];
+                    if (grp == 0) {
+#pragma unroll
+                        for (int i = 0; i < 3; ++i)
+                            sW[(i * QC + qq) * KBS + e] = g[0 * 3 + i] * d[0][h] + g[1 * 3 + i] * d[1][h] + g[2 * 3 + i] * d[2][h];
+                    } else {
+#pragma unroll
+                        for (int a = 0; a < 3; ++a)
+                            sW[((3 + a) * QC + qq) * KBS + e] = g[a * 3 + 0] * d[0][h] + g[a * 3 + 1] * d[1][h] +
+                                                                g[a * 3 + 2] * d[2][h];
                     }
                 }
             }
