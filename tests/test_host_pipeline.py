@@ -239,11 +239,14 @@ def test_device_stepper_routes_stages_through_the_slab_exchange(fused):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["tet_fused_f64", "tet_fused_f32", "tri_split_f64"])
+@pytest.mark.parametrize("case", ["tet_fused_f64", "tet_fused_f32", "tet5_fused_f32", "tri_split_f64"])
 def test_graphed_steps_bitwise_eager(case):
     """DeviceStepper.step_graphed (captured CUDA graph, replayed) gives the
-    eager step's result bit for bit, across the ping-pong buffer alternation."""
-    if case.startswith("tet"):
+    eager step's result bit for bit, across the ping-pong buffer alternation
+    (tcgen05, DMMA, mma.sync tf32 (N = 5) and per-phase kernels)."""
+    if case.startswith("tet5"):
+        mesh, N = meshgen.warped_cube_tet_mesh(3, 5), 5
+    elif case.startswith("tet"):
         mesh, N = meshgen.warped_cube_tet_mesh(3, 3), 3
     else:
         mesh, N = meshgen.warped_triangle_mesh(4, 3), 3
