@@ -48,8 +48,11 @@ struct CfgD {
     static constexpr int NF = 4, FLD = 4;
     // elements per CTA: 24 (three element tiles, six warps) for strong-weak N = 4,
     // so that two CTAs fit per SM (+1.5 %); 32 at N <= 5 otherwise; 16 at N = 6, 7
-    static constexpr int KB = (SW && N == 4) ? 24 : ((N <= 5 && (SW || N <= 4)) ? 32 : 16);
-    static constexpr int NW = KB == 24 ? 6 : 8, NTH = 32 * NW;
+    // 16-element CTAs of four warps, four per SM, at strong-weak N = 2 (+3.7 % over
+    // two 32-element CTAs; level at N = 3)
+    static constexpr bool SMALL = SW && N == 2;
+    static constexpr int KB = SMALL ? 16 : (SW && N == 4) ? 24 : ((N <= 5 && (SW || N <= 4)) ? 32 : 16);
+    static constexpr int NW = KB == 24 ? 6 : (SMALL ? 4 : 8), NTH = 32 * NW;
     static constexpr int KBS = KB + 4;                     // shared row stride (doubles)
     static constexpr int MT = KB / 8;                      // element tiles
     static constexpr int WPM = NW / MT;                    // warps per element tile
@@ -101,7 +104,7 @@ struct CfgD {
     static constexpr size_t SMEM = 16 + SQ + PH;
     // two CTAs per SM where they fit (<= 113 KB of shared memory; registers then
     // capped by the launch bounds): N = 3 12.5 -> 16.8 GDOF/s
-    static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;
+    static constexpr int MINB = (SMALL && SMEM <= 56 * 1024) ? 4 : SMEM <= 113 * 1024 ? 2 : 1;
 };
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
@@ -540,6 +543,13 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
         }
         __syncthreads();
         if (!C::DBLP && f + 1 < NF) gather(f + 1, sP);   // the traces are done with the buffer
+        // L2 prefetch of the next face's factors, loaded before its trace MMAs
+        if (f + 1 < NF)
+            for (int r = tid; r < 4 * NFQ; r += C::NTH) {
+                const double *p = P.fgeo + (size_t)(r / NFQ) * NFQT * S + (size_t)((f + 1) * NFQ + r % NFQ) * S + kblk;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(p + KB - 1));
+            }
         twait(0);
         // lift: R_c += (-Pf_f) g_c
 #pragma unroll 2
@@ -564,6 +574,14 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
     // ======================= WADG update + LSRK ===========================
     WADG_PROF_MARK(3);
     // R -> sR[c][j][e] (the A operand of z = Vu R); accumulators restart at zero
+    // L2 prefetch of this tile's old res rows, read by the LSRK write after the
+    // update (N = 2 / 3 / 4: +1.2 / +0.5 / +2.3 % with the face-factor prefetch)
+    if (a_rk != 0.0)
+        for (int r = tid; r < FLD * NP; r += C::NTH) {
+            const double *p = res + (size_t)r * S + kblk;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p + KB - 1));
+        }
     tma(0, sU1, ops + C::O_U1, C::IMG_U1);
     tma(1, sU2, ops + C::O_U2, C::IMG_U2);
 #pragma unroll

@@ -607,6 +607,13 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
         }
         __syncthreads();
         if (!C::DBLP && f + 1 < NF) gather(f + 1, sP);   // the traces are done with the buffer
+        // L2 prefetches of the next face's factors (loaded before its trace MMAs) and,
+        // below, of the rows the LSRK write reads: N = 6 / 7 +1.5 / +0.8 %, but
+        // N = 5 -5.5 % (two CTAs per SM there already hide the latency)
+        if (N >= 6 && f + 1 < NF)
+            for (int r = tid; r < 4 * NFQ; r += C::NTH)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(P.fgeo + (size_t)(r / NFQ) * NFQT * S +
+                                                            (size_t)((f + 1) * NFQ + r % NFQ) * S + kblk));
         twait(0);
         // lift: R_c += (-Pf_f) g_c
 #pragma unroll 1
@@ -633,6 +640,13 @@ k_stage_tmma(const fused::FProb<float> P, const float *__restrict__ Qin, float *
     WADG_PROF_MARK(3);
     tma(0, sU1, ops + C::O_U1, C::IMG_U1);
     tma(1, sU2, ops + C::O_U2, C::IMG_U2);
+    // L2 prefetch of this tile's Q_in and old res rows, read by the LSRK write
+    if (N >= 6)
+    for (int r = tid; r < 2 * FLD * NP; r += C::NTH) {
+        const float *base = r < FLD * NP ? Qin : res;
+        if (r < FLD * NP || a_rk != 0.f)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)(r % (FLD * NP)) * S + kblk));
+    }
     // R -> sRh / sRl[c][j][pos(e)] (the A operand of z = Vu R, split once);
     // accumulators restart at zero.  sQ is overwritten: the LSRK write re-reads Q_in.
     __syncthreads();
