@@ -502,7 +502,7 @@ def main():
                "lower_bound_ms": {"hbm": t_hbm * 1e3, "compute": t_cmp * 1e3}}
     # measured DRAM traffic per launch from the committed ncu --set full capture
     traffic = None
-    kname = {2: "umma", 3: "dmma", 4: "tmma"}.get(getattr(d, "fused_kind", 0), "fused")
+    kname = {2: "umma", 3: "dmma", 4: "tmma", 5: "n1"}.get(getattr(d, "fused_kind", 0), "fused")
     tname = f"ncu_stage_{kname}_{'f32' if cfg.dtype == 'float32' else 'f64'}_N{N}_{args.config}.json"
     tpath = os.path.join(ROOT, "profiles", "r02_" + tname)
     if not os.path.exists(tpath):
@@ -628,7 +628,8 @@ def main():
             "stage_kernel": "wadg_stage_fused" if fused else "wadg_volume+wadg_surface+wadg_update_lsrk",
             "fused_kernel": ({0: "k_stage_fused (CUDA-core FMA)", 2: "k_stage_umma (tcgen05 split-TF32, TMEM)",
                               3: "k_stage_dmma (FP64 tensor cores, mma.sync m8n8k4)",
-                              4: "k_stage_tmma (split-TF32 mma.sync m16n8k8)"}.get(getattr(d, "fused_kind", -1))
+                              4: "k_stage_tmma (split-TF32 mma.sync m16n8k8)",
+                              5: "k_stage_n1 (N = 1, one element per thread, registers)"}.get(getattr(d, "fused_kind", -1))
                              if fused else None),
             "clocks": clk,
             "storage_words_per_element": {"wadg_weights": 2 * Nqu, "dense_inverse": 2 * Np2,

@@ -87,7 +87,8 @@ typedef struct wadg_problem {
      * wadg_fused_config), NPP = Np rounded up to 4, zero padded:          */
     int32_t order;
     int32_t fused_kind;   /* kernel the operators below are packed for: 0 CUDA cores, 2 tcgen05,
-                           * 3 FP64 DMMA, 4 split-TF32 mma.sync (fp32, N >= 5)           */
+                           * 3 FP64 DMMA, 4 split-TF32 mma.sync (fp32, N >= 5),
+                           * 5 N = 1 thread-per-element registers (opVA: one image)     */
     const void *opVA;     /* D_r, D_s, D_t, Vq at (q, j)   (layout: wadg_fused_config) */
     const void *opVB;     /* DTW_r, DTW_s, DTW_t, Pq at (j, q)                         */
     const void *opU1;     /* Vu                                                        */
@@ -159,7 +160,9 @@ int wadg_energy(const wadg_problem *P, const void *Q, double *partials,
  *                 2 = tcgen05 kernel (one buffer of K-major tile images);
  *                 3 = DMMA kernel (one buffer of fragment-order images);
  *                 4 = split-TF32 mma.sync kernel (one buffer of fragment-order
- *                     hi / lo images)
+ *                     hi / lo images);
+ *                 5 = N = 1 thread-per-element kernel (one 464-value operator
+ *                     image, device.n1_operator_image; no dynamic shared memory)
  *   info[1] elements per CTA, [2] QC, [3] nch, [4] NPP (K extent over nodes),
  *   info[5], [6], [7]: kernel-specific extents (device.py reads them).
  * Returns nonzero if the pair is not compiled / does not fit. */
@@ -173,7 +176,7 @@ int wadg_fused_config_form(int dtype, int order, int formulation, int32_t *info,
 
 /* Debug: force the fused-stage kernel (0: CUDA-core FMA tiles, 2: split-TF32
  * tcgen05 with TMEM accumulators, 3: FP64 DMMA, 4: split-TF32 mma.sync m16n8k8,
- * where available); -1 restores
+ * 5: N = 1 thread-per-element registers, where available); -1 restores
  * the default.  Affects
  * wadg_fused_config, so set it before building a problem. */
 int wadg_debug_set_fused_variant(int variant);

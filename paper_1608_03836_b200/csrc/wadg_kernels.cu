@@ -30,6 +30,7 @@ namespace wadg {
 #include "wadg_fused_umma.cuh"
 #include "wadg_fused_dmma.cuh"
 #include "wadg_fused_tmma.cuh"
+#include "wadg_fused_n1.cuh"
 
 namespace wadg {
 
@@ -808,6 +809,15 @@ static bool use_tmma() {
     return true;
 }
 
+// thread-per-element register stage at N = 1 (strong-weak), both precisions:
+// faster than the tiled CUDA-core kernel there
+template <typename T, int N>
+static bool use_n1() {
+    if constexpr (N != 1) return false;
+    if (g_fused_variant >= 0) return g_fused_variant == 5;
+    return true;
+}
+
 // info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),
 //            quad-chunk row stride, node row stride, padded face points}
 template <typename T, int N>
@@ -864,6 +874,12 @@ static int fused_cfg(int32_t *info, int64_t *smem, int formulation = WADG_STRONG
             sm = C::SMEM;
             done = true;
         }
+    }
+    if (!done && use_n1<T, N>()) {
+        const int32_t w[8] = {5, n1::KB, n1::NQ, 1, n1::NP, n1::NQ, n1::NP, n1::OP_TOTAL};
+        for (int i = 0; i < 8; ++i) v[i] = w[i];
+        sm = 0;
+        done = true;
     }
     if (!done) {
         using C = fused::Cfg<T, N>;
@@ -995,6 +1011,21 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
                 return launch_tmma<N, false>(Pc, Qin, Qout, res, tp, tu, a, b, dt, b0, b1, st);
         }
         return fail("operators packed for the split-TF32 mma.sync stage, which is not compiled for this dtype / order / form");
+    }
+    if (Pc->fused_kind == 5) {
+        if constexpr (N == 1) {
+            if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
+            if (Pc->formulation != WADG_STRONG_WEAK) return fail("the N = 1 register stage is strong-weak only");
+            if (Pc->Kpad % n1::KB) return fail("Kpad must be a multiple of the fused block size");
+            const int nblk = Pc->Kpad / n1::KB;
+            if (b1 < 0 || b1 > nblk) b1 = nblk;
+            if (b0 < 0) b0 = 0;
+            if (b1 <= b0) return 0;
+            n1::k_stage_n1<T><<<b1 - b0, n1::KB, 0, st>>>(make_fprob<T>(*Pc), (const T *)Qin, (T *)Qout, (T *)res,
+                                                           (T)tp, (T)tu, (T)a, (T)b, (T)dt, b0);
+            return check_launch("wadg_stage_fused(n1)");
+        }
+        return fail("operators packed for the N = 1 register stage");
     }
     if (Pc->fused_kind != 0) return fail("unknown fused_kind");
     if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
@@ -1189,8 +1220,8 @@ int wadg_debug_set_phase_clock_buffer(void *buf) {
 }
 
 int wadg_debug_set_fused_variant(int variant) {
-    if (variant != -1 && variant != 0 && variant != 2 && variant != 3 && variant != 4)
-        return fail("variant must be -1, 0, 2, 3 or 4");
+    if (variant != -1 && variant != 0 && variant != 2 && variant != 3 && variant != 4 && variant != 5)
+        return fail("variant must be -1, 0, 2, 3, 4 or 5");
     g_fused_variant = variant;
     return 0;
 }

@@ -191,6 +191,26 @@ def frag_image(B, K, Nn):
     return Bp[kk, nn]
 
 
+def n1_operator_image(ref, ru, DTW):
+    """The 464 reference-operator values of the N = 1 thread-per-element stage
+    (csrc/wadg_fused_n1.cuh, n1::O_* offsets): D_a [a][q][j], Vq [q][j],
+    DTW_a^T [q][a][j], Pq^T [q][j], the own-trace interpolation Vfi applied to
+    the face nodes [f][fq][j], Vfi [fq][i] (16 slots), Pf^T [f][fq][j], and the
+    update rule's Vu [q][j] and Pu^T [q][j]."""
+    nf, nfq, Np = ref.n_faces, ref.nfq, ref.Np
+    Vfi = np.asarray(ref.face_interp)
+    VF = np.zeros((nf, nfq, Np))
+    for f in range(nf):
+        VF[f][:, list(ref.face_nodes[f])] = Vfi
+    vfi16 = np.zeros(16)
+    vfi16[:Vfi.size] = Vfi.ravel()
+    parts = [np.stack(list(ref.Dq)), ref.Vq, np.stack(DTW, axis=0).transpose(2, 0, 1), ref.Pq.T, VF, vfi16,
+             np.asarray(ref.Pfq).T.reshape(nf, nfq, Np), ru.Vq, ru.Pq.T]
+    img = np.concatenate([np.ascontiguousarray(x, dtype=np.float64).ravel() for x in parts])
+    assert img.size == 464, img.size
+    return img
+
+
 def dmma_operator_images(ref, ru, cfg, strong_weak=True):
     """All reference operators of the DMMA fused stage (csrc/wadg_fused_dmma.cuh,
     CfgD offsets), in fragment order: per volume chunk D_r, D_s, D_t (, Vq) (k =
@@ -494,6 +514,16 @@ class DeviceProblem:
             self.fused_kind = 4
             self.struct.order = N
             self.struct.fused_kind = 4
+            return kb
+        if cfg["kind"] == 5:                    # N = 1 thread-per-element kernel: one operator image
+            if self.Kpad % kb:
+                return None
+            self.ops["n1"] = self._t(n1_operator_image(ref, ru, DTW))
+            for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
+                setattr(self.struct, name, self.ops["n1"].data_ptr())
+            self.fused_kind = 5
+            self.struct.order = N
+            self.struct.fused_kind = 5
             return kb
         # CUDA-core kernel layouts (kind 0)
         NPP = roundup(NP, 4)
