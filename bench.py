@@ -629,7 +629,7 @@ def main():
             "fused_kernel": ({0: "k_stage_fused (CUDA-core FMA)", 2: "k_stage_umma (tcgen05 split-TF32, TMEM)",
                               3: "k_stage_dmma (FP64 tensor cores, mma.sync m8n8k4)",
                               4: "k_stage_tmma (split-TF32 mma.sync m16n8k8)",
-                              5: "k_stage_n1 (N = 1, one element per thread, registers)"}.get(getattr(d, "fused_kind", -1))
+                              5: "k_stage_reg (one element per thread, registers)"}.get(getattr(d, "fused_kind", -1))
                              if fused else None),
             "clocks": clk,
             "storage_words_per_element": {"wadg_weights": 2 * Nqu, "dense_inverse": 2 * Np2,

@@ -1,5 +1,6 @@
-// Fused LSRK45 stage for tetrahedra at N = 1, one thread per element, the
-// whole stage in registers.  Same algebra as k_stage_fused (strong-weak
+// Fused LSRK45 stage for tetrahedra at low order (the default at N = 1; N = 2
+// compiles and is parity-tested, but is slower than the tensor-core stages
+// there), one thread per element, the whole stage in registers.  Same algebra as k_stage_fused (strong-weak
 // volume, upwind/penalty surface, WADG update and LSRK axpy of
 // R/pkg/src/wadg/solver.py:207-301, 348-363; one kernel per stage, Q
 // ping-ponged).
@@ -16,26 +17,44 @@
 #pragma once
 
 namespace wadg {
-namespace n1 {
+namespace rk {
 
-constexpr int NP = 4, NQ = 8, NF = 4, NFP = 3, NFQ = 4, NQU = 8, FLD = 4;
+// per-order extents (tetrahedra, strong-weak rules: (N+1)^3 volume and update
+// points, (N+1)^2 points per face) and operator image offsets (values; rows
+// over nodes padded to NPS = rup(Np, 4) so that 4 consecutive operator values
+// are one aligned vector load), device.n1_operator_image
+template <int N>
+struct CfgR {
+    static constexpr int NP = (N + 1) * (N + 2) * (N + 3) / 6, NPS = fused::rup(NP, 4);
+    static constexpr int NQ = (N + 1) * (N + 1) * (N + 1), NQU = NQ;
+    static constexpr int NF = 4, NFP = (N + 1) * (N + 2) / 2, NFPS = fused::rup(NFP, 4), NFQ = (N + 1) * (N + 1);
+    static constexpr int FLD = 4;
+    static constexpr int O_D = 0;                                   // D_a  [a][q][j]
+    static constexpr int O_VQ = O_D + 3 * NQ * NPS;                 // Vq   [q][j]
+    static constexpr int O_DTW = O_VQ + NQ * NPS;                   // DTW_a^T [q][a][j]
+    static constexpr int O_PQ = O_DTW + NQ * 3 * NPS;               // Pq^T [q][j]
+    static constexpr int O_VF = O_PQ + NQ * NPS;                    // own-trace interpolation [f][fq][j]
+    static constexpr int O_VFI = O_VF + NF * NFQ * NPS;             // Vfi  [fq][i]
+    static constexpr int O_L = O_VFI + NFQ * NFPS;                  // Pf^T [f][fq][j]
+    static constexpr int O_VU = O_L + NF * NFQ * NPS;               // Vu   [q][j] (update rule)
+    static constexpr int O_PU = O_VU + NQU * NPS;                   // Pu^T [q][j]
+    static constexpr int OP_TOTAL = O_PU + NQU * NPS;               // 464 at N = 1
+};
 constexpr int KB = 128;                                  // elements (threads) per CTA
-// operator image offsets (values), device.n1_operator_image
-constexpr int O_D = 0;                                   // D_a  [a][q][j]
-constexpr int O_VQ = O_D + 3 * NQ * NP;                  // Vq   [q][j]
-constexpr int O_DTW = O_VQ + NQ * NP;                    // DTW_a^T [q][a][j]
-constexpr int O_PQ = O_DTW + NQ * 3 * NP;                // Pq^T [q][j]
-constexpr int O_VF = O_PQ + NQ * NP;                     // own-trace interpolation [f][fq][j]
-constexpr int O_VFI = O_VF + NF * NFQ * NP;              // Vfi  [fq][i] (16 slots)
-constexpr int O_L = O_VFI + 16;                          // Pf^T [f][fq][j]
-constexpr int O_VU = O_L + NF * NFQ * NP;                // Vu   [q][j] (update rule)
-constexpr int O_PU = O_VU + NQU * NP;                    // Pu^T [q][j]
-constexpr int OP_TOTAL = O_PU + NQU * NP;                // 464
+// registers: fp32 N = 1 128 (four CTAs per SM), fp32 N = 2 and fp64 N = 1 168
+// (three), fp64 N = 2 255 (two)
+template <typename T, int N>
+constexpr int minb() { return N == 1 ? (sizeof(T) == 4 ? 4 : 3) : (sizeof(T) == 4 ? 3 : 2); }
 
-template <typename T>
-__global__ void __launch_bounds__(KB, sizeof(T) == 4 ? 4 : 3)
-k_stage_n1(const fused::FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Qout, T *__restrict__ res,
-           T tau_p, T tau_u, T a_rk, T b_rk, T dt, int block0) {
+template <typename T, int N>
+__global__ void __launch_bounds__(KB, (minb<T, N>()))
+k_stage_reg(const fused::FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Qout, T *__restrict__ res,
+            T tau_p, T tau_u, T a_rk, T b_rk, T dt, int block0) {
+    using C = CfgR<N>;
+    constexpr int NP = C::NP, NPS = C::NPS, NQ = C::NQ, NQU = C::NQU, NF = C::NF, NFP = C::NFP, NFPS = C::NFPS;
+    constexpr int NFQ = C::NFQ, FLD = C::FLD;
+    constexpr int O_D = C::O_D, O_VQ = C::O_VQ, O_DTW = C::O_DTW, O_PQ = C::O_PQ, O_VF = C::O_VF, O_VFI = C::O_VFI;
+    constexpr int O_L = C::O_L, O_VU = C::O_VU, O_PU = C::O_PU, OP_TOTAL = C::OP_TOTAL;
     __shared__ __align__(16) T sOp[OP_TOTAL];
     __shared__ int32_t sExt[NF * 6 * NFP], sPerm[6 * NFP];
     const int tid = threadIdx.x;
@@ -99,14 +118,14 @@ k_stage_n1(const fused::FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Q
 #pragma unroll 1
     for (int qq = 0; qq < NQ; ++qq) {
         if (qq + 1 < NQ) load_G(Gn, qq + 1);
-        const T *D = sOp + O_D + qq * NP, *Vq = sOp + O_VQ + qq * NP;
-        const T *DTW = sOp + O_DTW + qq * 3 * NP, *Pq = sOp + O_PQ + qq * NP;
+        const T *D = sOp + O_D + qq * NPS, *Vq = sOp + O_VQ + qq * NPS;
+        const T *DTW = sOp + O_DTW + qq * 3 * NPS, *Pq = sOp + O_PQ + qq * NPS;
         T dp[3], U[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             T s = T(0);
 #pragma unroll
-            for (int j = 0; j < NP; ++j) s = fma(D[a * NQ * NP + j], q[0][j], s);
+            for (int j = 0; j < NP; ++j) s = fma(D[a * NQ * NPS + j], q[0][j], s);
             dp[a] = s;
         }
 #pragma unroll
@@ -120,7 +139,7 @@ k_stage_n1(const fused::FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Q
         for (int a = 0; a < 3; ++a) {
             const T F = G[a * 3 + 0] * U[0] + G[a * 3 + 1] * U[1] + G[a * 3 + 2] * U[2];
 #pragma unroll
-            for (int j = 0; j < NP; ++j) R[0][j] = fma(DTW[a * NP + j], F, R[0][j]);
+            for (int j = 0; j < NP; ++j) R[0][j] = fma(DTW[a * NPS + j], F, R[0][j]);
         }
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -154,27 +173,25 @@ k_stage_n1(const fused::FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Q
                     v = __ldg(P.halo + ((size_t)(-nb - 2) * FLD + c) * NFP + sPerm[(code % P.nor) * NFP + i]);
                 xp[c][i] = v;
             }
-        T fg[NFQ][4];
-#pragma unroll
-        for (int fq = 0; fq < NFQ; ++fq)
-#pragma unroll
-            for (int d = 0; d < 4; ++d) fg[fq][d] = __ldg(P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + k);
         const bool mirror = nb == -1;
-        const T *VF = sOp + O_VF + f * NFQ * NP, *L = sOp + O_L + f * NFQ * NP;
-#pragma unroll
+        const T *VF = sOp + O_VF + f * NFQ * NPS, *L = sOp + O_L + f * NFQ * NPS;
+#pragma unroll (N == 1 ? NFQ : 1)
         for (int fq = 0; fq < NFQ; ++fq) {
+            T fg[4];
+#pragma unroll
+            for (int d = 0; d < 4; ++d) fg[d] = __ldg(P.fgeo + (size_t)(d * NFQT + f * NFQ + fq) * S + k);
             T m[FLD], x[FLD];
 #pragma unroll
             for (int c = 0; c < FLD; ++c) {
                 T sm = T(0), sx = T(0);
 #pragma unroll
-                for (int j = 0; j < NP; ++j) sm = fma(VF[fq * NP + j], q[c][j], sm);
+                for (int j = 0; j < NP; ++j) sm = fma(VF[fq * NPS + j], q[c][j], sm);
 #pragma unroll
-                for (int i = 0; i < NFP; ++i) sx = fma(sOp[O_VFI + fq * NFP + i], xp[c][i], sx);
+                for (int i = 0; i < NFP; ++i) sx = fma(sOp[O_VFI + fq * NFPS + i], xp[c][i], sx);
                 m[c] = sm;
                 x[c] = mirror ? (c == 0 ? -sm : sm) : sx;
             }
-            const T n0 = fg[fq][0], n1 = fg[fq][1], n2 = fg[fq][2], sJh = fg[fq][3];
+            const T n0 = fg[0], n1 = fg[1], n2 = fg[2], sJh = fg[3];
             const T djp = x[0] - m[0];
             const T dUn = (x[1] - m[1]) * n0 + (x[2] - m[2]) * n1 + (x[3] - m[3]) * n2;
             const T avg = (x[1] + m[1]) * n0 + (x[2] + m[2]) * n1 + (x[3] + m[3]) * n2;
@@ -184,46 +201,81 @@ k_stage_n1(const fused::FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Q
 #pragma unroll
             for (int c = 0; c < FLD; ++c)
 #pragma unroll
-                for (int j = 0; j < NP; ++j) R[c][j] = fma(-L[fq * NP + j], g[c], R[c][j]);
+                for (int j = 0; j < NP; ++j) R[c][j] = fma(-L[fq * NPS + j], g[c], R[c][j]);
         }
     }
 
     // ---- WADG update: R'_c = Pu (omega Vu R_c), omega = c^2/J (p) or 1/J (u)
     // (R/pkg/src/wadg/operators.py:45-61), then the LSRK axpy ----
-    T Rn[FLD][NP];
+    if constexpr (N == 1) {
+        // all fields per point, the next point's weights in flight
+        T Rn[FLD][NP];
 #pragma unroll
-    for (int c = 0; c < FLD; ++c)
+        for (int c = 0; c < FLD; ++c)
 #pragma unroll
-        for (int j = 0; j < NP; ++j) Rn[c][j] = T(0);
-    T wun = __ldg(P.wu + k), wpn = P.wp ? __ldg(P.wp + k) : T(0);
+            for (int j = 0; j < NP; ++j) Rn[c][j] = T(0);
+        T wun = __ldg(P.wu + k), wpn = P.wp ? __ldg(P.wp + k) : T(0);
 #pragma unroll 2
-    for (int qq = 0; qq < NQU; ++qq) {
-        const T wu = wun, wp = P.wp ? wpn : P.c2 * wu;
-        if (qq + 1 < NQU) {
-            wun = __ldg(P.wu + (size_t)(qq + 1) * S + k);
-            if (P.wp) wpn = __ldg(P.wp + (size_t)(qq + 1) * S + k);
+        for (int qq = 0; qq < NQU; ++qq) {
+            const T wu = wun, wp = P.wp ? wpn : P.c2 * wu;
+            if (qq + 1 < NQU) {
+                wun = __ldg(P.wu + (size_t)(qq + 1) * S + k);
+                if (P.wp) wpn = __ldg(P.wp + (size_t)(qq + 1) * S + k);
+            }
+#pragma unroll
+            for (int c = 0; c < FLD; ++c) {
+                T z = T(0);
+#pragma unroll
+                for (int j = 0; j < NP; ++j) z = fma(sOp[O_VU + qq * NPS + j], R[c][j], z);
+                z *= (c == 0 ? wp : wu);
+#pragma unroll
+                for (int j = 0; j < NP; ++j) Rn[c][j] = fma(sOp[O_PU + qq * NPS + j], z, Rn[c][j]);
+            }
         }
 #pragma unroll
-        for (int c = 0; c < FLD; ++c) {
+        for (int c = 0; c < FLD; ++c)
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                const size_t o = (size_t)(c * NP + j) * S + k;
+                const T rold = a_rk != T(0) ? __ldg(res + o) : T(0);
+                const T r = a_rk * rold + dt * Rn[c][j];
+                res[o] = r;
+                Qout[o] = q[c][j] + b_rk * r;
+            }
+    } else {
+    // N = 2, field by field: z = Vu R_c at each point, times the weight,
+    // projected with Pu into R'_c (only one field's R' live), then the field's
+    // LSRK write.  The weight rows are L1 hits after the first field.
+#pragma unroll
+    for (int c = 0; c < FLD; ++c) {
+        const T *wrow = (c == 0 && P.wp) ? P.wp : P.wu;
+        const T wsc = (c == 0 && !P.wp) ? P.c2 : T(1);
+        T Rn[NP];
+#pragma unroll
+        for (int j = 0; j < NP; ++j) Rn[j] = T(0);
+        T wn = __ldg(wrow + k);
+#pragma unroll (N == 1 ? 2 : 1)
+        for (int qq = 0; qq < NQU; ++qq) {
+            const T w = wn * wsc;
+            if (qq + 1 < NQU) wn = __ldg(wrow + (size_t)(qq + 1) * S + k);
             T z = T(0);
 #pragma unroll
-            for (int j = 0; j < NP; ++j) z = fma(sOp[O_VU + qq * NP + j], R[c][j], z);
-            z *= (c == 0 ? wp : wu);
+            for (int j = 0; j < NP; ++j) z = fma(sOp[O_VU + qq * NPS + j], R[c][j], z);
+            z *= w;
 #pragma unroll
-            for (int j = 0; j < NP; ++j) Rn[c][j] = fma(sOp[O_PU + qq * NP + j], z, Rn[c][j]);
+            for (int j = 0; j < NP; ++j) Rn[j] = fma(sOp[O_PU + qq * NPS + j], z, Rn[j]);
         }
-    }
-#pragma unroll
-    for (int c = 0; c < FLD; ++c)
 #pragma unroll
         for (int j = 0; j < NP; ++j) {
             const size_t o = (size_t)(c * NP + j) * S + k;
             const T rold = a_rk != T(0) ? __ldg(res + o) : T(0);
-            const T r = a_rk * rold + dt * Rn[c][j];
+            const T r = a_rk * rold + dt * Rn[j];
             res[o] = r;
             Qout[o] = q[c][j] + b_rk * r;
         }
+    }
+    }
 }
 
-}  // namespace n1
+}  // namespace rk
 }  // namespace wadg

@@ -809,13 +809,14 @@ static bool use_tmma() {
     return true;
 }
 
-// thread-per-element register stage at N = 1 (strong-weak), both precisions:
-// faster than the tiled CUDA-core kernel there
+// thread-per-element register stage (strong-weak, N = 1, 2), both precisions:
+// the default at N = 1, faster than the tiled CUDA-core kernel there
+//
 template <typename T, int N>
-static bool use_n1() {
-    if constexpr (N != 1) return false;
+static bool use_reg() {
+    if constexpr (N > 2) return false;
     if (g_fused_variant >= 0) return g_fused_variant == 5;
-    return true;
+    return N == 1;
 }
 
 // info[8] = {kind, elems_per_block, qchunk, n_chunks, K-extent over nodes (NPP),
@@ -875,8 +876,9 @@ static int fused_cfg(int32_t *info, int64_t *smem, int formulation = WADG_STRONG
             done = true;
         }
     }
-    if (!done && use_n1<T, N>()) {
-        const int32_t w[8] = {5, n1::KB, n1::NQ, 1, n1::NP, n1::NQ, n1::NP, n1::OP_TOTAL};
+    if (!done && use_reg<T, N>()) {
+        using C = rk::CfgR<N>;
+        const int32_t w[8] = {5, rk::KB, C::NQ, 1, C::NPS, C::NFPS, C::NP, C::OP_TOTAL};
         for (int i = 0; i < 8; ++i) v[i] = w[i];
         sm = 0;
         done = true;
@@ -1013,19 +1015,19 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
         return fail("operators packed for the split-TF32 mma.sync stage, which is not compiled for this dtype / order / form");
     }
     if (Pc->fused_kind == 5) {
-        if constexpr (N == 1) {
+        if constexpr (N <= 2) {
             if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
-            if (Pc->formulation != WADG_STRONG_WEAK) return fail("the N = 1 register stage is strong-weak only");
-            if (Pc->Kpad % n1::KB) return fail("Kpad must be a multiple of the fused block size");
-            const int nblk = Pc->Kpad / n1::KB;
+            if (Pc->formulation != WADG_STRONG_WEAK) return fail("the register stage is strong-weak only");
+            if (Pc->Kpad % rk::KB) return fail("Kpad must be a multiple of the fused block size");
+            const int nblk = Pc->Kpad / rk::KB;
             if (b1 < 0 || b1 > nblk) b1 = nblk;
             if (b0 < 0) b0 = 0;
             if (b1 <= b0) return 0;
-            n1::k_stage_n1<T><<<b1 - b0, n1::KB, 0, st>>>(make_fprob<T>(*Pc), (const T *)Qin, (T *)Qout, (T *)res,
-                                                           (T)tp, (T)tu, (T)a, (T)b, (T)dt, b0);
-            return check_launch("wadg_stage_fused(n1)");
+            rk::k_stage_reg<T, N><<<b1 - b0, rk::KB, 0, st>>>(make_fprob<T>(*Pc), (const T *)Qin, (T *)Qout,
+                                                                (T *)res, (T)tp, (T)tu, (T)a, (T)b, (T)dt, b0);
+            return check_launch("wadg_stage_fused(register stage)");
         }
-        return fail("operators packed for the N = 1 register stage");
+        return fail("operators packed for the register stage, which is compiled for N = 1, 2 only");
     }
     if (Pc->fused_kind != 0) return fail("unknown fused_kind");
     if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");

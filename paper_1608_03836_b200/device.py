@@ -191,23 +191,30 @@ def frag_image(B, K, Nn):
     return Bp[kk, nn]
 
 
-def n1_operator_image(ref, ru, DTW):
-    """The 464 reference-operator values of the N = 1 thread-per-element stage
-    (csrc/wadg_fused_n1.cuh, n1::O_* offsets): D_a [a][q][j], Vq [q][j],
-    DTW_a^T [q][a][j], Pq^T [q][j], the own-trace interpolation Vfi applied to
-    the face nodes [f][fq][j], Vfi [fq][i] (16 slots), Pf^T [f][fq][j], and the
-    update rule's Vu [q][j] and Pu^T [q][j]."""
-    nf, nfq, Np = ref.n_faces, ref.nfq, ref.Np
+def n1_operator_image(ref, ru, DTW, total):
+    """The reference-operator values of the thread-per-element register stage
+    (csrc/wadg_fused_n1.cuh, rk::CfgR offsets; 464 at N = 1): D_a [a][q][j],
+    Vq [q][j], DTW_a^T [q][a][j], Pq^T [q][j], the own-trace interpolation Vfi
+    applied to the face nodes [f][fq][j], Vfi [fq][i], Pf^T [f][fq][j], and the
+    update rule's Vu [q][j] and Pu^T [q][j]; node rows padded to rup(Np, 4),
+    face-node rows to rup(Nfp, 4), with zeros."""
+    nf, nfq, Np, nfp = ref.n_faces, ref.nfq, ref.Np, ref.nfp
+    NPS, NFPS = roundup(Np, 4), roundup(nfp, 4)
+
+    def rows(a, width):           # pad the last axis to `width`
+        a = np.asarray(a, dtype=np.float64)
+        out = np.zeros(a.shape[:-1] + (width,))
+        out[..., :a.shape[-1]] = a
+        return out
     Vfi = np.asarray(ref.face_interp)
     VF = np.zeros((nf, nfq, Np))
     for f in range(nf):
         VF[f][:, list(ref.face_nodes[f])] = Vfi
-    vfi16 = np.zeros(16)
-    vfi16[:Vfi.size] = Vfi.ravel()
-    parts = [np.stack(list(ref.Dq)), ref.Vq, np.stack(DTW, axis=0).transpose(2, 0, 1), ref.Pq.T, VF, vfi16,
-             np.asarray(ref.Pfq).T.reshape(nf, nfq, Np), ru.Vq, ru.Pq.T]
-    img = np.concatenate([np.ascontiguousarray(x, dtype=np.float64).ravel() for x in parts])
-    assert img.size == 464, img.size
+    parts = [rows(np.stack(list(ref.Dq)), NPS), rows(ref.Vq, NPS), rows(np.stack(DTW, axis=0).transpose(2, 0, 1), NPS),
+             rows(ref.Pq.T, NPS), rows(VF, NPS), rows(Vfi, NFPS), rows(np.asarray(ref.Pfq).T.reshape(nf, nfq, Np), NPS),
+             rows(ru.Vq, NPS), rows(ru.Pq.T, NPS)]
+    img = np.concatenate([np.ascontiguousarray(x).ravel() for x in parts])
+    assert img.size == total, (img.size, total)
     return img
 
 
@@ -518,7 +525,7 @@ class DeviceProblem:
         if cfg["kind"] == 5:                    # N = 1 thread-per-element kernel: one operator image
             if self.Kpad % kb:
                 return None
-            self.ops["n1"] = self._t(n1_operator_image(ref, ru, DTW))
+            self.ops["n1"] = self._t(n1_operator_image(ref, ru, DTW, cfg["nfq8"]))
             for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
                 setattr(self.struct, name, self.ops["n1"].data_ptr())
             self.fused_kind = 5

@@ -289,13 +289,13 @@ def test_tensor_core_and_cuda_core_fused_kernels_agree(N, rng):
     assert rel(outs[2], ost.fields()) < 1e-5
 
 
+@pytest.mark.parametrize("N", [1, 2])
 @pytest.mark.parametrize("dtype,tol", [("float32", 1e-5), ("float64", 1e-12)])
-def test_n1_register_and_cuda_core_fused_kernels_agree(dtype, tol, rng):
-    """N = 1: the thread-per-element register stage (kind 5, the default) and
-    the CUDA-core tiled one give the same 2 steps to rounding (wall faces,
-    heterogeneous c^2, nonzero penalties), and both match the oracle."""
+def test_register_and_cuda_core_fused_kernels_agree(N, dtype, tol, rng):
+    """N = 1, 2: the thread-per-element register stage (kind 5; the default at
+    N = 1) and the CUDA-core tiled one give the same 2 steps to rounding (wall
+    faces, heterogeneous c^2, nonzero penalties), and both match the oracle."""
     from paper_1608_03836_b200 import _native
-    N = 1
     mesh = meshgen.warped_cube_tet_mesh(5, N)
     c2 = lambda x, y, z: 1.0 + 0.5 * np.sin(np.pi * x) * np.sin(np.pi * y) * np.sin(np.pi * z)
     cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, flux=FluxParams(0.7, 1.3), dtype=dtype)
@@ -312,13 +312,14 @@ def test_n1_register_and_cuda_core_fused_kernels_agree(dtype, tol, rng):
             outs[v] = st.fields()
     finally:
         _native.call("wadg_debug_set_fused_variant", -1)
-    assert solver.Discretization(mesh, cfg, solver.MediumField(c2)).dev.fused_kind == 5   # the default at N = 1
+    if N == 1:
+        assert solver.Discretization(mesh, cfg, solver.MediumField(c2)).dev.fused_kind == 5   # the default
     assert rel(outs[0], outs[5]) < (2e-6 if dtype == "float32" else 1e-13)
     od = O.OracleDiscretization(mesh, N, True, tau_p=0.7, tau_u=1.3, c2=c2)
     ost = O.State(fl[0], fl[1:])
     for _ in range(2):
         ost = O.lsrk_step(ost, 2e-3, lambda y: O.rhs_full(y, od))
-    record_parity(f"N=1 register stage vs oracle {dtype} 2 steps", rel(outs[5], ost.fields()), tol)
+    record_parity(f"register stage vs oracle N={N} {dtype} 2 steps", rel(outs[5], ost.fields()), tol)
     assert rel(outs[5], ost.fields()) < tol
 
 
