@@ -502,7 +502,7 @@ def main():
                "lower_bound_ms": {"hbm": t_hbm * 1e3, "compute": t_cmp * 1e3}}
     # measured DRAM traffic per launch from the committed ncu --set full capture
     traffic = None
-    kname = {2: "umma", 3: "dmma", 4: "tmma", 5: "n1"}.get(getattr(d, "fused_kind", 0), "fused")
+    kname = {2: "umma", 3: "dmma", 4: "tmma", 5: "reg"}.get(getattr(d, "fused_kind", 0), "fused")
     tname = f"ncu_stage_{kname}_{'f32' if cfg.dtype == 'float32' else 'f64'}_N{N}_{args.config}.json"
     tpath = os.path.join(ROOT, "profiles", "r02_" + tname)
     if not os.path.exists(tpath):

@@ -23,9 +23,16 @@ if case == "c5_f32":
     mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(48, 5), SolverConfig(N=5, formulation=Formulation.StrongWeak, dtype="float32"), 1.0, True
 elif case == "split_c4":
     mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(64, 4), SolverConfig(N=4, formulation=Formulation.StrongWeak, dtype="float32"), het, False
-elif case.startswith("c3_f64_N"):           # config-3 mesh, fp64 strong-weak at order N
+elif case.startswith("c3_f64_N") or case.startswith("c3_f32_N"):   # config-3 mesh, strong-weak at order N
     Nc = int(case[len("c3_f64_N"):])
-    mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(32, Nc), SolverConfig(N=Nc, formulation=Formulation.StrongWeak), 1.0, True
+    dt = "float64" if case.startswith("c3_f64") else "float32"
+    mesh, cfg, med, fused = (meshgen.warped_cube_tet_mesh(32, Nc),
+                             SolverConfig(N=Nc, formulation=Formulation.StrongWeak, dtype=dt), 1.0, True)
+elif case.startswith("big_f64_N") or case.startswith("big_f32_N"):  # K = 1.57M mesh, strong-weak at order N
+    Nc = int(case[len("big_f64_N"):])
+    dt = "float64" if case.startswith("big_f64") else "float32"
+    mesh, cfg, med, fused = (meshgen.warped_cube_tet_mesh(64, Nc),
+                             SolverConfig(N=Nc, formulation=Formulation.StrongWeak, dtype=dt), 1.0, True)
 elif case == "strong_f32_N4":
     mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(32, 4), SolverConfig(N=4, formulation=Formulation.Strong, dtype="float32"), 1.0, True
 elif case == "strong_f64_N4":
