@@ -59,7 +59,7 @@ def run_point(mesh, N, dtype, steps, warmup=2):
     e = solver.device_energy(disc, Q)
     return {
         "N": N, "dtype": dtype, "K": K, "Np": Np, "Nq": Nq,
-        "fused_kernel": {0: "cuda-core", 2: "tcgen05 split-tf32", 3: "dmma f64", 4: "mma.sync split-tf32"}[getattr(d, "fused_kind", 0)],
+        "fused_kernel": {0: "cuda-core", 2: "tcgen05 split-tf32", 3: "dmma f64", 4: "mma.sync split-tf32", 5: "register"}[getattr(d, "fused_kind", 0)],
         "ms_per_stage": ms_stage, "GDOF_s": 4 * K * Np / (ms_stage * 1e-3) / 1e9,
         "hbm_GBs": B_F / (ms_stage * 1e-3) / 1e9, "fp_TFLOPs": flops / (ms_stage * 1e-3) / 1e12,
         "energy_finite": bool(np.isfinite(e)),
