@@ -442,19 +442,22 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
     twait(0);
     __syncthreads();
     // exterior face-node values of face f -> buf[c][i][e] (rows NFP..NFPK-1 zero)
+    // NTH is a multiple of KB, so a thread's element is fixed: its neighbour,
+    // orientation code and their table rows are read once per face (with the
+    // weight prefetch below: N = 2 / 3 +3.7 / +2.2 %, N = 4, 5 level)
+    static_assert(C::NTH % KB == 0, "gather assumes whole element rows per thread group");
     auto gather = [&](int f, double *buf) {
-        for (int r = tid; r < FLD * NFPK * KB; r += C::NTH) {
-            const int el = r % KB, rest = r / KB;
+        const int el = tid % KB;
+        const int nb = sNbr[f * KB + el], code = sCode[f * KB + el];
+        const int32_t *ext = sExt + code * NFP;
+#pragma unroll 2
+        for (int rest = tid / KB; rest < FLD * NFPK; rest += C::NTH / KB) {
             const int i = rest % NFPK, c = rest / NFPK;
-            double *dst = buf + (c * NFPK + i) * KBS + el;
+            double *dst = buf + rest * KBS + el;
             if (i >= NFP) {
                 *dst = 0.0;
-                continue;
-            }
-            const int nb = sNbr[f * KB + el];
-            const int code = sCode[f * KB + el];
-            if (nb >= 0) {
-                fused::cp_async_elem(dst, Qin + (size_t)(c * NP + sExt[code * NFP + i]) * S + nb);
+            } else if (nb >= 0) {
+                fused::cp_async_elem(dst, Qin + (size_t)(c * NP + ext[i]) * S + nb);
             } else if (nb == -1) {       // mirror BC (solver.py:214-217): p+ = -p-, u+ = u-
                 const double m = sQ[(c * NPP + sFmask[f * NFP + i]) * KBS + el];
                 *dst = (c == 0) ? -m : m;
@@ -582,6 +585,15 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
             asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(p + KB - 1));
         }
+    // and of the update weights (c^2/J, 1/J), loaded before each chunk's MMAs
+    for (int r = tid; r < 2 * NQU; r += C::NTH) {
+        const double *w = r < NQU ? P.wu : P.wp;
+        if (w) {
+            const double *p = w + (size_t)(r % NQU) * S + kblk;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p + KB - 1));
+        }
+    }
     tma(0, sU1, ops + C::O_U1, C::IMG_U1);
     tma(1, sU2, ops + C::O_U2, C::IMG_U2);
 #pragma unroll
