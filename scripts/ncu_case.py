@@ -37,6 +37,13 @@ elif case == "strong_f32_N4":
     mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(32, 4), SolverConfig(N=4, formulation=Formulation.Strong, dtype="float32"), 1.0, True
 elif case == "strong_f64_N4":
     mesh, cfg, med, fused = meshgen.warped_cube_tet_mesh(32, 4), SolverConfig(N=4, formulation=Formulation.Strong), 1.0, True
+elif case == "c1_2d_big":                    # config-1 physics (2D triangles, fp64 N = 4) on 256^2 x 2 triangles
+    mesh, cfg, med, fused = (meshgen.warped_triangle_mesh(256, 4),
+                             SolverConfig(N=4, formulation=Formulation.StrongWeak), 1.0, False)
+elif case == "exact_c3_N4":                 # ExactCurvedMass comparator (dense M_J^-1), config-3 mesh, fp64 N = 4
+    mesh, cfg, med, fused = (meshgen.warped_cube_tet_mesh(32, 4),
+                             SolverConfig(N=4, formulation=Formulation.StrongWeak,
+                                          mass_mode=solver.MassMode.ExactCurvedMass), 1.0, False)
 else:
     raise SystemExit(f"unknown case {case}")
 disc = solver.Discretization(mesh, cfg, solver.MediumField(med))
