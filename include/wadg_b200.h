@@ -162,7 +162,7 @@ int wadg_energy(const wadg_problem *P, const void *Q, double *partials,
  *                 4 = split-TF32 mma.sync kernel (one buffer of fragment-order
  *                     hi / lo images);
  *                 5 = N = 1 thread-per-element kernel (one 464-value operator
- *                     image, device.n1_operator_image; no dynamic shared memory)
+ *                     image, device.reg_operator_image; no dynamic shared memory)
  *   info[1] elements per CTA, [2] QC, [3] nch, [4] NPP (K extent over nodes),
  *   info[5], [6], [7]: kernel-specific extents (device.py reads them).
  * Returns nonzero if the pair is not compiled / does not fit. */

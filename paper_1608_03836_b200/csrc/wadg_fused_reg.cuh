@@ -12,7 +12,7 @@
 // fields, the exterior face-node values and the right-hand side stay in
 // registers, every per-element array is read once with coalesced loads
 // (element-fastest layout), and the reference operators (464 values,
-// device.n1_operator_image) sit in shared memory, read with warp-uniform
+// device.reg_operator_image) sit in shared memory, read with warp-uniform
 // addresses (broadcast, compile-time offsets).
 #pragma once
 
@@ -22,7 +22,7 @@ namespace rk {
 // per-order extents (tetrahedra, strong-weak rules: (N+1)^3 volume and update
 // points, (N+1)^2 points per face) and operator image offsets (values; rows
 // over nodes padded to NPS = rup(Np, 4) so that 4 consecutive operator values
-// are one aligned vector load), device.n1_operator_image
+// are one aligned vector load), device.reg_operator_image
 template <int N>
 struct CfgR {
     static constexpr int NP = (N + 1) * (N + 2) * (N + 3) / 6, NPS = fused::rup(NP, 4);

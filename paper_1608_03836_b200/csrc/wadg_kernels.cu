@@ -30,7 +30,7 @@ namespace wadg {
 #include "wadg_fused_umma.cuh"
 #include "wadg_fused_dmma.cuh"
 #include "wadg_fused_tmma.cuh"
-#include "wadg_fused_n1.cuh"
+#include "wadg_fused_reg.cuh"
 
 namespace wadg {
 

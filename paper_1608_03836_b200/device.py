@@ -191,9 +191,9 @@ def frag_image(B, K, Nn):
     return Bp[kk, nn]
 
 
-def n1_operator_image(ref, ru, DTW, total):
+def reg_operator_image(ref, ru, DTW, total):
     """The reference-operator values of the thread-per-element register stage
-    (csrc/wadg_fused_n1.cuh, rk::CfgR offsets; 464 at N = 1): D_a [a][q][j],
+    (csrc/wadg_fused_reg.cuh, rk::CfgR offsets; 464 at N = 1): D_a [a][q][j],
     Vq [q][j], DTW_a^T [q][a][j], Pq^T [q][j], the own-trace interpolation Vfi
     applied to the face nodes [f][fq][j], Vfi [fq][i], Pf^T [f][fq][j], and the
     update rule's Vu [q][j] and Pu^T [q][j]; node rows padded to rup(Np, 4),
@@ -525,9 +525,9 @@ class DeviceProblem:
         if cfg["kind"] == 5:                    # N = 1 thread-per-element kernel: one operator image
             if self.Kpad % kb:
                 return None
-            self.ops["n1"] = self._t(n1_operator_image(ref, ru, DTW, cfg["nfq8"]))
+            self.ops["reg"] = self._t(reg_operator_image(ref, ru, DTW, cfg["nfq8"]))
             for name in ("opVA", "opVB", "opU1", "opU2", "liftT"):
-                setattr(self.struct, name, self.ops["n1"].data_ptr())
+                setattr(self.struct, name, self.ops["reg"].data_ptr())
             self.fused_kind = 5
             self.struct.order = N
             self.struct.fused_kind = 5
