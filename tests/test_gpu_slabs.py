@@ -62,11 +62,12 @@ class LoopbackDist:
 
 
 @pytest.mark.parametrize("local", [False, True])
-@pytest.mark.parametrize("dtype,N", [("float32", 3), ("float64", 3), ("float32", 5)])
+@pytest.mark.parametrize("dtype,N", [("float32", 3), ("float64", 3), ("float32", 5), ("float32", 1), ("float64", 1)])
 @pytest.mark.parametrize("fused", [True, False])
 def test_slab_exchange_loopback_is_bitwise_single_domain(dtype, N, fused, local, rng):
     """N = 3: the tcgen05 (fp32) and DMMA (fp64) stages; N = 5 fp32: the
-    split-TF32 mma.sync stage of config 5 (the weak-scaling configuration)."""
+    split-TF32 mma.sync stage of config 5 (the weak-scaling configuration);
+    N = 1: the one-element-per-thread register stage (halo slots read directly)."""
     world, nz = 3, 6
     mesh = meshgen.warped_cube_tet_mesh(4, N, nz=nz, z_range=(-1.0, 2.0))
     cfg = SolverConfig(N=N, formulation=Formulation.StrongWeak, dtype=dtype)
@@ -82,8 +83,8 @@ def test_slab_exchange_loopback_is_bitwise_single_domain(dtype, N, fused, local,
         slabs = [parallel.slab_discretization(mesh, cfg, medium, r, world, nz, dist=dists[r]) for r in range(world)]
     ranges = parallel.slab_ranges(mesh.K, world, nz)
     assert all(len(s.exchange.halo_runs_f if fused else s.exchange.halo_runs) > 0 for s in slabs)
-    if dtype == "float32":
-        kind = 2 if N <= 4 else 4
+    if dtype == "float32" or N == 1:
+        kind = 5 if N == 1 else (2 if N <= 4 else 4)
         assert whole.dev.fused_kind == kind and all(s.dev.fused_kind == kind for s in slabs)
     fl = [rng.standard_normal((mesh.K, whole.ref.Np)) for _ in range(4)]
     Qw = whole.to_device(FieldState.from_fields(fl))
