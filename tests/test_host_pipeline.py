@@ -85,7 +85,7 @@ def test_pipeline_chunks_cover_whole_waves():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("direct", [True, False])
-@pytest.mark.parametrize("dtype,N", [("float32", 4), ("float32", 2), ("float64", 3), ("float32", 5)])
+@pytest.mark.parametrize("dtype,N", [("float32", 4), ("float32", 2), ("float64", 3), ("float32", 5), ("float32", 1)])
 def test_host_pipeline_bitwise_device_stepper(dtype, N, direct):
     mesh = meshgen.warped_cube_tet_mesh(6, N)
     c2 = lambda x, y, z: 1 + 0.5 * np.sin(2 * np.pi * x) * np.cos(2 * np.pi * z)
@@ -239,13 +239,16 @@ def test_device_stepper_routes_stages_through_the_slab_exchange(fused):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["tet_fused_f64", "tet_fused_f32", "tet5_fused_f32", "tri_split_f64"])
+@pytest.mark.parametrize("case", ["tet_fused_f64", "tet_fused_f32", "tet5_fused_f32", "tet1_fused_f64", "tri_split_f64"])
 def test_graphed_steps_bitwise_eager(case):
     """DeviceStepper.step_graphed (captured CUDA graph, replayed) gives the
     eager step's result bit for bit, across the ping-pong buffer alternation
-    (tcgen05, DMMA, mma.sync tf32 (N = 5) and per-phase kernels)."""
+    (tcgen05, DMMA, mma.sync tf32 (N = 5), the N = 1 register stage and
+    per-phase kernels)."""
     if case.startswith("tet5"):
         mesh, N = meshgen.warped_cube_tet_mesh(3, 5), 5
+    elif case.startswith("tet1"):
+        mesh, N = meshgen.warped_cube_tet_mesh(3, 1), 1
     elif case.startswith("tet"):
         mesh, N = meshgen.warped_cube_tet_mesh(3, 3), 3
     else:
