@@ -23,11 +23,19 @@ namespace rk {
 // points, (N+1)^2 points per face) and operator image offsets (values; rows
 // over nodes padded to NPS = rup(Np, 4) so that 4 consecutive operator values
 // are one aligned vector load), device.reg_operator_image
-template <int N>
+// SW: strong-weak form; otherwise the strong form with the sufficiency rules
+// at N_geo = N ((2N-1)^3 volume, (2N)^2 face points; R/PAPER.md:288,294), the
+// update on the 2N+1 rule either way
+template <int N, bool SW = true>
 struct CfgR {
     static constexpr int NP = (N + 1) * (N + 2) * (N + 3) / 6, NPS = fused::rup(NP, 4);
-    static constexpr int NQ = (N + 1) * (N + 1) * (N + 1), NQU = NQ;
-    static constexpr int NF = 4, NFP = (N + 1) * (N + 2) / 2, NFPS = fused::rup(NFP, 4), NFQ = (N + 1) * (N + 1);
+    // strong form: (2N-1)^3 points, but the volume rule is floored at degree 2N
+    // (refelem.build_reference_element), which at N = 1 is the 2^3 rule
+    static constexpr int NQS1 = N == 1 ? 2 : 2 * N - 1;
+    static constexpr int NQ = SW ? (N + 1) * (N + 1) * (N + 1) : NQS1 * NQS1 * NQS1;
+    static constexpr int NQU = (N + 1) * (N + 1) * (N + 1);
+    static constexpr int NF = 4, NFP = (N + 1) * (N + 2) / 2, NFPS = fused::rup(NFP, 4);
+    static constexpr int NFQ = SW ? (N + 1) * (N + 1) : 4 * N * N;
     static constexpr int FLD = 4;
     static constexpr int O_D = 0;                                   // D_a  [a][q][j]
     static constexpr int O_VQ = O_D + 3 * NQ * NPS;                 // Vq   [q][j]
@@ -48,11 +56,11 @@ constexpr int KB = 128;                                  // elements (threads) p
 template <typename T, int N>
 constexpr int minb() { return N == 1 ? (sizeof(T) == 4 ? 4 : 3) : (sizeof(T) == 4 ? 3 : 2); }
 
-template <typename T, int N>
+template <typename T, int N, bool SW = true>
 __global__ void __launch_bounds__(KB, (minb<T, N>()))
 k_stage_reg(const fused::FProb<T> P, const T *__restrict__ Qin, T *__restrict__ Qout, T *__restrict__ res,
             T tau_p, T tau_u, T a_rk, T b_rk, T dt, int block0) {
-    using C = CfgR<N>;
+    using C = CfgR<N, SW>;
     constexpr int NP = C::NP, NPS = C::NPS, NQ = C::NQ, NQU = C::NQU, NF = C::NF, NFP = C::NFP, NFPS = C::NFPS;
     constexpr int NFQ = C::NFQ, FLD = C::FLD;
     constexpr int O_D = C::O_D, O_VQ = C::O_VQ, O_DTW = C::O_DTW, O_PQ = C::O_PQ, O_VF = C::O_VF, O_VFI = C::O_VFI;
@@ -122,32 +130,58 @@ k_stage_reg(const fused::FProb<T> P, const T *__restrict__ Qin, T *__restrict__ 
         if (qq + 1 < NQ) load_G(Gn, qq + 1);
         const T *D = sOp + O_D + qq * NPS, *Vq = sOp + O_VQ + qq * NPS;
         const T *DTW = sOp + O_DTW + qq * 3 * NPS, *Pq = sOp + O_PQ + qq * NPS;
-        T dp[3], U[3];
+        if constexpr (!SW) {
+            // strong form: du_a,c = D_a Q_c; gp_i = sum_a G_ai du_a,0, div =
+            // sum_i sum_a G_ai du_a,i; R_p -= Pq div, R_u_i -= Pq gp_i
+            // (R/pkg/src/wadg/solver.py:259-264)
+            T du[3][FLD];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            T s = T(0);
+            for (int a = 0; a < 3; ++a)
 #pragma unroll
-            for (int j = 0; j < NP; ++j) s = fma(D[a * NQ * NPS + j], q[0][j], s);
-            dp[a] = s;
-        }
+                for (int c = 0; c < FLD; ++c) {
+                    T s = T(0);
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            T s = T(0);
+                    for (int j = 0; j < NP; ++j) s = fma(D[a * NQ * NPS + j], q[c][j], s);
+                    du[a][c] = s;
+                }
+            T div = T(0);
 #pragma unroll
-            for (int j = 0; j < NP; ++j) s = fma(Vq[j], q[1 + i][j], s);
-            U[i] = s;
-        }
+            for (int i = 0; i < 3; ++i) {
+                const T gp = G[0 * 3 + i] * du[0][0] + G[1 * 3 + i] * du[1][0] + G[2 * 3 + i] * du[2][0];
+                div += G[0 * 3 + i] * du[0][1 + i] + G[1 * 3 + i] * du[1][1 + i] + G[2 * 3 + i] * du[2][1 + i];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const T F = G[a * 3 + 0] * U[0] + G[a * 3 + 1] * U[1] + G[a * 3 + 2] * U[2];
+                for (int j = 0; j < NP; ++j) R[1 + i][j] = fma(-Pq[j], gp, R[1 + i][j]);
+            }
 #pragma unroll
-            for (int j = 0; j < NP; ++j) R[0][j] = fma(DTW[a * NPS + j], F, R[0][j]);
-        }
+            for (int j = 0; j < NP; ++j) R[0][j] = fma(-Pq[j], div, R[0][j]);
+        } else {
+            T dp[3], U[3];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const T gp = G[0 * 3 + i] * dp[0] + G[1 * 3 + i] * dp[1] + G[2 * 3 + i] * dp[2];
+            for (int a = 0; a < 3; ++a) {
+                T s = T(0);
 #pragma unroll
-            for (int j = 0; j < NP; ++j) R[1 + i][j] = fma(-Pq[j], gp, R[1 + i][j]);
+                for (int j = 0; j < NP; ++j) s = fma(D[a * NQ * NPS + j], q[0][j], s);
+                dp[a] = s;
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                T s = T(0);
+#pragma unroll
+                for (int j = 0; j < NP; ++j) s = fma(Vq[j], q[1 + i][j], s);
+                U[i] = s;
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const T F = G[a * 3 + 0] * U[0] + G[a * 3 + 1] * U[1] + G[a * 3 + 2] * U[2];
+#pragma unroll
+                for (int j = 0; j < NP; ++j) R[0][j] = fma(DTW[a * NPS + j], F, R[0][j]);
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const T gp = G[0 * 3 + i] * dp[0] + G[1 * 3 + i] * dp[1] + G[2 * 3 + i] * dp[2];
+#pragma unroll
+                for (int j = 0; j < NP; ++j) R[1 + i][j] = fma(-Pq[j], gp, R[1 + i][j]);
+            }
         }
 #pragma unroll
         for (int r = 0; r < 9; ++r) G[r] = Gn[r];
@@ -197,7 +231,7 @@ k_stage_reg(const fused::FProb<T> P, const T *__restrict__ Qin, T *__restrict__ 
             const T djp = x[0] - m[0];
             const T dUn = (x[1] - m[1]) * n0 + (x[2] - m[2]) * n1 + (x[3] - m[3]) * n2;
             const T avg = (x[1] + m[1]) * n0 + (x[2] + m[2]) * n1 + (x[3] + m[3]) * n2;
-            const T fpp = avg - tau_p * djp;
+            const T fpp = (SW ? avg : dUn) - tau_p * djp;   // strong: [u.n] (solver.py:220-232)
             const T fuu = djp - tau_u * dUn;
             const T g[FLD] = {fpp * sJh, fuu * (sJh * n0), fuu * (sJh * n1), fuu * (sJh * n2)};
 #pragma unroll

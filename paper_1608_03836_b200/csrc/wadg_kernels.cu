@@ -812,9 +812,9 @@ static bool use_tmma() {
 // thread-per-element register stage (strong-weak, N = 1, 2), both precisions:
 // the default at N = 1, faster than the tiled CUDA-core kernel there
 //
-template <typename T, int N>
+template <typename T, int N, bool SW = true>
 static bool use_reg() {
-    if constexpr (N > 2) return false;
+    if constexpr (N > 2 || (!SW && N != 1)) return false;
     if (g_fused_variant >= 0) return g_fused_variant == 5;
     return N == 1;
 }
@@ -826,7 +826,16 @@ static int fused_cfg(int32_t *info, int64_t *smem, int formulation = WADG_STRONG
     size_t sm = 0;
     int32_t v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool done = false;
-    if (formulation != WADG_STRONG_WEAK) {   // strong form: the DMMA (fp64) or mma.sync tf32 (fp32) stage
+    if (formulation != WADG_STRONG_WEAK) {   // strong form: the DMMA (fp64) or mma.sync tf32 (fp32) stage,
+                                             // the register stage at N = 1
+        if (use_reg<T, N, false>()) {
+            using C = rk::CfgR<N, false>;
+            const int32_t w[8] = {5, rk::KB, C::NQ, 1, C::NPS, C::NFPS, C::NP, C::OP_TOTAL};
+            if (info)
+                for (int i = 0; i < 8; ++i) info[i] = w[i];
+            if (smem) *smem = 0;
+            return 0;
+        }
         if constexpr (tmma_available<T, N, false>()) {
             if (use_tmma<T, N, false>()) {
                 using C = tk::CfgT<N, false>;
@@ -1017,14 +1026,19 @@ static int fused_launch(const wadg_problem *Pc, const void *Qin, void *Qout, voi
     if (Pc->fused_kind == 5) {
         if constexpr (N <= 2) {
             if (lay) return fail("row-layout fields need the tcgen05 stage (fp32, N = 2..4)");
-            if (Pc->formulation != WADG_STRONG_WEAK) return fail("the register stage is strong-weak only");
             if (Pc->Kpad % rk::KB) return fail("Kpad must be a multiple of the fused block size");
             const int nblk = Pc->Kpad / rk::KB;
             if (b1 < 0 || b1 > nblk) b1 = nblk;
             if (b0 < 0) b0 = 0;
             if (b1 <= b0) return 0;
-            rk::k_stage_reg<T, N><<<b1 - b0, rk::KB, 0, st>>>(make_fprob<T>(*Pc), (const T *)Qin, (T *)Qout,
-                                                                (T *)res, (T)tp, (T)tu, (T)a, (T)b, (T)dt, b0);
+            if (Pc->formulation == WADG_STRONG_WEAK) {
+                rk::k_stage_reg<T, N, true><<<b1 - b0, rk::KB, 0, st>>>(
+                    make_fprob<T>(*Pc), (const T *)Qin, (T *)Qout, (T *)res, (T)tp, (T)tu, (T)a, (T)b, (T)dt, b0);
+            } else {
+                if constexpr (N != 1) return fail("the register stage's strong form is compiled for N = 1 only");
+                rk::k_stage_reg<T, 1, false><<<b1 - b0, rk::KB, 0, st>>>(
+                    make_fprob<T>(*Pc), (const T *)Qin, (T *)Qout, (T *)res, (T)tp, (T)tu, (T)a, (T)b, (T)dt, b0);
+            }
             return check_launch("wadg_stage_fused(register stage)");
         }
         return fail("operators packed for the register stage, which is compiled for N = 1, 2 only");
@@ -1242,8 +1256,9 @@ static int stage_fused(const wadg_problem *P, const void *Qin, void *Qout, void 
                        double a, double b, double dt, int block_begin, int block_end, int lay, void *stream) {
     if (validate(P)) return 1;
     if (P->dim != 3) return fail("fused stage: tetrahedra only");
-    if (P->formulation != WADG_STRONG_WEAK && P->fused_kind != 3 && P->fused_kind != 4)
-        return fail("fused stage: the strong form runs on the DMMA (fp64) or mma.sync tf32 (fp32) stage only");
+    if (P->formulation != WADG_STRONG_WEAK && P->fused_kind != 3 && P->fused_kind != 4 && P->fused_kind != 5)
+        return fail("fused stage: the strong form runs on the DMMA (fp64), mma.sync tf32 (fp32) or N = 1 register "
+                    "stage only");
     if (P->minv_p) return fail("fused stage: WADG mass inverse only (use wadg_stage for ExactCurvedMass)");
     if (!P->opVA || !P->opVB || !P->opU1 || !P->opU2 || !P->liftT) return fail("fused operators not packed");
     if (Qin == Qout) return fail("fused stage needs distinct Q_in / Q_out buffers");

@@ -456,7 +456,8 @@ class DeviceProblem:
         if self.sw and not (ref.Nq == (N + 1) ** 3 and ref.nfq == (N + 1) ** 2):
             return None
         # strong form: the sufficiency rules at N_geo = N, (2N-1)^3 volume and (2N)^2 face points
-        if not self.sw and not (ref.Nq == (2 * N - 1) ** 3 and ref.nfq == (2 * N) ** 2):
+        # (the volume rule floored at degree 2N: 2^3 points at N = 1)
+        if not self.sw and not (ref.Nq == max(2, 2 * N - 1 if N > 1 else 2) ** 3 and ref.nfq == (2 * N) ** 2):
             return None
         code = _native.WADG_F64 if self.dtype == torch.float64 else _native.WADG_F32
         form = _native.WADG_STRONG_WEAK if self.sw else _native.WADG_STRONG

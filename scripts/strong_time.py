@@ -23,6 +23,8 @@ for N in args.orders:
     for form, name in ((Formulation.Strong, "strong"), (Formulation.StrongWeak, "strong-weak")):
         disc = solver.Discretization(mesh, SolverConfig(N=N, formulation=form, dtype=args.dtype))
         for fused in (True, False):
+            if fused and disc.dev.fused is None:      # no fused stage for this (form, N, dtype)
+                continue
             st = solver.DeviceStepper(disc, fused=fused)
             Q = disc.dev.empty_fields().normal_()
             Q[:, :, mesh.K:] = 0
