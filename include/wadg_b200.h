@@ -169,9 +169,10 @@ int wadg_energy(const wadg_problem *P, const void *Q, double *partials,
 int wadg_fused_config(int dtype, int order, int32_t *info, int64_t *smem_bytes);
 
 /* The same for a formulation (WADG_STRONG_WEAK or WADG_STRONG).  The strong
- * form (the sufficiency rules at N_geo = N) has fused stages at N = 2..5: fp64
- * on the FP64 tensor cores (kind 3), fp32 on split-TF32 mma.sync (kind 4);
- * other pairs return nonzero. */
+ * form (the sufficiency rules at N_geo = N) has fused stages at N = 1 (the
+ * register stage, kind 5, both precisions) and N = 2..5: fp64 on the FP64
+ * tensor cores (kind 3), fp32 on split-TF32 mma.sync (kind 4); other pairs
+ * return nonzero. */
 int wadg_fused_config_form(int dtype, int order, int formulation, int32_t *info, int64_t *smem_bytes);
 
 /* Debug: force the fused-stage kernel (0: CUDA-core FMA tiles, 2: split-TF32
