@@ -631,7 +631,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
             for (int t = 0; t < AT; ++t)
 #pragma unroll
                 for (int c = 0; c < FLD; ++c) z[t][c][0] = z[t][c][1] = 0.0;
-#pragma unroll 2
+#pragma unroll (N >= 6 ? 3 : 2)   // z = Vu R: NKS = 21, 30 at N = 6, 7 (+1.7 / +1.3 %)
             for (int ks = 0; ks < C::NKS; ++ks) {
                 double x[FLD];
 #pragma unroll
