@@ -399,7 +399,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
                 }
             }
         } else
-#pragma unroll 2
+#pragma unroll 4   // QC / 4 = 4 k steps: fully unrolled (with the lift and R' loops, +1 to +2.7 % at N = 2..7)
         for (int ks = 0; ks < QC / 4; ++ks) {
             double w[6];
 #pragma unroll
@@ -555,7 +555,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
             }
         twait(0);
         // lift: R_c += (-Pf_f) g_c
-#pragma unroll 2
+#pragma unroll (C::NFKS % 3 == 0 ? 3 : 2)
         for (int ks = 0; ks < C::NFKS; ++ks) {
             double gv[FLD];
 #pragma unroll
@@ -664,7 +664,7 @@ k_stage_dmma(const fused::FProb<double> P, const double *__restrict__ Qin, doubl
         if (ch + 1 < C::NCHU) tma(0, sU1, ops + C::O_U1 + (size_t)(ch + 1) * C::IMG_U1, C::IMG_U1);
         twait(1);
         // R'_c += Pu (omega z_c)
-#pragma unroll 2
+#pragma unroll 4
         for (int ks = 0; ks < QC / 4; ++ks) {
             double wv[FLD];
 #pragma unroll
